@@ -1,0 +1,308 @@
+/*
+ * dsr.h -- C ABI of the B200-native DynaSOAr hot path (libdsr.so).
+ *
+ * DynaSOAr (Springer & Masuhara, arXiv 1810.11765; "P:n" = PAPER.md line n)
+ * is an object allocator with five operations:
+ *   parallel_do<T, &T::f>(args)   run f on every object of T existing at launch
+ *   parallel_new<T>(n, args)      construct n objects; constructor i gets id i
+ *   new(d_allocator) T(args)      device-side allocation
+ *   destroy(d_allocator, p)       device-side deallocation
+ *   device_do<T, &T::f>(args)     sequential for-each inside one thread
+ * Types and methods are fixed at compile time ("The types ... must be
+ * specified at compile time"), so methods and constructors are selected by id
+ * from tables compiled into the library (DSR_M_* / DSR_C_* / DSR_K_* below).
+ *
+ * Conventions for every entry point:
+ *   - returns dsr_status; DSR_ERR_INVALID is returned before any launch when
+ *     an argument is out of range; DSR_ERR_CUDA when a CUDA call fails.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *     stream).  Calls are stream-ordered and asynchronous unless their name
+ *     ends in _sync or they are documented as synchronising.
+ *   - "device pointer" arguments must point into device memory of the
+ *     current device; "host pointer" arguments into host memory.
+ *   - Device-side OOM / retry-budget exhaustion never aborts a kernel: the
+ *     operation yields a null handle and ORs a bit into the heap's sticky
+ *     error word, reported by the next synchronising call (dsr_poll_error,
+ *     *_sync, dsr_check_invariants, dsr_fragmentation, dsr_stats).
+ *   - One host thread per heap; calls on one heap are ordered by one stream.
+ */
+#ifndef DSR_H
+#define DSR_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DSR_OK = 0,
+  DSR_ERR_INVALID = 1,       /* bad argument, detected on the host before launch */
+  DSR_ERR_OOM = 2,           /* device-side: free block bitmap exhausted (reading R-OOM) */
+  DSR_ERR_CUDA = 3,          /* a CUDA runtime call failed */
+  DSR_ERR_RETRY_BUDGET = 4,  /* debug builds: a spin exceeded its bound (P:1146 illegal use) */
+  DSR_ERR_INVARIANT = 5,     /* dsr_check_invariants found violations */
+  DSR_ERR_UNSUPPORTED = 6    /* id not compiled into this library */
+} dsr_status;
+
+/* Object handle ("fake pointer", Fig. 5; Listing 2):
+ *   bits  0-5  slot in block          (mask 0x3F)
+ *   bits  6-49 block index            (mask 0x3FFFFFFFFFFC0; reading R-BID: an index, not an address)
+ *   bits 50-55 block capacity N_T - 1 (mask 0xFC000000000000; reading R-CAP)
+ *   bits 56-63 type id (1-based; 0 = null / free block, reading R-TYPEID)
+ * 0 is the null handle. */
+typedef uint64_t dsr_handle;
+
+#define DSR_MAX_TYPES 8
+#define DSR_MAX_FIELDS 16
+#define DSR_MAX_LEVELS 6
+
+/* One object type: its fields in declaration order (inherited fields first,
+ * P:293).  field_bytes[f] in {1, 2, 4, 8, 16}. */
+typedef struct {
+  uint32_t num_fields;
+  uint32_t field_bytes[DSR_MAX_FIELDS];
+} dsr_type_desc;
+
+/* Heap layout in the caller's device buffer.  All
+ * offsets are bytes from the buffer start.  Computed by dsr_layout_compute. */
+typedef struct {
+  uint32_t ntypes;
+  uint32_t cap[DSR_MAX_TYPES];                     /* N_T = floor(64 size(T_s)/size(T)) */
+  uint32_t col_off[DSR_MAX_TYPES][DSR_MAX_FIELDS]; /* SOA column offsets inside a block */
+  uint32_t block_bytes;                            /* data bytes per block, multiple of 128 */
+  uint64_t M;                                      /* number of blocks */
+  uint32_t nlevels;                                /* levels of each M-bit hierarchical bitmap */
+  uint64_t level_words[8];                         /* u64 containers per level */
+  uint64_t off_data, off_alloc_bm, off_iter_bm, off_type, off_R, off_bitmaps;
+  uint64_t bitmap_words;                           /* u64 words reserved per hierarchical bitmap */
+  uint64_t total_bytes;                            /* bytes of the buffer used (<= heap_bytes) */
+} dsr_layout;
+
+/* dsr_config.flags */
+#define DSR_F_NO_ROTATE   0x1u  /* plain ffs instead of rotated search ("NoShift") */
+#define DSR_F_NO_COALESCE 0x2u  /* one reservation per thread ("NoCoal") */
+#define DSR_F_STATS       0x4u  /* maintain device counters (dsr_stats) */
+#define DSR_F_SPIN_ON_OOM 0x8u  /* paper behaviour: loop forever on OOM */
+
+typedef struct {
+  uint32_t active_retries;   /* r: try_find_set attempts before the slow path (Fig. 11); 0 -> 5 */
+  uint32_t flags;            /* DSR_F_* */
+  uint64_t seed;             /* rotation seed */
+} dsr_config;
+
+typedef struct {
+  uint64_t allocs;           /* successful new */
+  uint64_t frees;            /* successful destroy */
+  uint64_t block_inits;      /* slow-path initialize_block (Alg. 8) */
+  uint64_t block_frees;      /* successful invalidate -> free.set (Alg. 2 l.7-11) */
+  uint64_t rollbacks;        /* type-changed reservations rolled back (Alg. 1 l.14) */
+  uint64_t invalidate_fail;  /* failed / rolled-back invalidations (Alg. 9 l.8) */
+  uint64_t reserve_retries;  /* reservations that lost every selected bit (Alg. 6 loop) */
+  uint64_t oom;              /* OOM events */
+} dsr_counters;
+
+typedef struct dsr_heap dsr_heap;   /* opaque, host side, owned by the library */
+
+/* ---------------------------------------------------------------- layout
+ * Pure host computation of the heap layout for `ntypes` types in a buffer of
+ * heap_bytes (P:286 M equal-size blocks; P:305-313 capacity; column
+ * alignment reading R-LAYOUT).  Errors: ntypes not in [1, 8], a field size
+ * not in {1,2,4,8,16}, a type > 64x the smallest, heap too small. */
+dsr_status dsr_layout_compute(const dsr_type_desc* types, uint32_t ntypes, uint64_t heap_bytes,
+                              dsr_layout* out);
+
+/* ---------------------------------------------------------------- heap
+ * Create a heap in the caller-owned device buffer dev_buf (heap_bytes
+ * bytes, 256-byte aligned, must outlive the heap; e.g. a torch uint8 CUDA
+ * tensor).  Launches the init kernel on `stream`: free = all 1 for bits < M
+ * (P:350), allocated/active = 0, every object bitmap all 1
+ * ("invalidated" == "uninitialized").  cfg may be NULL (defaults).
+ * The returned heap object is owned by the library until dsr_heap_destroy. */
+dsr_status dsr_heap_create(const dsr_type_desc* types, uint32_t ntypes, void* dev_buf, uint64_t heap_bytes,
+                           const dsr_config* cfg, void* stream, dsr_heap** out);
+/* Re-run the init kernel (all objects dropped).  Stream-ordered. */
+dsr_status dsr_heap_reset(dsr_heap* h, void* stream);
+/* Free the host object; never frees dev_buf. */
+dsr_status dsr_heap_destroy(dsr_heap* h);
+/* Copy the layout (host). */
+dsr_status dsr_heap_layout(const dsr_heap* h, dsr_layout* out);
+/* Change r / flags / seed for subsequent launches. */
+dsr_status dsr_heap_configure(dsr_heap* h, const dsr_config* cfg);
+
+/* ---------------------------------------------------------------- operations
+ * parallel_new<T>(n, args): constructor `ctor_id` runs for ids
+ * 0..n-1; objects are allocated with warp-aggregated device new.  args
+ * (args_bytes bytes, host memory) is copied into kernel parameter space; its
+ * struct type is fixed by ctor_id (see the DSR_C_* list). */
+dsr_status dsr_parallel_new(dsr_heap* h, uint32_t type, uint64_t n, uint32_t ctor_id, const void* args,
+                            size_t args_bytes, void* stream);
+
+/* parallel_do<T, method>(args): snapshot the iteration bitmaps
+ * (P:291), compact allocated[T] into the block list R with warp ballots and
+ * prefix sums, then run `method_id` on every object of
+ * T that exists at launch.  Objects created during the pass are not visited.
+ * The method may allocate any type, destroy objects of other types, and
+ * destroy only `this` among T.  No host synchronisation. */
+dsr_status dsr_parallel_do(dsr_heap* h, uint32_t type, uint32_t method_id, const void* args, size_t args_bytes,
+                           void* stream);
+
+/* The two halves of dsr_parallel_do, for callers that time them apart or
+ * reuse one block list R for several passes over a type whose set of blocks
+ * cannot change in between (e.g. a static Cell grid): the prologue builds R
+ * (and the snapshot if `method_id` may allocate); the body runs the method
+ * over the current R.  dsr_parallel_do == prologue + body. */
+dsr_status dsr_doall_prologue(dsr_heap* h, uint32_t type, uint32_t method_id, void* stream);
+dsr_status dsr_doall_body(dsr_heap* h, uint32_t type, uint32_t method_id, const void* args, size_t args_bytes,
+                          void* stream);
+
+/* Launch a compiled user kernel `kernel_id` over n logical threads that may
+ * call device new/destroy -- e.g. the microbenchmark's allocation
+ * kernel or the Linux Scalability kernels.  args as above. */
+dsr_status dsr_launch(dsr_heap* h, uint32_t kernel_id, uint64_t n, const void* args, size_t args_bytes,
+                      void* stream);
+
+/* Number of live objects of `type` = sum over allocated[T] of used slots,
+ * written as one u64 to dev_out (device pointer).  Stream-ordered. */
+dsr_status dsr_live_count(dsr_heap* h, uint32_t type, uint64_t* dev_out, void* stream);
+/* Same, synchronising, into host memory. */
+dsr_status dsr_live_count_sync(dsr_heap* h, uint32_t type, uint64_t* host_out, void* stream);
+
+/* Synchronise `stream`; return and clear the sticky device error
+ * (DSR_ERR_OOM / DSR_ERR_RETRY_BUDGET) or DSR_OK. */
+dsr_status dsr_poll_error(dsr_heap* h, void* stream);
+
+/* Quiescent audit (synchronising): hierarchy consistency of every bitmap
+ * (Definition), free/allocated partition of [0, M), active ⊆
+ * allocated, active iff non-full, block type ids, padding bits
+ * (P:978), no empty allocated block.  *failures_out (host, may be NULL) gets
+ * the number of violations; returns DSR_ERR_INVARIANT if any. */
+dsr_status dsr_check_invariants(dsr_heap* h, void* stream, uint64_t* failures_out);
+
+/* Fragmentation F over all allocated blocks (synchronising), and the
+ * number of allocated blocks per type (host array of ntypes, may be NULL). */
+dsr_status dsr_fragmentation(dsr_heap* h, double* out, uint64_t* blocks_per_type, void* stream);
+
+/* Device counters (synchronising; zero unless DSR_F_STATS). */
+dsr_status dsr_stats(dsr_heap* h, dsr_counters* out, void* stream);
+dsr_status dsr_stats_reset(dsr_heap* h, void* stream);
+
+/* Copy raw heap state to host memory for parity tests (synchronising):
+ * what = 0: alloc_bm[M] (u64); 1: type[M] (u8); 2: words of the free bitmap;
+ * 3: words of allocated[type]; 4: words of active[type]; 5: R[M] (u32) and
+ * the R count.  Bitmap words are level 0 first, then level 1, ...
+ * (layout.level_words).  *used gets the bytes written. */
+dsr_status dsr_copy_state(dsr_heap* h, uint32_t what, uint32_t type, void* host_out, size_t cap, size_t* used,
+                          void* stream);
+
+/* Number of kernels this library launched since load (host counter). */
+uint64_t dsr_kernel_launches(void);
+const char* dsr_status_str(dsr_status s);
+/* Library build string: "sm_100a <git/date>". */
+const char* dsr_build_info(void);
+
+/* ================================================================ ids
+ * Method ids (dsr_parallel_do), constructor ids (dsr_parallel_new) and user
+ * kernel ids (dsr_launch) compiled into this library, with their argument
+ * structs (copied by value).  Device pointers inside args are device memory.
+ */
+
+/* ---- allocator microbenchmark (BASELINE configs[4], SURVEY c.4) ----
+ * types: 0 = A{3 x u32}, 1 = B{4 x u32}, 2 = C{6 x u32} */
+typedef struct { uint64_t seed; uint64_t t0; } dsr_mb_new_args;   /* thread t -> new [A,A,B,C][(t0+t)&3] */
+typedef struct { uint64_t* out3; } dsr_mb_reduce_args;           /* out3[0..2] += (count, sum, xor) */
+enum {
+  DSR_K_MB_NEW = 1,          /* args dsr_mb_new_args; fields k = low32(key(seed,0,MB_FIELD,16t+k)) */
+  DSR_M_MB_REDUCE = 1,       /* args dsr_mb_reduce_args (no allocation: reads the allocation bitmap) */
+  DSR_M_MB_FREE_ODD = 2,     /* args none: destroy(this) if field0 & 1 */
+  DSR_M_MB_FREE_ALL = 3      /* args none: destroy(this) */
+};
+
+/* ---- Linux Scalability ----
+ * one type of 64 B (16 x u32); thread t allocates n objects, stored to
+ * handles[t*n + i]; the free kernel destroys them. */
+typedef struct { uint64_t* handles; uint32_t per_thread; uint32_t type; } dsr_ls_args;
+enum { DSR_K_LS_ALLOC = 2, DSR_K_LS_FREE = 3 };
+
+/* ---- single-thread replay / torture (test kernels) ---- */
+typedef struct {
+  const uint32_t* ops;       /* pairs (op, arg): op 0 = new type arg, op 1 = destroy handle of op #arg */
+  uint64_t nops;
+  uint64_t* handles_out;     /* one per op (0 for destroy) */
+} dsr_replay_args;
+typedef struct {
+  uint64_t seed;
+  uint32_t iters;            /* alloc/free rounds per thread */
+  uint32_t keep;             /* 1: keep the survivors; 0: free everything at the end */
+  uint64_t* ledger;          /* per thread up to 8 live handles at the end (0 = none) */
+  uint64_t* errors;          /* canary mismatches */
+} dsr_torture_args;
+enum { DSR_K_REPLAY = 4, DSR_K_TORTURE = 5 };
+typedef struct { uint64_t* out; uint64_t* count; } dsr_collect_args;   /* out[atomic++] = this */
+enum { DSR_M_COLLECT = 4 };    /* any type: append every visited handle */
+
+/* ---- Game of Life (BASELINE configs[0]/[3], reading R-GOL) ----
+ * types: 0 = Alive{cell u32, is_new u8, action u8}, 1 = Candidate{cell u32, action u8}
+ * cell: device array of W*H handles (0 = empty). */
+typedef struct { uint64_t* cell; uint32_t W, H; const uint8_t* alive0; uint32_t* dump; } dsr_gol_args;
+enum {
+  DSR_K_GOL_INIT_ALIVE = 10,     /* n = W*H; Alive(c) for alive0[c] */
+  DSR_K_GOL_INIT_CAND = 11,      /* n = W*H; Candidate(c) for dead c with >= 1 alive neighbour */
+  DSR_M_GOL_CAND_PREPARE = 10,   /* type 1 */
+  DSR_M_GOL_ALIVE_PREPARE = 11,  /* type 0 */
+  DSR_M_GOL_CAND_UPDATE = 12,    /* type 1 (allocates Alive) */
+  DSR_M_GOL_ALIVE_UPDATE = 13,   /* type 0 (allocates Candidate) */
+  DSR_M_GOL_DUMP = 14            /* any type: dump[cell] = kind | is_new << 8 | action << 16 */
+};
+
+/* ---- Wa-Tor (BASELINE configs[1], reading R-WATOR) ----
+ * types: 0 = Fish{cell, target, egg: u32}, 1 = Shark{cell, target, egg, energy: u32},
+ *        2 = Cell{id u32, agent u64, req[5] u8}
+ * cells: device array of W*H Cell handles (filled by DSR_C_WT_CELL). */
+typedef struct {
+  uint64_t* cells;
+  uint32_t W, H;
+  uint32_t FB, SB, SS;
+  uint64_t seed;
+  uint32_t step;
+  const uint8_t* kind0; const uint32_t* egg0; const uint32_t* energy0;   /* init only */
+  uint32_t* out_kind; uint32_t* out_egg; uint32_t* out_energy;           /* dump only */
+  unsigned long long* counters;   /* [0] fish born, [1] sharks born, [2] eaten, [3] starved */
+} dsr_wator_args;
+enum {
+  DSR_C_WT_CELL = 20,            /* parallel_new<Cell>(W*H): cells[i] = this */
+  DSR_K_WT_INIT_AGENTS = 21,     /* n = W*H: Fish/Shark from kind0/egg0/energy0 */
+  DSR_M_WT_CELL_PREPARE = 20, DSR_M_WT_FISH_PREPARE = 21, DSR_M_WT_CELL_DECIDE_FISH = 22,
+  DSR_M_WT_FISH_UPDATE = 23, DSR_M_WT_SHARK_PREPARE = 24, DSR_M_WT_CELL_DECIDE_SHARK = 25,
+  DSR_M_WT_SHARK_UPDATE = 26, DSR_M_WT_DUMP = 27
+};
+
+/* ---- N-body with collisions (BASELINE configs[2], reading R-NBODY) ----
+ * type 0 = Body{x, y, vx, vy, fx, fy, m: f32; id, target, incoming: u32; merged: u8}
+ * Snapshot S: id-indexed SOA device arrays of length n (sm = 0 for dead ids). */
+typedef struct {
+  float *sx, *sy, *sm, *svx, *svy;    /* snapshot arrays */
+  uint64_t* shandle;                  /* id -> handle */
+  const float *x0, *y0, *vx0, *vy0, *m0;  /* init only */
+  float G, dt, eps, R;
+  uint32_t n;
+  uint32_t id_offset;                 /* first id owned by this rank */
+  float* out;                         /* dump: 6 floats per id (x,y,vx,vy,m,alive) */
+} dsr_nbody_args;
+enum {
+  DSR_C_NB_BODY = 30,            /* parallel_new<Body>(n): body i from x0..m0 */
+  DSR_M_NB_SNAPSHOT = 30,        /* S[id] = (x, y, m, vx, vy), shandle[id] = this */
+  DSR_M_NB_FORCE = 31,           /* compute_force: tiled all-pairs over S (device_do) */
+  DSR_M_NB_MOVE = 32,
+  DSR_M_NB_PREPARE_MERGE = 33,
+  DSR_M_NB_CLAIM = 34,
+  DSR_M_NB_ABSORB = 35,
+  DSR_M_NB_DELETE_MERGED = 36,
+  DSR_M_NB_DUMP = 37,
+  DSR_K_NB_CLEAR_SNAPSHOT = 30   /* n = ids: sm[i] = 0 */
+};
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,7 @@
+// app_gol.cu -- placeholder (filled in later)
+#include "dsr_host.h"
+namespace dsr {
+bool gol_method_info(uint32_t, MethodInfo*) { return false; }
+bool gol_method_launch(uint32_t, const LaunchCtx&, uint32_t, int, const void*) { return false; }
+bool gol_kernel_launch(uint32_t, const LaunchCtx&, uint64_t, const void*, size_t, int*) { return false; }
+}  // namespace dsr

@@ -1,0 +1,265 @@
+// app_microbench.cu -- allocator microbenchmark (BASELINE configs[4], SURVEY
+// c.4), Linux Scalability and the allocator test kernels
+// (single-thread replay, concurrent torture, handle collection).
+#include "dsr_host.h"
+#include "dsr_doall.cuh"
+
+namespace dsr {
+
+__constant__ uint32_t kMbType[4] = {0, 0, 1, 2};   // [A, A, B, C][t & 3]
+
+// ---- phase 1 / 4: user kernel, thread t does new [A,A,B,C][t&3] (device new)
+__global__ void __launch_bounds__(256) k_mb_new(DevHeap h, uint64_t n, dsr_mb_new_args a) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t t = a.t0 + i;
+    const uint32_t T = kMbType[t & 3];
+    const uint64_t hd = dsr_new(h, T);
+    if (hd) {
+      const uint32_t nf = h.types[T].nfields;
+      for (uint32_t k = 0; k < nf; ++k)
+        *field_ptr<uint32_t>(h, T, k, h_bid(hd), h_slot(hd)) = (uint32_t)rng_key(a.seed, 0, 5, t * 16 + k);
+    }
+  }
+}
+
+// ---- phase 2 / 5: field reduction.  Vectorised do-all body: one thread per
+// 4 consecutive slots ("quad") of a block; each field column is read with one
+// 128-bit non-coherent load per quad (16 lanes cover a 64-slot u32 column).
+template <int NF>
+__global__ void __launch_bounds__(256) k_mb_reduce(DevHeap h, uint32_t T, unsigned long long* out3) {
+  const uint32_t r = ld_relaxed_u32((const uint32_t*)&h.ctrl[CTRL_RCOUNT]);
+  const uint32_t Q = h.types[T].cap >> 2;         // caps 64/48/32 are multiples of 4
+  const uint64_t total = (uint64_t)r * Q;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t cols[NF];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) cols[f] = h.types[T].col_off[f];
+  uint64_t cnt = 0, sum = 0;
+  uint32_t x = 0;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const uint32_t bi = (uint32_t)(e / Q);
+    const uint32_t q = (uint32_t)(e - (uint64_t)bi * Q);
+    const uint32_t b = __ldg(h.R + bi);
+    const uint32_t m4 = (uint32_t)(__ldg((const unsigned long long*)h.alloc_bm + b) >> (4 * q)) & 0xFu;
+    if (!m4) continue;
+    const uint8_t* base = h.data + (size_t)b * h.block_bytes + 16u * q;
+    uint4 v[NF];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) v[f] = __ldcs(reinterpret_cast<const uint4*>(base + cols[f]));
+    cnt += __popc(m4);
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      const uint32_t a0 = (m4 & 1) ? v[f].x : 0u, a1 = (m4 & 2) ? v[f].y : 0u;
+      const uint32_t a2 = (m4 & 4) ? v[f].z : 0u, a3 = (m4 & 8) ? v[f].w : 0u;
+      sum += (uint64_t)a0 + a1 + (uint64_t)a2 + a3;
+      x ^= a0 ^ a1 ^ a2 ^ a3;
+    }
+  }
+  // warp then CTA reduction, one atomic per CTA and output
+  __shared__ unsigned long long s_c[8], s_s[8];
+  __shared__ uint32_t s_x[8];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    x ^= __shfl_xor_sync(0xffffffffu, x, o);
+  }
+  const uint32_t wid = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { s_c[wid] = cnt; s_s[wid] = sum; s_x[wid] = x; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long c = 0, s = 0;
+    uint32_t xx = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) { c += s_c[k]; s += s_s[k]; xx ^= s_x[k]; }
+    if (c) {
+      atomicAdd(out3 + 0, c);
+      atomicAdd(out3 + 1, s);
+      atomicXor(out3 + 2, (unsigned long long)xx);
+    }
+  }
+}
+
+// ---- phase 3 / 6: self-deletion methods
+struct MbFreeOdd {
+  struct Args { uint64_t unused; };
+  DSR_NO_ACC
+  static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args&, Acc&) {
+    if (*field_ptr<uint32_t>(h, T, 0, b, s) & 1u) dsr_destroy(h, make_handle(T, h.types[T].cap, b, s));
+  }
+};
+struct MbFreeAll {
+  struct Args { uint64_t unused; };
+  DSR_NO_ACC
+  static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args&, Acc&) {
+    dsr_destroy(h, make_handle(T, h.types[T].cap, b, s));
+  }
+};
+// handle collection (tests): out[atomic++] = this
+struct Collect {
+  typedef dsr_collect_args Args;
+  DSR_NO_ACC
+  static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args& a, Acc&) {
+    const unsigned long long k = atomicAdd((unsigned long long*)a.count, 1ull);
+    a.out[k] = make_handle(T, h.types[T].cap, b, s);
+  }
+};
+
+// ---- Linux Scalability: n allocations per thread, then a free kernel
+__global__ void k_ls_alloc(DevHeap h, uint64_t nthreads, dsr_ls_args a) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nthreads) return;
+  for (uint32_t i = 0; i < a.per_thread; ++i) a.handles[t * a.per_thread + i] = dsr_new(h, a.type);
+}
+__global__ void k_ls_free(DevHeap h, uint64_t nthreads, dsr_ls_args a) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nthreads) return;
+  for (uint32_t i = 0; i < a.per_thread; ++i) dsr_destroy(h, a.handles[t * a.per_thread + i]);
+}
+
+// ---- single-thread replay (parity with the oracle's sequential model)
+__global__ void k_replay(DevHeap h, dsr_replay_args a) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  for (uint64_t i = 0; i < a.nops; ++i) {
+    const uint32_t op = a.ops[2 * i], arg = a.ops[2 * i + 1];
+    if (op == 0) {
+      a.handles_out[i] = dsr_new(h, arg);
+    } else {
+      dsr_destroy(h, a.handles_out[arg]);
+      a.handles_out[i] = 0;
+    }
+  }
+}
+
+// ---- concurrent torture: random new/destroy from divergent lanes with
+// canaries in the first and last field of every object
+__global__ void __launch_bounds__(256) k_torture(DevHeap h, uint64_t nthreads, dsr_torture_args a) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nthreads) return;
+  uint64_t mine[8];
+  uint32_t tag[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) { mine[k] = 0; tag[k] = 0; }
+  uint64_t errs = 0;
+  for (uint32_t it = 0; it < a.iters; ++it) {
+    const uint64_t r = rng_key(a.seed, t, 9, it);
+    const uint32_t k = (uint32_t)(r & 7);
+    uint64_t cur = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) if ((uint32_t)j == k) cur = mine[j];
+    if (cur) {
+      const uint32_t T = h_type(cur);
+      const uint32_t last = h.types[T].nfields - 1;
+      uint32_t want = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) if ((uint32_t)j == k) want = tag[j];
+      if (*field_ptr<uint32_t>(h, cur, 0) != (uint32_t)t || *field_ptr<uint32_t>(h, cur, last) != want) ++errs;
+      dsr_destroy(h, cur);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) if ((uint32_t)j == k) mine[j] = 0;
+    } else {
+      const uint32_t T = (uint32_t)((r >> 8) % h.ntypes);
+      const uint64_t hd = dsr_new(h, T);
+      if (hd) {
+        const uint32_t w = (uint32_t)(r >> 32) | 1u;
+        *field_ptr<uint32_t>(h, hd, 0) = (uint32_t)t;
+        *field_ptr<uint32_t>(h, hd, h.types[T].nfields - 1) = w;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) if ((uint32_t)j == k) { mine[j] = hd; tag[j] = w; }
+      }
+    }
+  }
+  for (int j = 0; j < 8; ++j) {
+    if (mine[j]) {
+      const uint32_t T = h_type(mine[j]);
+      if (*field_ptr<uint32_t>(h, mine[j], 0) != (uint32_t)t ||
+          *field_ptr<uint32_t>(h, mine[j], h.types[T].nfields - 1) != tag[j]) ++errs;
+      if (!a.keep) { dsr_destroy(h, mine[j]); mine[j] = 0; }
+    }
+    if (a.ledger) a.ledger[t * 8 + j] = mine[j];
+  }
+  if (errs && a.errors) atomicAdd((unsigned long long*)a.errors, (unsigned long long)errs);
+}
+
+// ------------------------------------------------------------------ tables
+bool mb_method_info(uint32_t id, MethodInfo* mi) {
+  switch (id) {
+    case DSR_M_MB_REDUCE: *mi = {0, sizeof(dsr_mb_reduce_args)}; return true;
+    case DSR_M_MB_FREE_ODD: *mi = {0, 0}; return true;
+    case DSR_M_MB_FREE_ALL: *mi = {0, 0}; return true;
+    case DSR_M_COLLECT: *mi = {0, sizeof(dsr_collect_args)}; return true;
+  }
+  return false;
+}
+
+bool mb_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot, const void* args) {
+  static const uint64_t zero[2] = {0, 0};
+  switch (id) {
+    case DSR_M_MB_REDUCE: {
+      const dsr_mb_reduce_args* a = (const dsr_mb_reduce_args*)args;
+      const uint32_t nf = c.h.types[T].nfields;
+      unsigned long long* o = (unsigned long long*)a->out3;
+      if (c.h.types[T].cap % 4 != 0) return false;
+      for (uint32_t f = 0; f < nf; ++f)
+        if (c.h.types[T].fsize[f] != 4) return false;
+      switch (nf) {
+        case 1: k_mb_reduce<1><<<c.grid, 256, 0, c.st>>>(c.h, T, o); break;
+        case 2: k_mb_reduce<2><<<c.grid, 256, 0, c.st>>>(c.h, T, o); break;
+        case 3: k_mb_reduce<3><<<c.grid, 256, 0, c.st>>>(c.h, T, o); break;
+        case 4: k_mb_reduce<4><<<c.grid, 256, 0, c.st>>>(c.h, T, o); break;
+        case 6: k_mb_reduce<6><<<c.grid, 256, 0, c.st>>>(c.h, T, o); break;
+        case 8: k_mb_reduce<8><<<c.grid, 256, 0, c.st>>>(c.h, T, o); break;
+        case 16: k_mb_reduce<16><<<c.grid, 256, 0, c.st>>>(c.h, T, o); break;
+        default: return false;
+      }
+      count_launch();
+      return true;
+    }
+    case DSR_M_MB_FREE_ODD: launch_doall<MbFreeOdd>(c, T, snapshot, zero); return true;
+    case DSR_M_MB_FREE_ALL: launch_doall<MbFreeAll>(c, T, snapshot, zero); return true;
+    case DSR_M_COLLECT: launch_doall<Collect>(c, T, snapshot, args); return true;
+  }
+  return false;
+}
+
+bool mb_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* args, size_t bytes, int* ok) {
+  *ok = 1;
+  switch (id) {
+    case DSR_K_MB_NEW: {
+      if (bytes != sizeof(dsr_mb_new_args) || c.h.ntypes < 3) { *ok = 0; return true; }
+      k_mb_new<<<grid_for(c, n), 256, 0, c.st>>>(c.h, n, *(const dsr_mb_new_args*)args);
+      count_launch();
+      return true;
+    }
+    case DSR_K_LS_ALLOC:
+    case DSR_K_LS_FREE: {
+      if (bytes != sizeof(dsr_ls_args)) { *ok = 0; return true; }
+      const dsr_ls_args a = *(const dsr_ls_args*)args;
+      if (a.type >= c.h.ntypes) { *ok = 0; return true; }
+      const int g = (int)((n + 255) / 256);
+      if (id == DSR_K_LS_ALLOC) k_ls_alloc<<<g, 256, 0, c.st>>>(c.h, n, a);
+      else k_ls_free<<<g, 256, 0, c.st>>>(c.h, n, a);
+      count_launch();
+      return true;
+    }
+    case DSR_K_REPLAY: {
+      if (bytes != sizeof(dsr_replay_args)) { *ok = 0; return true; }
+      k_replay<<<1, 1, 0, c.st>>>(c.h, *(const dsr_replay_args*)args);
+      count_launch();
+      return true;
+    }
+    case DSR_K_TORTURE: {
+      if (bytes != sizeof(dsr_torture_args)) { *ok = 0; return true; }
+      for (uint32_t t = 0; t < c.h.ntypes; ++t)
+        for (uint32_t f = 0; f < c.h.types[t].nfields; ++f)
+          if (f == 0 || f == c.h.types[t].nfields - 1)
+            if (c.h.types[t].fsize[f] != 4) { *ok = 0; return true; }
+      k_torture<<<(int)((n + 255) / 256), 256, 0, c.st>>>(c.h, n, *(const dsr_torture_args*)args);
+      count_launch();
+      return true;
+    }
+  }
+  return false;
+}
+
+}  // namespace dsr

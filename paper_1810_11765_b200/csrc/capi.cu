@@ -1,0 +1,546 @@
+// capi.cu -- the C ABI of libdsr.so (include/dsr.h): host layout, heap
+// lifecycle, do-all orchestration, audit / statistics kernels.
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include "dsr_host.h"
+#include "dsr_doall.cuh"
+
+#ifndef DSR_BUILD_INFO
+#define DSR_BUILD_INFO "sm_100a"
+#endif
+
+namespace dsr {
+std::atomic<unsigned long long> g_launches{0};
+}
+using namespace dsr;
+
+struct dsr_heap {
+  dsr_layout L;
+  dsr_type_desc types[DSR_MAX_TYPES];
+  DevHeap dev;
+  int device;
+  int sms;
+};
+
+#define CUDA_TRY(x)                                         \
+  do {                                                      \
+    cudaError_t e_ = (x);                                   \
+    if (e_ != cudaSuccess) {                                \
+      fprintf(stderr, "[dsr] %s: %s\n", #x, cudaGetErrorString(e_)); \
+      return DSR_ERR_CUDA;                                  \
+    }                                                       \
+  } while (0)
+
+static uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+// ---------------------------------------------------------------- layout
+// Reading R-LAYOUT.  Regions, each 256-B aligned:
+// control page (4 KiB) | data M*block_bytes | alloc_bm M*8 | iter_bm M*8 |
+// type M*1 | R M*4 | (1 + 2*ntypes) hierarchical bitmaps of bitmap_words u64.
+static void shape(uint64_t n, uint32_t* nlev, uint64_t* lw, uint64_t* tot) {
+  uint32_t l = 0;
+  uint64_t t = 0;
+  for (;;) {
+    uint64_t w = (n + 63) / 64;
+    if (!w) w = 1;
+    lw[l++] = w;
+    t += w;
+    if (n <= 64) break;
+    n = w;
+  }
+  *nlev = l;
+  *tot = t;
+}
+static uint64_t place(dsr_layout* L, uint64_t M) {
+  uint64_t off = 4096;
+  L->M = M;
+  L->off_data = off;     off = align_up(off + M * L->block_bytes, 256);
+  L->off_alloc_bm = off; off = align_up(off + M * 8, 256);
+  L->off_iter_bm = off;  off = align_up(off + M * 8, 256);
+  L->off_type = off;     off = align_up(off + M, 256);
+  L->off_R = off;        off = align_up(off + M * 4, 256);
+  uint64_t tot = 0;
+  shape(M ? M : 1, &L->nlevels, L->level_words, &tot);
+  L->bitmap_words = align_up(tot, 32);
+  L->off_bitmaps = off;
+  off += (1 + 2 * (uint64_t)L->ntypes) * L->bitmap_words * 8;
+  L->total_bytes = off;
+  return off;
+}
+
+extern "C" dsr_status dsr_layout_compute(const dsr_type_desc* types, uint32_t ntypes, uint64_t heap_bytes,
+                                         dsr_layout* L) {
+  if (!types || !L || ntypes < 1 || ntypes > DSR_MAX_TYPES) return DSR_ERR_INVALID;
+  memset(L, 0, sizeof(*L));
+  L->ntypes = ntypes;
+  uint64_t sz[DSR_MAX_TYPES], smallest = ~0ull;
+  for (uint32_t t = 0; t < ntypes; ++t) {
+    const dsr_type_desc& d = types[t];
+    if (d.num_fields < 1 || d.num_fields > DSR_MAX_FIELDS) return DSR_ERR_INVALID;
+    sz[t] = 0;
+    for (uint32_t f = 0; f < d.num_fields; ++f) {
+      const uint32_t b = d.field_bytes[f];
+      if (b != 1 && b != 2 && b != 4 && b != 8 && b != 16) return DSR_ERR_INVALID;
+      sz[t] += b;
+    }
+    if (sz[t] < smallest) smallest = sz[t];
+  }
+  uint64_t data = 0;
+  for (uint32_t t = 0; t < ntypes; ++t) {
+    const uint64_t cap = (64 * smallest) / sz[t];
+    if (cap == 0) return DSR_ERR_INVALID;                     // > 64x the smallest type
+    L->cap[t] = (uint32_t)cap;
+    uint64_t end = 0;
+    for (uint32_t f = 0; f < types[t].num_fields; ++f) {
+      const uint64_t bytes = cap * types[t].field_bytes[f];
+      uint64_t a = 16;
+      while (a < bytes && a < 128) a <<= 1;                  // min(128, pow2 >= bytes), >= 16
+      const uint64_t off = align_up(end, a);
+      L->col_off[t][f] = (uint32_t)off;
+      end = off + bytes;
+    }
+    if (end > data) data = end;
+  }
+  L->block_bytes = (uint32_t)align_up(data, 128);
+  uint64_t lo = 0, hi = heap_bytes / L->block_bytes + 1;
+  if (hi > 0xFFFFFFFFull) hi = 0xFFFFFFFFull;
+  while (lo < hi) {
+    const uint64_t mid = lo + (hi - lo + 1) / 2;
+    if (place(L, mid) <= heap_bytes) lo = mid; else hi = mid - 1;
+  }
+  if (lo == 0) return DSR_ERR_INVALID;
+  place(L, lo);
+  return DSR_OK;
+}
+
+// ---------------------------------------------------------------- init kernels
+// free bitmap: bits < size_l set on every level, everything else 0
+__global__ void k_init_free(DevBitmap b, uint64_t nbits) {
+  uint64_t size = nbits;
+  for (uint32_t l = 0; l < b.nlevels; ++l) {
+    const uint64_t words = (size + 63) / 64;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+      const uint64_t lo = i * 64;
+      const uint64_t nb = size - lo >= 64 ? 64 : size - lo;
+      b.lvl[l][i] = nb == 64 ? ~0ull : ((1ull << nb) - 1ull);
+    }
+    size = words;
+  }
+}
+
+static dsr_status heap_init(dsr_heap* h, cudaStream_t st) {
+  const dsr_layout& L = h->L;
+  uint8_t* base = h->dev.data - L.off_data;
+  CUDA_TRY(cudaMemsetAsync(base, 0, 4096, st));
+  CUDA_TRY(cudaMemsetAsync(base + L.off_alloc_bm, 0xFF, L.M * 8, st));     // invalidated == uninitialised
+  CUDA_TRY(cudaMemsetAsync(base + L.off_type, 0, L.M, st));
+  CUDA_TRY(cudaMemsetAsync(base + L.off_bitmaps, 0, (1 + 2 * (uint64_t)L.ntypes) * L.bitmap_words * 8, st));
+  k_init_free<<<64, 256, 0, st>>>(h->dev.freebm, L.M);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DSR_OK;
+}
+
+static void fill_bitmap(DevBitmap* b, uint64_t* words, const dsr_layout& L) {
+  uint64_t off = 0;
+  for (uint32_t l = 0; l < DSR_MAX_LEVELS; ++l) b->lvl[l] = nullptr;
+  for (uint32_t l = 0; l < L.nlevels; ++l) {
+    b->lvl[l] = words + off;
+    off += L.level_words[l];
+  }
+  b->nlevels = L.nlevels;
+  b->nbits = L.M;
+}
+
+static void apply_cfg(dsr_heap* h, const dsr_config* cfg) {
+  h->dev.r_attempts = (cfg && cfg->active_retries) ? cfg->active_retries : 5;   // r = 5
+  h->dev.flags = cfg ? cfg->flags : 0u;
+  h->dev.seed = cfg ? cfg->seed : 0x5eedull;
+}
+
+extern "C" dsr_status dsr_heap_create(const dsr_type_desc* types, uint32_t ntypes, void* dev_buf, uint64_t heap_bytes,
+                                      const dsr_config* cfg, void* stream, dsr_heap** out) {
+  if (!out || !dev_buf || ((uintptr_t)dev_buf & 255)) return DSR_ERR_INVALID;
+  *out = nullptr;
+  dsr_layout L;
+  dsr_status s = dsr_layout_compute(types, ntypes, heap_bytes, &L);
+  if (s != DSR_OK) return s;
+  if (L.nlevels > DSR_MAX_LEVELS) return DSR_ERR_INVALID;
+  dsr_heap* h = new (std::nothrow) dsr_heap;
+  if (!h) return DSR_ERR_INVALID;
+  memset(h, 0, sizeof(*h));
+  h->L = L;
+  memcpy(h->types, types, sizeof(dsr_type_desc) * ntypes);
+  if (cudaGetDevice(&h->device) != cudaSuccess ||
+      cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->device) != cudaSuccess) {
+    delete h;
+    return DSR_ERR_CUDA;
+  }
+  uint8_t* base = (uint8_t*)dev_buf;
+  DevHeap& d = h->dev;
+  d.data = base + L.off_data;
+  d.alloc_bm = (uint64_t*)(base + L.off_alloc_bm);
+  d.iter_bm = (uint64_t*)(base + L.off_iter_bm);
+  d.type = base + L.off_type;
+  d.R = (uint32_t*)(base + L.off_R);
+  d.ctrl = (ull*)base;
+  d.M = (uint32_t)L.M;
+  d.block_bytes = L.block_bytes;
+  d.ntypes = ntypes;
+  uint64_t* bm = (uint64_t*)(base + L.off_bitmaps);
+  fill_bitmap(&d.freebm, bm, L);
+  for (uint32_t t = 0; t < ntypes; ++t) {
+    fill_bitmap(&d.allocbm[t], bm + (1 + 2 * t) * L.bitmap_words, L);
+    fill_bitmap(&d.activebm[t], bm + (2 + 2 * t) * L.bitmap_words, L);
+    DevType& ty = d.types[t];
+    ty.cap = L.cap[t];
+    ty.nfields = types[t].num_fields;
+    ty.valid = ty.cap == 64 ? ~0ull : ((1ull << ty.cap) - 1ull);
+    ty.pad = ~ty.valid;
+    for (uint32_t f = 0; f < ty.nfields; ++f) {
+      ty.fsize[f] = types[t].field_bytes[f];
+      ty.col_off[f] = L.col_off[t][f];
+    }
+  }
+  apply_cfg(h, cfg);
+  s = heap_init(h, (cudaStream_t)stream);
+  if (s != DSR_OK) { delete h; return s; }
+  *out = h;
+  return DSR_OK;
+}
+
+extern "C" dsr_status dsr_heap_reset(dsr_heap* h, void* stream) {
+  if (!h) return DSR_ERR_INVALID;
+  return heap_init(h, (cudaStream_t)stream);
+}
+extern "C" dsr_status dsr_heap_destroy(dsr_heap* h) {
+  if (!h) return DSR_ERR_INVALID;
+  delete h;
+  return DSR_OK;
+}
+extern "C" dsr_status dsr_heap_layout(const dsr_heap* h, dsr_layout* out) {
+  if (!h || !out) return DSR_ERR_INVALID;
+  *out = h->L;
+  return DSR_OK;
+}
+extern "C" dsr_status dsr_heap_configure(dsr_heap* h, const dsr_config* cfg) {
+  if (!h) return DSR_ERR_INVALID;
+  apply_cfg(h, cfg);
+  return DSR_OK;
+}
+
+static LaunchCtx ctx(dsr_heap* h, void* stream) {
+  LaunchCtx c;
+  c.h = h->dev;
+  c.st = (cudaStream_t)stream;
+  c.sms = h->sms;
+  c.grid = h->sms * 8;   // 8 x 256 threads = 2048 resident threads per SM
+  return c;
+}
+
+// ---------------------------------------------------------------- operations
+static bool method_info(uint32_t method_id, MethodInfo* mi) {
+  return mb_method_info(method_id, mi) || gol_method_info(method_id, mi) || wt_method_info(method_id, mi) ||
+         nb_method_info(method_id, mi);
+}
+
+extern "C" dsr_status dsr_doall_prologue(dsr_heap* h, uint32_t type, uint32_t method_id, void* stream) {
+  if (!h || type >= h->L.ntypes) return DSR_ERR_INVALID;
+  MethodInfo mi;
+  if (!method_info(method_id, &mi)) return DSR_ERR_UNSUPPORTED;
+  cudaStream_t st = (cudaStream_t)stream;
+  // R := compact(allocated[T]) (+ iteration-bitmap snapshot when the method may allocate)
+  CUDA_TRY(cudaMemsetAsync(&h->dev.ctrl[CTRL_RCOUNT], 0, 8, st));
+  const uint64_t nwords = (h->L.M + 63) / 64;
+  k_compact<<<(int)((nwords + kCompactThreads - 1) / kCompactThreads), kCompactThreads, 0, st>>>(h->dev, type,
+                                                                                                  mi.allocates);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DSR_OK;
+}
+
+extern "C" dsr_status dsr_doall_body(dsr_heap* h, uint32_t type, uint32_t method_id, const void* args,
+                                     size_t args_bytes, void* stream) {
+  if (!h || type >= h->L.ntypes) return DSR_ERR_INVALID;
+  MethodInfo mi;
+  if (!method_info(method_id, &mi)) return DSR_ERR_UNSUPPORTED;
+  if (mi.args_bytes && (args_bytes != mi.args_bytes || !args)) return DSR_ERR_INVALID;
+  static const uint64_t zero_args[16] = {0};
+  if (!mi.args_bytes) args = zero_args;
+  LaunchCtx c = ctx(h, stream);
+  bool ok = mb_method_launch(method_id, c, type, mi.allocates, args) ||
+            gol_method_launch(method_id, c, type, mi.allocates, args) ||
+            wt_method_launch(method_id, c, type, mi.allocates, args) ||
+            nb_method_launch(method_id, c, type, mi.allocates, args);
+  if (!ok) return DSR_ERR_INVALID;
+  CUDA_TRY(cudaGetLastError());
+  return DSR_OK;
+}
+
+extern "C" dsr_status dsr_parallel_do(dsr_heap* h, uint32_t type, uint32_t method_id, const void* args,
+                                      size_t args_bytes, void* stream) {
+  MethodInfo mi;
+  if (!h || type >= h->L.ntypes) return DSR_ERR_INVALID;
+  if (!method_info(method_id, &mi)) return DSR_ERR_UNSUPPORTED;
+  if (mi.args_bytes && (args_bytes != mi.args_bytes || !args)) return DSR_ERR_INVALID;
+  dsr_status s = dsr_doall_prologue(h, type, method_id, stream);
+  if (s != DSR_OK) return s;
+  return dsr_doall_body(h, type, method_id, args, args_bytes, stream);
+}
+
+extern "C" dsr_status dsr_parallel_new(dsr_heap* h, uint32_t type, uint64_t n, uint32_t ctor_id, const void* args,
+                                       size_t args_bytes, void* stream) {
+  if (!h || type >= h->L.ntypes) return DSR_ERR_INVALID;
+  if (n == 0) return DSR_OK;
+  LaunchCtx c = ctx(h, stream);
+  int ok = 1;
+  bool known = wt_ctor_launch(ctor_id, c, type, n, args, args_bytes, &ok) ||
+               nb_ctor_launch(ctor_id, c, type, n, args, args_bytes, &ok);
+  if (!known) return DSR_ERR_UNSUPPORTED;
+  if (!ok) return DSR_ERR_INVALID;
+  CUDA_TRY(cudaGetLastError());
+  return DSR_OK;
+}
+
+extern "C" dsr_status dsr_launch(dsr_heap* h, uint32_t kernel_id, uint64_t n, const void* args, size_t args_bytes,
+                                 void* stream) {
+  if (!h || !args) return DSR_ERR_INVALID;
+  if (n == 0) return DSR_OK;
+  LaunchCtx c = ctx(h, stream);
+  int ok = 1;
+  bool known = mb_kernel_launch(kernel_id, c, n, args, args_bytes, &ok) ||
+               gol_kernel_launch(kernel_id, c, n, args, args_bytes, &ok) ||
+               wt_kernel_launch(kernel_id, c, n, args, args_bytes, &ok) ||
+               nb_kernel_launch(kernel_id, c, n, args, args_bytes, &ok);
+  if (!known) return DSR_ERR_UNSUPPORTED;
+  if (!ok) return DSR_ERR_INVALID;
+  CUDA_TRY(cudaGetLastError());
+  return DSR_OK;
+}
+
+// ---------------------------------------------------------------- live count / stats
+__global__ void k_live(DevHeap h, uint32_t T, unsigned long long* out) {
+  const DevBitmap& ab = h.allocbm[T];
+  const uint64_t nwords = ((uint64_t)h.M + 63) / 64;
+  unsigned long long acc = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nwords; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t w = ab.lvl[0][i];
+    while (w) {
+      const uint32_t b = (uint32_t)(i * 64 + __ffsll((long long)w) - 1);
+      w &= w - 1;
+      acc += __popcll(h.alloc_bm[b] & h.types[T].valid);
+    }
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+extern "C" dsr_status dsr_live_count(dsr_heap* h, uint32_t type, uint64_t* dev_out, void* stream) {
+  if (!h || !dev_out || type >= h->L.ntypes) return DSR_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemsetAsync(dev_out, 0, 8, st));
+  k_live<<<h->sms * 4, 256, 0, st>>>(h->dev, type, (unsigned long long*)dev_out);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DSR_OK;
+}
+
+extern "C" dsr_status dsr_live_count_sync(dsr_heap* h, uint32_t type, uint64_t* host_out, void* stream) {
+  if (!h || !host_out || type >= h->L.ntypes) return DSR_ERR_INVALID;
+  uint64_t* scratch = (uint64_t*)&h->dev.ctrl[CTRL_SCRATCH];
+  dsr_status s = dsr_live_count(h, type, scratch, stream);
+  if (s != DSR_OK) return s;
+  CUDA_TRY(cudaMemcpyAsync(host_out, scratch, 8, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  return DSR_OK;
+}
+
+extern "C" dsr_status dsr_poll_error(dsr_heap* h, void* stream) {
+  if (!h) return DSR_ERR_INVALID;
+  unsigned long long e = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemcpyAsync(&e, &h->dev.ctrl[CTRL_ERR], 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemsetAsync(&h->dev.ctrl[CTRL_ERR], 0, 8, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (e & ERRB_OOM) return DSR_ERR_OOM;
+  if (e & ERRB_BUDGET) return DSR_ERR_RETRY_BUDGET;
+  return DSR_OK;
+}
+
+// ---------------------------------------------------------------- quiescent audit
+__device__ __forceinline__ bool bget(const DevBitmap& b, uint64_t pos) { return (b.lvl[0][pos >> 6] >> (pos & 63)) & 1; }
+
+__global__ void k_audit_blocks(DevHeap h, unsigned long long* fails) {
+  unsigned long long bad = 0;
+  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < h.M; b += (uint64_t)gridDim.x * blockDim.x) {
+    const bool fr = bget(h.freebm, b);
+    int owners = fr ? 1 : 0;
+    const uint64_t w = h.alloc_bm[b];
+    for (uint32_t t = 0; t < h.ntypes; ++t) {
+      const bool al = bget(h.allocbm[t], b), ac = bget(h.activebm[t], b);
+      if (ac && !al) ++bad;                                   // active ⊆ allocated
+      if (!al) continue;
+      ++owners;
+      const DevType& ty = h.types[t];
+      if (h.type[b] != t + 1) ++bad;                          // block type id
+      if ((w | ty.valid) != ~0ull) ++bad;                     // padding bits set
+      if ((w & ty.valid) == 0) ++bad;                         // allocated blocks are non-empty
+      if (ac != (w != ~0ull)) ++bad;                          // active iff non-full
+    }
+    if (owners != 1) ++bad;                                   // free ⊎ allocated[.] partition [0, M)
+    if (fr && w != ~0ull) ++bad;                              // free blocks are invalidated
+  }
+  if (bad) atomicAdd(fails, bad);
+}
+
+// hierarchy consistency b^{l+1}_i = OR(C^l_i) (Def. P:1115) and no bit >= size
+__global__ void k_audit_bitmap(DevBitmap b, unsigned long long* fails) {
+  unsigned long long bad = 0;
+  uint64_t size = b.nbits;
+  for (uint32_t l = 0; l < b.nlevels; ++l) {
+    const uint64_t words = (size + 63) / 64;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (uint64_t)gridDim.x * blockDim.x) {
+      const uint64_t w = b.lvl[l][i];
+      const uint64_t lo = i * 64;
+      const uint64_t nb = size - lo >= 64 ? 64 : size - lo;
+      if (nb < 64 && (w >> nb)) ++bad;
+      if (l + 1 < b.nlevels) {
+        const bool up = (b.lvl[l + 1][i >> 6] >> (i & 63)) & 1;
+        if (up != (w != 0)) ++bad;
+      }
+    }
+    size = words;
+  }
+  if (bad) atomicAdd(fails, bad);
+}
+
+extern "C" dsr_status dsr_check_invariants(dsr_heap* h, void* stream, uint64_t* failures_out) {
+  if (!h) return DSR_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* f = &h->dev.ctrl[CTRL_AUDIT];
+  CUDA_TRY(cudaMemsetAsync(f, 0, 8, st));
+  k_audit_blocks<<<h->sms * 4, 256, 0, st>>>(h->dev, f);
+  k_audit_bitmap<<<h->sms, 256, 0, st>>>(h->dev.freebm, f);
+  count_launch(2);
+  for (uint32_t t = 0; t < h->L.ntypes; ++t) {
+    k_audit_bitmap<<<h->sms, 256, 0, st>>>(h->dev.allocbm[t], f);
+    k_audit_bitmap<<<h->sms, 256, 0, st>>>(h->dev.activebm[t], f);
+    count_launch(2);
+  }
+  unsigned long long hf = 0;
+  CUDA_TRY(cudaMemcpyAsync(&hf, f, 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (failures_out) *failures_out = hf;
+  return hf ? DSR_ERR_INVARIANT : DSR_OK;
+}
+
+// ---------------------------------------------------------------- fragmentation
+__global__ void k_frag(DevHeap h, unsigned long long* acc /* [t*3 + {used, slots, blocks}] */) {
+  for (uint32_t t = 0; t < h.ntypes; ++t) {
+    const uint64_t nwords = ((uint64_t)h.M + 63) / 64;
+    unsigned long long used = 0, blocks = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nwords; i += (uint64_t)gridDim.x * blockDim.x) {
+      uint64_t w = h.allocbm[t].lvl[0][i];
+      while (w) {
+        const uint32_t b = (uint32_t)(i * 64 + __ffsll((long long)w) - 1);
+        w &= w - 1;
+        used += __popcll(h.alloc_bm[b] & h.types[t].valid);
+        ++blocks;
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      used += __shfl_xor_sync(0xffffffffu, used, o);
+      blocks += __shfl_xor_sync(0xffffffffu, blocks, o);
+    }
+    if ((threadIdx.x & 31) == 0 && blocks) {
+      atomicAdd(acc + 3 * t + 0, used);
+      atomicAdd(acc + 3 * t + 2, blocks);
+    }
+  }
+}
+
+extern "C" dsr_status dsr_fragmentation(dsr_heap* h, double* out, uint64_t* blocks_per_type, void* stream) {
+  if (!h || !out) return DSR_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* acc = &h->dev.ctrl[CTRL_AUDIT + 1];
+  CUDA_TRY(cudaMemsetAsync(acc, 0, 8 * 3 * DSR_MAX_TYPES, st));
+  k_frag<<<h->sms * 4, 256, 0, st>>>(h->dev, acc);
+  count_launch();
+  unsigned long long hv[3 * DSR_MAX_TYPES];
+  CUDA_TRY(cudaMemcpyAsync(hv, acc, sizeof(hv), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  double unused = 0, slots = 0;
+  for (uint32_t t = 0; t < h->L.ntypes; ++t) {
+    const double s = (double)hv[3 * t + 2] * h->L.cap[t];
+    slots += s;
+    unused += s - (double)hv[3 * t];
+    if (blocks_per_type) blocks_per_type[t] = hv[3 * t + 2];
+  }
+  *out = slots > 0 ? unused / slots : 0.0;     // 0 without blocks (reading C36)
+  return DSR_OK;
+}
+
+extern "C" dsr_status dsr_stats(dsr_heap* h, dsr_counters* out, void* stream) {
+  if (!h || !out) return DSR_ERR_INVALID;
+  unsigned long long v[ST_N];
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemcpyAsync(v, &h->dev.ctrl[CTRL_STATS], sizeof(v), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  out->allocs = v[ST_ALLOCS];
+  out->frees = v[ST_FREES];
+  out->block_inits = v[ST_INITS];
+  out->block_frees = v[ST_BFREES];
+  out->rollbacks = v[ST_ROLLBACKS];
+  out->invalidate_fail = v[ST_INVFAIL];
+  out->reserve_retries = v[ST_RESRETRY];
+  out->oom = v[ST_OOM];
+  return DSR_OK;
+}
+extern "C" dsr_status dsr_stats_reset(dsr_heap* h, void* stream) {
+  if (!h) return DSR_ERR_INVALID;
+  CUDA_TRY(cudaMemsetAsync(&h->dev.ctrl[CTRL_STATS], 0, 8 * ST_N, (cudaStream_t)stream));
+  return DSR_OK;
+}
+
+extern "C" dsr_status dsr_copy_state(dsr_heap* h, uint32_t what, uint32_t type, void* host_out, size_t cap,
+                                     size_t* used, void* stream) {
+  if (!h || !host_out) return DSR_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  const void* src = nullptr;
+  size_t n = 0;
+  uint64_t lw = 0;
+  for (uint32_t l = 0; l < h->L.nlevels; ++l) lw += h->L.level_words[l];
+  switch (what) {
+    case 0: src = h->dev.alloc_bm; n = h->L.M * 8; break;
+    case 1: src = h->dev.type; n = h->L.M; break;
+    case 2: src = h->dev.freebm.lvl[0]; n = lw * 8; break;
+    case 3: if (type >= h->L.ntypes) return DSR_ERR_INVALID; src = h->dev.allocbm[type].lvl[0]; n = lw * 8; break;
+    case 4: if (type >= h->L.ntypes) return DSR_ERR_INVALID; src = h->dev.activebm[type].lvl[0]; n = lw * 8; break;
+    case 5: src = h->dev.R; n = h->L.M * 4; break;
+    default: return DSR_ERR_INVALID;
+  }
+  if (cap < n + (what == 5 ? 8 : 0)) return DSR_ERR_INVALID;
+  CUDA_TRY(cudaMemcpyAsync(host_out, src, n, cudaMemcpyDeviceToHost, st));
+  if (what == 5) CUDA_TRY(cudaMemcpyAsync((uint8_t*)host_out + n, &h->dev.ctrl[CTRL_RCOUNT], 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (used) *used = n + (what == 5 ? 8 : 0);
+  return DSR_OK;
+}
+
+extern "C" uint64_t dsr_kernel_launches(void) { return g_launches.load(); }
+
+extern "C" const char* dsr_status_str(dsr_status s) {
+  switch (s) {
+    case DSR_OK: return "DSR_OK";
+    case DSR_ERR_INVALID: return "DSR_ERR_INVALID";
+    case DSR_ERR_OOM: return "DSR_ERR_OOM";
+    case DSR_ERR_CUDA: return "DSR_ERR_CUDA";
+    case DSR_ERR_RETRY_BUDGET: return "DSR_ERR_RETRY_BUDGET";
+    case DSR_ERR_INVARIANT: return "DSR_ERR_INVARIANT";
+    case DSR_ERR_UNSUPPORTED: return "DSR_ERR_UNSUPPORTED";
+  }
+  return "DSR_ERR_?";
+}
+extern "C" const char* dsr_build_info(void) { return DSR_BUILD_INFO; }

@@ -1,0 +1,382 @@
+// dsr_device.cuh -- device side of the B200 DynaSOAr hot path (sm_100a).
+//
+// Lock-free hierarchical bitmaps, block heap with slot
+// reservation / freeing / invalidation (App. A) and the
+// warp-aggregated object allocator (Algs. 1-2 P:375-426, request coalescing
+// and bitmap rotation P:646-654, n-th set bit P:689).
+//
+// Memory model (reading R-MEMORY / C21): every bitmap word is modified with
+// 64-bit relaxed device-scope atomics (atom.global.{or,and}.b64); plain reads
+// of shared words are ld.relaxed.gpu.  initialize_block writes the type id,
+// then fence (__threadfence = fence.sc.gpu), then the object bitmap; a thread
+// whose atomicOr reserved a slot fences before reading the type (Alg. 1 l.10,
+// footnote P:1091) -- fence-fence synchronisation through the bitmap word.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/dsr.h"
+
+namespace dsr {
+
+typedef unsigned long long ull;
+
+struct DevBitmap {
+  uint64_t* lvl[DSR_MAX_LEVELS];   // level 0 = leaf containers
+  uint32_t nlevels;
+  uint32_t pad_;
+  uint64_t nbits;
+};
+
+struct DevType {
+  uint32_t cap;                    // N_T
+  uint32_t nfields;
+  uint64_t valid;                  // low N_T bits
+  uint64_t pad;                    // ~valid: padding bits kept at 1
+  uint32_t fsize[DSR_MAX_FIELDS];
+  uint32_t col_off[DSR_MAX_FIELDS];
+};
+
+// control page word offsets (u64 units) -- DESIGN.md "HBM layout"
+enum { CTRL_ERR = 0, CTRL_RCOUNT = 1, CTRL_SCRATCH = 2, CTRL_STATS = 16, CTRL_AUDIT = 40 };
+enum { ERRB_OOM = 1, ERRB_BUDGET = 2 };
+enum { ST_ALLOCS = 0, ST_FREES, ST_INITS, ST_BFREES, ST_ROLLBACKS, ST_INVFAIL, ST_RESRETRY, ST_OOM, ST_N };
+
+struct DevHeap {
+  uint8_t* data;          // M * block_bytes SOA data segments
+  uint64_t* alloc_bm;     // object allocation bitmap per block
+  uint64_t* iter_bm;      // object iteration bitmap per block
+  uint8_t* type;          // type id per block, 1-based, 0 = never initialised
+  uint32_t* R;            // do-all block list
+  ull* ctrl;              // control page
+  uint32_t M;
+  uint32_t block_bytes;
+  uint32_t ntypes;
+  uint32_t r_attempts;
+  uint32_t flags;
+  uint32_t pad_;
+  uint64_t seed;
+  DevBitmap freebm;
+  DevBitmap allocbm[DSR_MAX_TYPES];
+  DevBitmap activebm[DSR_MAX_TYPES];
+  DevType types[DSR_MAX_TYPES];
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u8(const uint8_t* p) {
+  uint16_t v;
+  asm volatile("ld.relaxed.gpu.global.u8 %0, [%1];" : "=h"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_u8(uint8_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u8 [%0], %1;" ::"l"(p), "h"((uint16_t)v) : "memory");
+}
+__device__ __forceinline__ uint64_t atom_or(uint64_t* p, uint64_t m) { return atomicOr((ull*)p, (ull)m); }
+__device__ __forceinline__ uint64_t atom_and(uint64_t* p, uint64_t m) { return atomicAnd((ull*)p, (ull)m); }
+__device__ __forceinline__ uint64_t rotr64(uint64_t x, uint32_t r) { return r ? (x >> r) | (x << (64 - r)) : x; }
+__device__ __forceinline__ uint64_t rotl64(uint64_t x, uint32_t r) { return r ? (x << r) | (x >> (64 - r)) : x; }
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ uint64_t shfl64(uint32_t mask, uint64_t v, uint32_t src) {
+  uint32_t lo = __shfl_sync(mask, (uint32_t)v, src), hi = __shfl_sync(mask, (uint32_t)(v >> 32), src);
+  return ((uint64_t)hi << 32) | lo;
+}
+// 0-based n-th set bit of x ("b <- b & (b-1) ... then ffs"; __fns does it in hardware)
+__device__ __forceinline__ uint32_t nth_bit(uint64_t x, uint32_t n) {
+  uint32_t lo = (uint32_t)x, c = __popc(lo);
+  if (n < c) return __fns(lo, 0, (int)n + 1);
+  return 32u + __fns((uint32_t)(x >> 32), 0, (int)(n - c) + 1);
+}
+__device__ __forceinline__ void backoff(uint32_t& ns) {
+  __nanosleep(ns);
+  ns = ns < 256 ? ns * 2 : 256;
+}
+__device__ __forceinline__ void flag_error(const DevHeap& h, uint32_t bit) { atomicOr(&h.ctrl[CTRL_ERR], (ull)bit); }
+__device__ __forceinline__ void stat_add(const DevHeap& h, int which, uint64_t v) {
+  if (h.flags & DSR_F_STATS) atomicAdd(&h.ctrl[CTRL_STATS + which], (ull)v);
+}
+
+// counter-based RNG, reading R-RNG (SplitMix64 output function)
+__device__ __forceinline__ uint64_t sm64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t rng_key(uint64_t seed, uint64_t step, uint64_t phase, uint64_t idx) {
+  return sm64(sm64(sm64(seed) ^ step) ^ ((phase << 40) | idx));
+}
+
+// ------------------------------------------------------------------ handles (Fig. 5, Listing 2)
+__device__ __forceinline__ uint64_t make_handle(uint32_t T, uint32_t cap, uint32_t bid, uint32_t slot) {
+  return ((uint64_t)(T + 1) << 56) | ((uint64_t)(cap - 1) << 50) | ((uint64_t)bid << 6) | slot;
+}
+__device__ __forceinline__ uint32_t h_slot(uint64_t h) { return (uint32_t)(h & 0x3Full); }
+__device__ __forceinline__ uint32_t h_bid(uint64_t h) { return (uint32_t)((h & 0x3FFFFFFFFFFC0ull) >> 6); }
+__device__ __forceinline__ uint32_t h_type(uint64_t h) { return (uint32_t)(h >> 56) - 1u; }  // 0-based
+__device__ __forceinline__ bool h_is(uint64_t h, uint32_t T) { return (h >> 56) == (uint64_t)(T + 1); }
+
+template <class V>
+__device__ __forceinline__ V* field_ptr(const DevHeap& h, uint32_t T, uint32_t f, uint32_t bid, uint32_t slot) {
+  // Listing 2: block + field_offset * capacity + slot * sizeof
+  return reinterpret_cast<V*>(h.data + (size_t)bid * h.block_bytes + h.types[T].col_off[f]) + slot;
+}
+template <class V>
+__device__ __forceinline__ V* field_ptr(const DevHeap& h, uint64_t hd, uint32_t f) {
+  return field_ptr<V>(h, h_type(hd), f, h_bid(hd), h_slot(hd));
+}
+
+// ------------------------------------------------------------------ rotation (reading R-ROT / C3)
+__device__ __forceinline__ uint64_t rot_hash(const DevHeap& h, uint64_t who, uint64_t retry) {
+  if (h.flags & DSR_F_NO_ROTATE) return 0;
+  return sm64(who * 0x9E3779B97F4A7C15ull ^ (retry << 32) ^ h.seed);
+}
+__device__ __forceinline__ uint64_t warp_gid() {
+  return ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+}
+
+// ------------------------------------------------------------------ hierarchical bitmap
+// set(pos) at level l: "switches the bit from 0 to 1, retries until the bit
+// was changed"; cascades set-first upward (Def. P:1129).  Upper
+// levels always use the retrying versions.
+__device__ __forceinline__ void bm_set_from(const DevBitmap& b, uint32_t l, uint64_t pos) {
+  for (; l < b.nlevels; ++l) {
+    uint64_t* w = b.lvl[l] + (pos >> 6);
+    const uint64_t m = 1ull << (pos & 63);
+    uint64_t prev;
+    uint32_t ns = 32;
+    for (;;) {
+      if (!(ld_relaxed(w) & m)) {
+        prev = atom_or(w, m);
+        if (!(prev & m)) break;
+      }
+      backoff(ns);   // legal use: an in-flight clear of this bit is pending
+    }
+    if (prev != 0) return;     // not set-first: upper level already 1
+    pos >>= 6;
+  }
+}
+__device__ __forceinline__ void bm_clear_from(const DevBitmap& b, uint32_t l, uint64_t pos) {
+  for (; l < b.nlevels; ++l) {
+    uint64_t* w = b.lvl[l] + (pos >> 6);
+    const uint64_t m = 1ull << (pos & 63);
+    uint64_t prev;
+    uint32_t ns = 32;
+    for (;;) {
+      if (ld_relaxed(w) & m) {
+        prev = atom_and(w, ~m);
+        if (prev & m) break;
+      }
+      backoff(ns);
+    }
+    if (prev != m) return;     // Alg. 3 l.6: cascade only if popc(prev) = 1
+    pos >>= 6;
+  }
+}
+__device__ __forceinline__ void bm_set(const DevBitmap& b, uint64_t pos) { bm_set_from(b, 0, pos); }
+__device__ __forceinline__ void bm_clear(const DevBitmap& b, uint64_t pos) { bm_clear_from(b, 0, pos); }
+
+// Alg. 3 (try_clear) and its symmetric try_set
+__device__ __forceinline__ bool bm_try_clear(const DevBitmap& b, uint64_t pos) {
+  uint64_t* w = b.lvl[0] + (pos >> 6);
+  const uint64_t m = 1ull << (pos & 63);
+  const uint64_t prev = atom_and(w, ~m);
+  if (!(prev & m)) return false;
+  if (prev == m && b.nlevels > 1) bm_clear_from(b, 1, pos >> 6);
+  return true;
+}
+__device__ __forceinline__ bool bm_try_set(const DevBitmap& b, uint64_t pos) {
+  uint64_t* w = b.lvl[0] + (pos >> 6);
+  const uint64_t m = 1ull << (pos & 63);
+  const uint64_t prev = atom_or(w, m);
+  if (prev & m) return false;
+  if (prev == 0 && b.nlevels > 1) bm_set_from(b, 1, pos >> 6);
+  return true;
+}
+__device__ __forceinline__ bool bm_get(const DevBitmap& b, uint64_t pos) {
+  return (ld_relaxed(b.lvl[0] + (pos >> 6)) >> (pos & 63)) & 1;
+}
+
+// Alg. 4 try_find_set, top-down; each level's container is rotated by 6
+// bits of `rh` before ffs.  May FAIL spuriously.
+__device__ __forceinline__ int64_t bm_try_find_set(const DevBitmap& b, uint64_t rh) {
+  uint64_t cid = 0;
+  for (int l = (int)b.nlevels - 1; l >= 0; --l) {
+    const uint64_t c = ld_relaxed(b.lvl[l] + cid);
+    if (c == 0) return -1;
+    const uint32_t r = (uint32_t)(rh >> (6 * l)) & 63u;
+    const uint32_t i = ((uint32_t)__ffsll((long long)rotr64(c, r)) - 1u + r) & 63u;
+    cid = cid * 64 + i;
+  }
+  return (int64_t)cid;
+}
+// clear(): find + try_clear until the clear succeeds (reading R-CLEARANY)
+__device__ __forceinline__ int64_t bm_clear_any(const DevHeap& h, const DevBitmap& b, uint64_t who, uint64_t retry0) {
+  for (uint64_t k = 0;; ++k) {
+    const int64_t i = bm_try_find_set(b, rot_hash(h, who, retry0 + k));
+    if (i < 0) return -1;
+    if (bm_try_clear(b, (uint64_t)i)) return i;
+  }
+}
+
+// ------------------------------------------------------------------ blocks (App. A)
+// Alg. 8: type <- T; fence; bitmap <- padding mask
+__device__ __forceinline__ void init_block(const DevHeap& h, uint32_t T, uint32_t bid) {
+  st_relaxed_u8(h.type + bid, T + 1);
+  __threadfence();
+  st_relaxed(h.alloc_bm + bid, h.types[T].pad);
+}
+
+// Alg. 6 generalised to a coalesced multi-slot reservation: pick up to `need`
+// free slots (rotated) and set them with ONE atomicOr; returns the
+// slots this call actually flipped (may be fewer; 0 = block full/invalidated).
+__device__ __forceinline__ uint64_t block_reserve(const DevHeap& h, uint32_t bid, uint32_t need, uint32_t rot,
+                                                  uint64_t* before_out) {
+  uint64_t* w = h.alloc_bm + bid;
+  uint64_t cur = ld_relaxed(w);
+  for (;;) {
+    const uint64_t fr = ~cur;
+    if (fr == 0) return 0;
+    uint64_t rf = rotr64(fr, rot);
+    if ((uint32_t)__popcll(rf) > need) rf &= (2ull << nth_bit(rf, need - 1)) - 1ull;   // first `need` bits
+    const uint64_t sel = rotl64(rf, rot);
+    const uint64_t before = atom_or(w, sel);
+    const uint64_t got = sel & ~before;
+    if (got) { *before_out = before; return got; }
+    stat_add(h, ST_RESRETRY, 1);
+    cur = before | sel;
+  }
+}
+
+// Alg. 9 (iterative, footnote P:1077) with padding: succeeds iff every
+// non-padding bit was 0, i.e. before == pad(t).
+__device__ __forceinline__ bool block_invalidate(const DevHeap& h, uint32_t bid) {
+  uint64_t* w = h.alloc_bm + bid;
+  for (;;) {
+    const uint64_t before = atom_or(w, ~0ull);
+    if (before == ~0ull) return false;
+    const uint32_t t = ld_relaxed_u8(h.type + bid) - 1u;   // fixed while we hold invalidated bits
+    const uint64_t pad = h.types[t].pad;
+    if (before == pad) return true;
+    stat_add(h, ST_INVFAIL, 1);
+    const uint64_t before_rb = atom_and(w, before);         // rollback exactly our bits
+    if (before_rb != ~0ull) bm_clear(h.activebm[t], bid);   // deferred deactivation
+    if ((before_rb & before) != pad) return false;          // not empty again
+  }
+}
+
+// Alg. 7 + Alg. 2 for a mask of slots of one block of type T (coalesced free).
+// FIRST iff before == ~0; EMPTY iff the remaining bits are padding only;
+// both at once: activate, then invalidate (reading R-FIRSTEMPTY / C17).
+__device__ __forceinline__ void block_free(const DevHeap& h, uint32_t T, uint32_t bid, uint64_t mask) {
+  const uint64_t before = atom_and(h.alloc_bm + bid, ~mask);
+  const bool first = before == ~0ull;
+  const bool empty = (before & ~mask) == h.types[T].pad;
+  if (first) bm_set(h.activebm[T], bid);
+  if (empty) {
+    if (block_invalidate(h, bid)) {
+      const uint32_t t = ld_relaxed_u8(h.type + bid) - 1u;
+      bm_clear(h.activebm[t], bid);
+      bm_clear(h.allocbm[t], bid);
+      bm_set(h.freebm, bid);
+      stat_add(h, ST_BFREES, 1);
+    }
+  }
+}
+
+// Alg. 1 for one coalesced request of `need` slots (leader lane only).
+// Returns the reserved slot mask (0 = OOM) and the block in *bid_out.
+static __device__ __noinline__ uint64_t reserve_chunk(const DevHeap& h, uint32_t T, uint32_t need, uint32_t* bid_out) {
+  const uint64_t who = warp_gid();
+  uint32_t oom_tries = 0;
+  for (uint64_t iter = 0;; ++iter) {
+    int64_t bid = -1;
+    for (uint32_t a = 0; a < h.r_attempts && bid < 0; ++a)                  // r attempts
+      bid = bm_try_find_set(h.activebm[T], rot_hash(h, who, iter * 16 + a));
+    if (bid < 0) {                                                            // slow path
+      bid = bm_clear_any(h, h.freebm, who, iter * 16 + 8);
+      if (bid < 0) {
+        // free bitmap empty (or transiently inconsistent): look for active blocks again
+        if ((h.flags & DSR_F_SPIN_ON_OOM) || ++oom_tries < 64) { uint32_t ns = 128; backoff(ns); continue; }
+        flag_error(h, ERRB_OOM);
+        stat_add(h, ST_OOM, 1);
+        return 0;
+      }
+      init_block(h, T, (uint32_t)bid);
+      bm_set(h.allocbm[T], (uint64_t)bid);
+      bm_set(h.activebm[T], (uint64_t)bid);
+      stat_add(h, ST_INITS, 1);
+    }
+    uint64_t before = 0;
+    const uint32_t rot = (uint32_t)(rot_hash(h, who, iter * 16 + 15) >> 58);
+    const uint64_t got = block_reserve(h, (uint32_t)bid, need, rot, &before);
+    if (!got) continue;                                                       // full or invalidated
+    __threadfence();                                                          // acquire the type id
+    const uint32_t t = ld_relaxed_u8(h.type + bid) - 1u;                      // volatile read (Alg. 1 l.10)
+    if ((before | got) == ~0ull) bm_clear(h.activebm[t], (uint64_t)bid);      // FULL -> inactive (l.12)
+    if (t == T) { *bid_out = (uint32_t)bid; return got; }
+    block_free(h, t, (uint32_t)bid, got);                                     // type changed: rollback (l.14)
+    stat_add(h, ST_ROLLBACKS, 1);
+  }
+}
+
+// Device new<T> with allocation request coalescing: lanes of
+// the calling warp that request the same type elect a leader, the leader
+// reserves slots for all of them, each lane takes the rank-th reserved slot.
+// Any subset of lanes may call it (divergent call sites allowed).
+__device__ __forceinline__ uint64_t dsr_new(const DevHeap& h, uint32_t T) {
+  const uint32_t lane = lane_id();
+  const uint32_t act = __activemask();
+  const uint32_t peers = (h.flags & DSR_F_NO_COALESCE) ? (1u << lane) : __match_any_sync(act, T);
+  const uint32_t leader = __ffs(peers) - 1;
+  const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+  const uint32_t count = __popc(peers);
+  const uint32_t cap = h.types[T].cap;
+  uint64_t mine = 0;
+  uint32_t done = 0;
+  while (done < count) {
+    uint64_t got = 0;
+    uint32_t bid = 0;
+    if (lane == leader) got = reserve_chunk(h, T, count - done, &bid);
+    got = shfl64(peers, got, leader);
+    bid = __shfl_sync(peers, bid, leader);
+    if (got == 0) break;                                   // OOM: remaining lanes get null
+    const uint32_t n = __popcll(got);
+    if (rank >= done && rank < done + n) mine = make_handle(T, cap, bid, nth_bit(got, rank - done));
+    done += n;
+  }
+  if (lane == leader) stat_add(h, ST_ALLOCS, done);
+  return mine;
+}
+
+// Device destroy: lanes freeing slots of the same block combine their
+// bits into one atomicAnd (coalesced version of Alg. 7).
+__device__ __forceinline__ void dsr_destroy(const DevHeap& h, uint64_t x) {
+  if (x == 0) return;
+  const uint32_t lane = lane_id();
+  const uint32_t act = __activemask();
+  const uint64_t key = x >> 6;
+  const uint32_t peers = (h.flags & DSR_F_NO_COALESCE) ? (1u << lane) : __match_any_sync(act, (ull)key);
+  const uint32_t leader = __ffs(peers) - 1;
+  const uint64_t bit = 1ull << h_slot(x);
+  const uint32_t lo = __reduce_or_sync(peers, (uint32_t)bit);
+  const uint32_t hi = __reduce_or_sync(peers, (uint32_t)(bit >> 32));
+  if (lane == leader) {
+    const uint64_t mask = ((uint64_t)hi << 32) | lo;
+    block_free(h, h_type(x), h_bid(x), mask);
+    stat_add(h, ST_FREES, __popcll(mask));
+  }
+}
+
+}  // namespace dsr

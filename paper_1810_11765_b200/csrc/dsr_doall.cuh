@@ -1,0 +1,119 @@
+// dsr_doall.cuh -- parallel do-all (§3.6, Alg. 5).
+//
+// Prologue (k_compact): one pass over the leaf containers of allocated[T]
+// that (a) skips containers whose nested-level bit is 0, (b) counts
+// set bits, prefix-sums them across the CTA (warp shuffles) and reserves a
+// CTA-wide range of R with ONE atomicAdd (the paper's atomic cursor, P:641,
+// at CTA rather than thread granularity), (c) writes R coalesced (lane j of a
+// warp expands bit j / j+32 of a container) and (d) optionally snapshots the
+// iteration bitmaps iter_bm[b] = alloc_bm[b] & valid(N_T) (C12).  The
+// count r stays on the device (ctrl[CTRL_RCOUNT]); nothing returns to the host.
+//
+// Body (k_doall<Method>): a persistent grid strides over the r*N_T elements
+// e -> block R[e / N_T], slot e % N_T (reading R-ASSIGN / C9: the paper's
+// id_O / id_B formulas with an element stride, exact for every n).  Lanes of
+// a warp take consecutive slots of a block, so every SOA field access of a
+// warp is one contiguous column segment.
+#pragma once
+#include "dsr_device.cuh"
+
+namespace dsr {
+
+constexpr int kCompactThreads = 256;
+
+static __global__ void __launch_bounds__(kCompactThreads) k_compact(DevHeap h, uint32_t T, int snapshot) {
+  __shared__ uint64_t s_word[kCompactThreads];
+  __shared__ uint32_t s_off[kCompactThreads];
+  __shared__ uint32_t s_warp[kCompactThreads / 32];
+  __shared__ uint32_t s_base;
+  const DevBitmap& ab = h.allocbm[T];
+  const uint64_t nwords = ((uint64_t)h.M + 63) / 64;
+  const uint64_t i = (uint64_t)blockIdx.x * kCompactThreads + threadIdx.x;
+  uint64_t w = 0;
+  if (i < nwords) {
+    bool any = true;
+    if (ab.nlevels > 1) any = (ab.lvl[1][i >> 6] >> (i & 63)) & 1ull;    // hierarchical skip
+    if (any) w = ab.lvl[0][i];
+  }
+  const uint32_t cnt = __popcll(w);
+  // CTA exclusive scan of cnt
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t inc = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= (uint32_t)o) inc += v;
+  }
+  if (lane == 31) s_warp[wid] = inc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t run = 0;
+    for (int k = 0; k < kCompactThreads / 32; ++k) { const uint32_t t = s_warp[k]; s_warp[k] = run; run += t; }
+    s_base = run ? atomicAdd((unsigned int*)&h.ctrl[CTRL_RCOUNT], run) : 0u;
+  }
+  __syncthreads();
+  s_word[threadIdx.x] = w;
+  s_off[threadIdx.x] = s_base + s_warp[wid] + inc - cnt;
+  __syncwarp();
+  // warp-cooperative expansion of this warp's 32 containers
+  const uint64_t valid = h.types[T].valid;
+  for (int k = 0; k < 32; ++k) {
+    const uint32_t src = wid * 32 + k;
+    const uint64_t wk = s_word[src];
+    if (wk == 0) continue;
+    const uint32_t off = s_off[src];
+    const uint64_t cidx = (uint64_t)blockIdx.x * kCompactThreads + src;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const uint32_t bit = lane + 32 * half;
+      if ((wk >> bit) & 1ull) {
+        const uint32_t pos = off + __popcll(wk & ((1ull << bit) - 1ull));
+        const uint32_t b = (uint32_t)(cidx * 64 + bit);
+        h.R[pos] = b;
+        if (snapshot) h.iter_bm[b] = h.alloc_bm[b] & valid;
+      }
+    }
+  }
+}
+
+// Persistent-grid element loop shared by all method kernels.
+template <class Mth>
+__global__ void __launch_bounds__(256) k_doall(DevHeap h, uint32_t T, int snapshot, typename Mth::Args a) {
+  const uint32_t r = ld_relaxed_u32((const uint32_t*)&h.ctrl[CTRL_RCOUNT]);
+  const uint32_t N = h.types[T].cap;
+  const uint64_t total = (uint64_t)r * N;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  typename Mth::Acc acc;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const uint32_t bi = (uint32_t)(e / N);
+    const uint32_t s = (uint32_t)(e - (uint64_t)bi * N);
+    const uint32_t b = h.R[bi];
+    const uint64_t w = snapshot ? h.iter_bm[b] : ld_relaxed(h.alloc_bm + b);
+    if ((w >> s) & 1ull) Mth::run(h, T, b, s, a, acc);
+  }
+  Mth::flush(acc, a);
+}
+
+// Method helpers: most methods keep no per-thread accumulator.
+struct NoAcc {};
+#define DSR_NO_ACC                                                        \
+  typedef NoAcc Acc;                                                      \
+  static __device__ __forceinline__ void flush(Acc&, const Args&) {}
+
+// Per-thread event counters flushed with one warp-aggregated atomic per lane
+// group (used by Wa-Tor / N-body for born/eaten/starved/merged counts).
+struct Counters4 {
+  uint32_t c[4];
+  __device__ Counters4() : c{0, 0, 0, 0} {}
+};
+__device__ __forceinline__ void flush_counters4(Counters4& acc, unsigned long long* out) {
+  if (!out) return;
+  const uint32_t act = __activemask();
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t v = __reduce_add_sync(act, acc.c[k]);
+    if (v && lane_id() == (uint32_t)(__ffs(act) - 1)) atomicAdd(out + k, (unsigned long long)v);
+  }
+}
+
+}  // namespace dsr

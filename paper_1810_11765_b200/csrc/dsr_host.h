@@ -1,0 +1,58 @@
+// dsr_host.h -- host-side plumbing shared by the C ABI and the app tables.
+#pragma once
+#include <cuda_runtime.h>
+#include <atomic>
+#include "dsr_device.cuh"
+#include "dsr_doall.cuh"
+
+namespace dsr {
+
+struct LaunchCtx {
+  DevHeap h;
+  cudaStream_t st;
+  int grid;            // persistent grid size for element loops (multiple of #SMs)
+  int sms;
+};
+
+struct MethodInfo {
+  int allocates;       // 1: the method may allocate (needs the iteration-bitmap snapshot)
+  size_t args_bytes;   // expected sizeof(args)
+};
+
+extern std::atomic<unsigned long long> g_launches;
+inline void count_launch(unsigned long long k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+// Per-app tables.  Each returns false when the id is not theirs.
+bool mb_method_info(uint32_t id, MethodInfo* mi);
+bool mb_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot, const void* args);
+bool mb_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* args, size_t bytes, int* ok);
+
+bool gol_method_info(uint32_t id, MethodInfo* mi);
+bool gol_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot, const void* args);
+bool gol_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* args, size_t bytes, int* ok);
+
+bool wt_method_info(uint32_t id, MethodInfo* mi);
+bool wt_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot, const void* args);
+bool wt_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* args, size_t bytes, int* ok);
+bool wt_ctor_launch(uint32_t id, const LaunchCtx& c, uint32_t T, uint64_t n, const void* args, size_t bytes, int* ok);
+
+bool nb_method_info(uint32_t id, MethodInfo* mi);
+bool nb_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot, const void* args);
+bool nb_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* args, size_t bytes, int* ok);
+bool nb_ctor_launch(uint32_t id, const LaunchCtx& c, uint32_t T, uint64_t n, const void* args, size_t bytes, int* ok);
+
+// launch helper for element-loop method kernels
+template <class Mth>
+inline void launch_doall(const LaunchCtx& c, uint32_t T, int snapshot, const void* args) {
+  typename Mth::Args a = *reinterpret_cast<const typename Mth::Args*>(args);
+  k_doall<Mth><<<c.grid, 256, 0, c.st>>>(c.h, T, snapshot, a);
+  count_launch();
+}
+
+inline int grid_for(const LaunchCtx& c, uint64_t n, int threads = 256) {
+  uint64_t g = (n + threads - 1) / threads;
+  if (g > (uint64_t)c.grid) g = (uint64_t)c.grid;
+  return g ? (int)g : 1;
+}
+
+}  // namespace dsr

@@ -1,0 +1,86 @@
+"""Allocator microbenchmark driver (BASELINE configs[4]; SURVEY c.4): the host
+loop of dsr_launch / dsr_parallel_do calls.  All work runs in libdsr.so."""
+from __future__ import annotations
+
+import ctypes as C
+
+from . import dsr
+
+MB_TYPES = [[4, 4, 4], [4, 4, 4, 4], [4] * 6]   # A{3 x u32}, B{4 x u32}, C{6 x u32}
+PHASES = ["init", "new1", "reduce2", "free3", "new4", "reduce5", "drain6"]
+
+
+class Microbench:
+    def __init__(self, n1=1 << 26, n2=1 << 25, seed=1, heap_bytes=None, device=None, retries=5, flags=0,
+                 stream=None):
+        import torch
+        self.n1, self.n2, self.seed = n1, n2, seed
+        if heap_bytes is None:
+            # room for every object of phase 1 + 4 at the worst per-block fill, x2 for contention slack
+            heap_bytes = max(64 << 20, int((n1 + n2) * 24 * 2.0))
+        self.heap = dsr.Heap(MB_TYPES, heap_bytes, device=device, retries=retries, flags=flags, stream=stream)
+        self.out = torch.zeros(18, dtype=torch.int64, device=self.heap.device)   # u64 bit patterns
+        self.stream = stream
+
+    def _reduce_args(self, k):
+        return dsr.MbReduceArgs(self.out.data_ptr() + 8 * k)
+
+    def step(self, stream=None, events=None, body_events=None):
+        """One pass of the whole hot path: heap init, new 2^26, reduce, free odd,
+        new 2^25, reduce, drain.  `events`: optional list of 7 torch.cuda.Event
+        pairs recorded around the phases; `body_events`: 6 pairs around the
+        reduce bodies (k_mb_reduce) of phases 2 and 5 (timing only)."""
+        h = self.heap
+        s = stream if stream is not None else self.stream
+
+        def ev(i, end):
+            if events is not None:
+                events[i][1 if end else 0].record(s)
+
+        def reduce(t, k, j):
+            h.doall_prologue(t, dsr.M_MB_REDUCE, s)
+            if body_events is not None:
+                body_events[j][0].record(s)
+            h.doall_body(t, dsr.M_MB_REDUCE, self._reduce_args(k), s)
+            if body_events is not None:
+                body_events[j][1].record(s)
+
+        ev(0, 0)
+        h.reset(s)
+        import torch
+        with torch.cuda.stream(s if s is not None else torch.cuda.current_stream()):
+            self.out.zero_()
+        ev(0, 1)
+        ev(1, 0); h.launch(dsr.K_MB_NEW, self.n1, dsr.MbNewArgs(self.seed, 0), s); ev(1, 1)
+        ev(2, 0)
+        for t in range(3):
+            reduce(t, 3 * t, t)
+        ev(2, 1)
+        ev(3, 0)
+        for t in range(3):
+            h.parallel_do(t, dsr.M_MB_FREE_ODD, None, s)
+        ev(3, 1)
+        ev(4, 0); h.launch(dsr.K_MB_NEW, self.n2, dsr.MbNewArgs(self.seed, self.n1), s); ev(4, 1)
+        ev(5, 0)
+        for t in range(3):
+            reduce(t, 9 + 3 * t, 3 + t)
+        ev(5, 1)
+        ev(6, 0)
+        for t in range(3):
+            h.parallel_do(t, dsr.M_MB_FREE_ALL, None, s)
+        ev(6, 1)
+
+    def results(self):
+        """(2, 3, 3) numpy uint64: phase 2/5 x type x (count, sum, xor)."""
+        import numpy as np
+        return self.out.cpu().numpy().view(np.uint64).reshape(2, 3, 3)
+
+    def counts(self):
+        """Per-step operation counts for throughput metrics (needs results())."""
+        r = self.results()
+        ph2 = int(r[0, :, 0].sum())
+        ph5 = int(r[1, :, 0].sum())
+        freed3 = ph2 + self.n2 - ph5                 # phase 3 frees = phase-2 live + n2 - phase-5 live
+        return {"allocs": self.n1 + self.n2, "frees": freed3 + ph5,
+                "visits": ph2 + ph2 + ph5 + ph5,     # reduce2, free3, reduce5, drain6
+                "scan_objects": ph2 + ph5}

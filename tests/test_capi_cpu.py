@@ -1,0 +1,83 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol that
+include/dsr.h declares, and its host-side layout equals the oracle's."""
+import ctypes
+import random
+import re
+from pathlib import Path
+
+import pytest
+
+from conftest import ROOT, split_fields
+
+
+def declared_functions():
+    txt = (ROOT / "include" / "dsr.h").read_text()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(dsr_[a-z_0-9]+)\s*\(", txt, flags=re.M)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_1810_11765_b200 import build, dsr
+    build.build()
+    return dsr
+
+
+def test_library_exports_every_declared_symbol(L):
+    names = declared_functions()
+    assert len(names) >= 20
+    lib = ctypes.CDLL(str(L.LIBPATH))
+    for n in names:
+        assert hasattr(lib, n), n
+    assert L.lib().dsr_build_info().startswith(b"sm_100a")
+
+
+def test_status_strings(L):
+    assert L.status_str(L.OK) == "DSR_OK"
+    assert L.status_str(L.ERR_OOM) == "DSR_ERR_OOM"
+
+
+def test_layout_equals_oracle(L, O):
+    rnd = random.Random(11)
+    cases = [[[4, 4, 4], [4, 4, 4, 4], [4] * 6], [[4, 1, 1], [4, 1]], [[4, 4, 4], [4, 4, 4, 4], [4, 8, 1, 1, 1, 1, 1]],
+             [[4] * 7 + [4, 4, 4, 1]]]
+    for _ in range(150):
+        T = rnd.randint(1, 8)
+        tf = [[rnd.choice([1, 2, 4, 8, 16]) for _ in range(rnd.randint(1, 16))] for _ in range(T)]
+        if max(map(sum, tf)) <= 64 * min(map(sum, tf)):
+            cases.append(tf)
+    for tf in cases:
+        for heap in (1 << 20, 123456789, 1 << 31):
+            a = L.layout_compute(tf, heap)
+            b = O.layout(tf, heap)
+            for k, v in b.items():
+                if k == "col_off":
+                    assert [a[k][t][:len(tf[t])] for t in range(len(tf))] == v
+                else:
+                    assert a[k] == v, (k, tf, heap)
+
+
+def test_layout_rejects_invalid(L):
+    with pytest.raises(ValueError):
+        L.layout_compute([[4], [16] * 16 + [4]], 1 << 20)        # > 16 fields (binding)
+    with pytest.raises(L.DsrError):
+        L.layout_compute([[4], [3]], 1 << 20)                     # field size 3
+    with pytest.raises(L.DsrError):
+        L.layout_compute([[2], [16] * 9], 1 << 20)                # 144 B > 64 x 2 B
+    with pytest.raises(L.DsrError):
+        L.layout_compute([[4]], 4096)                             # no room for a block
+
+
+def test_product_path_fails_loudly_without_gpu(L):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(RuntimeError):
+        L.Heap([[4]], 1 << 20)
+
+
+def test_product_package_never_imports_the_oracle():
+    pkg = ROOT / "paper_1810_11765_b200"
+    for p in list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")) + list(pkg.rglob("*.h")):
+        txt = p.read_text()
+        assert not re.search(r"(^|\n)\s*(from|import)\s+oracle|liboracle|oracle\.h|oracle/", txt), p
