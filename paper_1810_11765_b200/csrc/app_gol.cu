@@ -1,7 +1,162 @@
-// app_gol.cu -- placeholder (filled in later)
+// app_gol.cu -- Game of Life with O(#alive) work (Table 1; reading
+// R-GOL).  Types: 0 = Alive{cell u32, is_new u8, action u8},
+// 1 = Candidate{cell u32, action u8}.  The static cell grid `cell[c]` holds
+// the handle of the object at c (0 = empty); liveness of a neighbour is read
+// from the handle's type bits, never from the object ("fast
+// instance-of checks").  Four do-alls per generation (Table 1):
+//   1 Candidate.prepare  2 Alive.prepare  3 Candidate.update  4 Alive.update
+// In pass 4 a new Alive creates a Candidate on every empty neighbour exactly
+// once: the creator claims the empty cell with atomicCAS(0 -> RESERVED), so
+// the created set is the same for every visit order.
 #include "dsr_host.h"
+
 namespace dsr {
-bool gol_method_info(uint32_t, MethodInfo*) { return false; }
-bool gol_method_launch(uint32_t, const LaunchCtx&, uint32_t, int, const void*) { return false; }
-bool gol_kernel_launch(uint32_t, const LaunchCtx&, uint64_t, const void*, size_t, int*) { return false; }
+
+enum { GOL_ALIVE = 0, GOL_CAND = 1 };
+enum { ACT_NONE = 0, ACT_SPAWN = 1, ACT_DIE = 2 };
+constexpr uint64_t kReserved = 1;   // not a handle: type bits 0
+
+__device__ __forceinline__ uint32_t gol_nbr(uint32_t W, uint32_t H, uint32_t c, int k) {
+  // Moore neighbourhood on the W x H torus, k = 0..7 (row-major order of offsets)
+  const uint32_t x = c % W, y = c / W;
+  const int dx = (k < 3) ? k - 1 : (k == 3 ? -1 : (k == 4 ? 1 : k - 6));
+  const int dy = (k < 3) ? -1 : (k < 5 ? 0 : 1);
+  const uint32_t nx = dx < 0 ? (x == 0 ? W - 1 : x - 1) : (dx > 0 ? (x + 1 == W ? 0 : x + 1) : x);
+  const uint32_t ny = dy < 0 ? (y == 0 ? H - 1 : y - 1) : (dy > 0 ? (y + 1 == H ? 0 : y + 1) : y);
+  return ny * W + nx;
+}
+
+__device__ __forceinline__ uint32_t gol_alive_nbrs(const dsr_gol_args& a, uint32_t c) {
+  uint32_t k = 0;
+#pragma unroll
+  for (int d = 0; d < 8; ++d) k += h_is(__ldg((const unsigned long long*)a.cell + gol_nbr(a.W, a.H, c, d)), GOL_ALIVE);
+  return k;
+}
+
+__device__ __forceinline__ uint64_t new_alive(const DevHeap& h, uint32_t c, uint8_t is_new) {
+  const uint64_t nh = dsr_new(h, GOL_ALIVE);
+  if (nh) {
+    *field_ptr<uint32_t>(h, nh, 0) = c;
+    *field_ptr<uint8_t>(h, nh, 1) = is_new;
+    *field_ptr<uint8_t>(h, nh, 2) = ACT_NONE;
+  }
+  return nh;
+}
+__device__ __forceinline__ uint64_t new_cand(const DevHeap& h, uint32_t c) {
+  const uint64_t nh = dsr_new(h, GOL_CAND);
+  if (nh) {
+    *field_ptr<uint32_t>(h, nh, 0) = c;
+    *field_ptr<uint8_t>(h, nh, 1) = ACT_NONE;
+  }
+  return nh;
+}
+
+// ---- initial state: Alive for alive cells, Candidate for dead cells with an alive neighbour
+__global__ void __launch_bounds__(256) k_gol_init(DevHeap h, uint64_t n, dsr_gol_args a, int cand) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t c = (uint32_t)i;
+    const bool alive = a.alive0[c];
+    if (!cand) {
+      if (alive) a.cell[c] = new_alive(h, c, 0);
+    } else if (!alive) {
+      bool any = false;
+      for (int d = 0; d < 8; ++d) any |= a.alive0[gol_nbr(a.W, a.H, c, d)] != 0;
+      if (any) a.cell[c] = new_cand(h, c);
+    }
+  }
+}
+
+struct GolCandPrepare {   // pass 1
+  typedef dsr_gol_args Args;
+  DSR_NO_ACC
+  static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args& a, Acc&) {
+    const uint32_t c = *field_ptr<uint32_t>(h, T, 0, b, s);
+    const uint32_t k = gol_alive_nbrs(a, c);
+    *field_ptr<uint8_t>(h, T, 1, b, s) = k == 3 ? ACT_SPAWN : (k == 0 ? ACT_DIE : ACT_NONE);
+  }
+};
+struct GolAlivePrepare {  // pass 2
+  typedef dsr_gol_args Args;
+  DSR_NO_ACC
+  static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args& a, Acc&) {
+    const uint32_t c = *field_ptr<uint32_t>(h, T, 0, b, s);
+    const uint32_t k = gol_alive_nbrs(a, c);
+    *field_ptr<uint8_t>(h, T, 1, b, s) = 0;
+    *field_ptr<uint8_t>(h, T, 2, b, s) = (k < 2 || k > 3) ? ACT_DIE : ACT_NONE;
+  }
+};
+struct GolCandUpdate {    // pass 3 (allocates Alive)
+  typedef dsr_gol_args Args;
+  DSR_NO_ACC
+  static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args& a, Acc&) {
+    const uint8_t act = *field_ptr<uint8_t>(h, T, 1, b, s);
+    if (act == ACT_NONE) return;
+    const uint32_t c = *field_ptr<uint32_t>(h, T, 0, b, s);
+    dsr_destroy(h, make_handle(T, h.types[T].cap, b, s));
+    if (act == ACT_SPAWN) a.cell[c] = new_alive(h, c, 1);
+    else a.cell[c] = 0;
+  }
+};
+struct GolAliveUpdate {   // pass 4 (allocates Candidate)
+  typedef dsr_gol_args Args;
+  DSR_NO_ACC
+  static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args& a, Acc&) {
+    const uint32_t c = *field_ptr<uint32_t>(h, T, 0, b, s);
+    if (*field_ptr<uint8_t>(h, T, 1, b, s)) {            // new Alive: candidates on empty neighbours
+      for (int d = 0; d < 8; ++d) {
+        const uint32_t e = gol_nbr(a.W, a.H, c, d);
+        unsigned long long* pe = (unsigned long long*)a.cell + e;
+        if (ld_relaxed((const uint64_t*)pe) == 0 && atomicCAS(pe, 0ull, kReserved) == 0ull) *pe = new_cand(h, e);
+      }
+    } else if (*field_ptr<uint8_t>(h, T, 2, b, s) == ACT_DIE) {
+      dsr_destroy(h, make_handle(T, h.types[T].cap, b, s));
+      a.cell[c] = new_cand(h, c);
+    }
+  }
+};
+struct GolDump {
+  typedef dsr_gol_args Args;
+  DSR_NO_ACC
+  static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args& a, Acc&) {
+    const uint32_t c = *field_ptr<uint32_t>(h, T, 0, b, s);
+    uint32_t v;
+    if (T == GOL_ALIVE) v = 1u | ((uint32_t)*field_ptr<uint8_t>(h, T, 1, b, s) << 8) | ((uint32_t)*field_ptr<uint8_t>(h, T, 2, b, s) << 16);
+    else v = 2u | ((uint32_t)*field_ptr<uint8_t>(h, T, 1, b, s) << 16);
+    a.dump[c] = v;
+  }
+};
+
+bool gol_method_info(uint32_t id, MethodInfo* mi) {
+  switch (id) {
+    case DSR_M_GOL_CAND_PREPARE: case DSR_M_GOL_ALIVE_PREPARE: case DSR_M_GOL_DUMP:
+      *mi = {0, sizeof(dsr_gol_args)}; return true;
+    case DSR_M_GOL_CAND_UPDATE: case DSR_M_GOL_ALIVE_UPDATE:
+      *mi = {1, sizeof(dsr_gol_args)}; return true;
+  }
+  return false;
+}
+
+bool gol_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot, const void* args) {
+  switch (id) {
+    case DSR_M_GOL_CAND_PREPARE: launch_doall<GolCandPrepare>(c, T, snapshot, args); return true;
+    case DSR_M_GOL_ALIVE_PREPARE: launch_doall<GolAlivePrepare>(c, T, snapshot, args); return true;
+    case DSR_M_GOL_CAND_UPDATE: launch_doall<GolCandUpdate>(c, T, snapshot, args); return true;
+    case DSR_M_GOL_ALIVE_UPDATE: launch_doall<GolAliveUpdate>(c, T, snapshot, args); return true;
+    case DSR_M_GOL_DUMP: launch_doall<GolDump>(c, T, snapshot, args); return true;
+  }
+  return false;
+}
+
+bool gol_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* args, size_t bytes, int* ok) {
+  *ok = 1;
+  if (id != DSR_K_GOL_INIT_ALIVE && id != DSR_K_GOL_INIT_CAND) return false;
+  if (bytes != sizeof(dsr_gol_args) || c.h.ntypes < 2) { *ok = 0; return true; }
+  const dsr_gol_args a = *(const dsr_gol_args*)args;
+  if ((uint64_t)a.W * a.H != n) { *ok = 0; return true; }
+  k_gol_init<<<grid_for(c, n), 256, 0, c.st>>>(c.h, n, a, id == DSR_K_GOL_INIT_CAND);
+  count_launch();
+  return true;
+}
+
 }  // namespace dsr

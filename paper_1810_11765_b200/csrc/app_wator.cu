@@ -1,8 +1,272 @@
-// app_wator.cu -- placeholder (filled in later)
+// app_wator.cu -- Wa-Tor predator-prey (Table 1; reading R-WATOR).
+// Types: 0 = Fish{cell, target, egg: u32}, 1 = Shark{cell, target, egg, energy: u32},
+// 2 = Cell{id u32, agent u64, req[5] u8}.  Cells are heap objects created by
+// parallel_new in id order; cells[id] maps an id to its handle.
+// Eight do-alls per step (Table 1): Cell.prepare, Fish.prepare, Cell.decide,
+// Fish.update, Cell.prepare, Shark.prepare, Cell.decide, Shark.update.
+// Conflicts are resolved by the target cell (request / decide), so every
+// field has one writer per pass and the result does not depend on the order
+// in which objects are visited; randomness is key(seed, step, phase, cell).
 #include "dsr_host.h"
+
 namespace dsr {
-bool wt_method_info(uint32_t, MethodInfo*) { return false; }
-bool wt_method_launch(uint32_t, const LaunchCtx&, uint32_t, int, const void*) { return false; }
-bool wt_kernel_launch(uint32_t, const LaunchCtx&, uint64_t, const void*, size_t, int*) { return false; }
-bool wt_ctor_launch(uint32_t, const LaunchCtx&, uint32_t, uint64_t, const void*, size_t, int*) { return false; }
+
+enum { WT_FISH = 0, WT_SHARK = 1, WT_CELL = 2 };
+enum { PH_FISH_REQ = 1, PH_FISH_DEC = 2, PH_SHARK_REQ = 3, PH_SHARK_DEC = 4 };
+
+__device__ __forceinline__ uint32_t wt_nbr(uint32_t W, uint32_t H, uint32_t c, uint32_t d) {
+  // von Neumann neighbour d in {N, E, S, W} on the torus
+  const uint32_t x = c % W, y = c / W;
+  switch (d) {
+    case 0: return (y == 0 ? H - 1 : y - 1) * W + x;
+    case 1: return y * W + (x + 1 == W ? 0 : x + 1);
+    case 2: return (y + 1 == H ? 0 : y + 1) * W + x;
+    default: return y * W + (x == 0 ? W - 1 : x - 1);
+  }
+}
+__device__ __forceinline__ uint64_t* wt_agent(const DevHeap& h, const dsr_wator_args& a, uint32_t c) {
+  return field_ptr<uint64_t>(h, a.cells[c], 1);
+}
+__device__ __forceinline__ uint8_t* wt_req(const DevHeap& h, const dsr_wator_args& a, uint32_t c, uint32_t k) {
+  return field_ptr<uint8_t>(h, a.cells[c], 2 + k);
+}
+__device__ __forceinline__ uint32_t wt_pick(const uint32_t* list, uint32_t n, uint64_t key) {
+  return list[(uint32_t)((key >> 32) % n)];
+}
+
+__device__ __forceinline__ uint64_t new_fish(const DevHeap& h, uint32_t c, uint32_t egg) {
+  const uint64_t nh = dsr_new(h, WT_FISH);
+  if (nh) {
+    *field_ptr<uint32_t>(h, nh, 0) = c;
+    *field_ptr<uint32_t>(h, nh, 1) = c;
+    *field_ptr<uint32_t>(h, nh, 2) = egg;
+  }
+  return nh;
+}
+__device__ __forceinline__ uint64_t new_shark(const DevHeap& h, uint32_t c, uint32_t egg, uint32_t energy) {
+  const uint64_t nh = dsr_new(h, WT_SHARK);
+  if (nh) {
+    *field_ptr<uint32_t>(h, nh, 0) = c;
+    *field_ptr<uint32_t>(h, nh, 1) = c;
+    *field_ptr<uint32_t>(h, nh, 2) = egg;
+    *field_ptr<uint32_t>(h, nh, 3) = energy;
+  }
+  return nh;
+}
+
+// ---- parallel_new<Cell>(W*H): constructor i gets id i
+__global__ void __launch_bounds__(256) k_wt_new_cells(DevHeap h, uint64_t n, dsr_wator_args a) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t nh = dsr_new(h, WT_CELL);
+    if (nh) {
+      *field_ptr<uint32_t>(h, nh, 0) = (uint32_t)i;
+      *field_ptr<uint64_t>(h, nh, 1) = 0;
+      for (uint32_t k = 0; k < 5; ++k) *field_ptr<uint8_t>(h, nh, 2 + k) = 0;
+    }
+    a.cells[i] = nh;
+  }
+}
+__global__ void __launch_bounds__(256) k_wt_init_agents(DevHeap h, uint64_t n, dsr_wator_args a) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t c = (uint32_t)i;
+    const uint8_t k = a.kind0[c];
+    uint64_t nh = 0;
+    if (k == 1) nh = new_fish(h, c, a.egg0[c]);
+    else if (k == 2) nh = new_shark(h, c, a.egg0[c], a.energy0[c]);
+    if (k) *wt_agent(h, a, c) = nh;
+  }
+}
+
+struct WtCellPrepare {
+  typedef dsr_wator_args Args;
+  DSR_NO_ACC
+  static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args&, Acc&) {
+#pragma unroll
+    for (uint32_t k = 0; k < 5; ++k) *field_ptr<uint8_t>(h, T, 2 + k, b, s) = 0;
+  }
+};
+
+template <int PHASE>
+struct WtCellDecide {
+  typedef dsr_wator_args Args;
+  DSR_NO_ACC
+  static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args& a, Acc&) {
+    if (*field_ptr<uint8_t>(h, T, 6, b, s)) return;               // own agent stays
+    uint32_t D[4], nd = 0;
+#pragma unroll
+    for (uint32_t d = 0; d < 4; ++d)
+      if (*field_ptr<uint8_t>(h, T, 2 + d, b, s)) D[nd++] = d;
+    if (!nd) return;
+    const uint32_t id = *field_ptr<uint32_t>(h, T, 0, b, s);
+    const uint32_t d = wt_pick(D, nd, rng_key(a.seed, a.step, PHASE, id));
+    const uint64_t ag = *wt_agent(h, a, wt_nbr(a.W, a.H, id, d));
+    *field_ptr<uint32_t>(h, ag, 1) = id;                            // Fish/Shark.target (field 1 of both)
+  }
+};
+
+struct WtFishPrepare {
+  typedef dsr_wator_args Args;
+  DSR_NO_ACC
+  static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args& a, Acc&) {
+    const uint32_t c = *field_ptr<uint32_t>(h, T, 0, b, s);
+    *field_ptr<uint32_t>(h, T, 2, b, s) += 1;
+    *field_ptr<uint32_t>(h, T, 1, b, s) = c;
+    uint32_t fr[4], nf = 0;
+#pragma unroll
+    for (uint32_t d = 0; d < 4; ++d)
+      if (*wt_agent(h, a, wt_nbr(a.W, a.H, c, d)) == 0) fr[nf++] = d;
+    if (nf) {
+      const uint32_t d = wt_pick(fr, nf, rng_key(a.seed, a.step, PH_FISH_REQ, c));
+      *wt_req(h, a, wt_nbr(a.W, a.H, c, d), d ^ 2) = 1;
+    } else {
+      *wt_req(h, a, c, 4) = 1;
+    }
+  }
+};
+
+struct WtFishUpdate {   // allocates Fish (snapshot pass)
+  typedef dsr_wator_args Args;
+  typedef Counters4 Acc;
+  static __device__ __forceinline__ void flush(Acc& acc, const Args& a) { flush_counters4(acc, a.counters); }
+  static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args& a, Acc& acc) {
+    const uint32_t c = *field_ptr<uint32_t>(h, T, 0, b, s);
+    const uint32_t t = *field_ptr<uint32_t>(h, T, 1, b, s);
+    if (t == c) return;
+    *wt_agent(h, a, c) = 0;
+    *wt_agent(h, a, t) = make_handle(T, h.types[T].cap, b, s);
+    *field_ptr<uint32_t>(h, T, 0, b, s) = t;
+    uint32_t* egg = field_ptr<uint32_t>(h, T, 2, b, s);
+    if (*egg >= a.FB) {
+      *egg = 0;
+      *wt_agent(h, a, c) = new_fish(h, c, 0);
+      acc.c[0] += 1;
+    }
+  }
+};
+
+struct WtSharkPrepare {
+  typedef dsr_wator_args Args;
+  DSR_NO_ACC
+  static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args& a, Acc&) {
+    const uint32_t c = *field_ptr<uint32_t>(h, T, 0, b, s);
+    *field_ptr<uint32_t>(h, T, 2, b, s) += 1;
+    uint32_t* en = field_ptr<uint32_t>(h, T, 3, b, s);
+    *en -= 1;
+    *field_ptr<uint32_t>(h, T, 1, b, s) = c;
+    if (*en == 0) return;                                           // starves in Shark.update
+    uint32_t fd[4], nfd = 0, fr[4], nfr = 0;
+#pragma unroll
+    for (uint32_t d = 0; d < 4; ++d) {
+      const uint64_t ag = *wt_agent(h, a, wt_nbr(a.W, a.H, c, d));
+      if (ag == 0) fr[nfr++] = d;
+      else if (h_is(ag, WT_FISH)) fd[nfd++] = d;
+    }
+    const uint64_t key = rng_key(a.seed, a.step, PH_SHARK_REQ, c);
+    if (nfd) {
+      const uint32_t d = wt_pick(fd, nfd, key);
+      *wt_req(h, a, wt_nbr(a.W, a.H, c, d), d ^ 2) = 1;
+    } else if (nfr) {
+      const uint32_t d = wt_pick(fr, nfr, key);
+      *wt_req(h, a, wt_nbr(a.W, a.H, c, d), d ^ 2) = 1;
+    } else {
+      *wt_req(h, a, c, 4) = 1;
+    }
+  }
+};
+
+struct WtSharkUpdate {  // allocates Shark (snapshot pass); destroys Fish and itself
+  typedef dsr_wator_args Args;
+  typedef Counters4 Acc;
+  static __device__ __forceinline__ void flush(Acc& acc, const Args& a) { flush_counters4(acc, a.counters); }
+  static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args& a, Acc& acc) {
+    const uint32_t c = *field_ptr<uint32_t>(h, T, 0, b, s);
+    const uint64_t self = make_handle(T, h.types[T].cap, b, s);
+    uint32_t* en = field_ptr<uint32_t>(h, T, 3, b, s);
+    if (*en == 0) {
+      *wt_agent(h, a, c) = 0;
+      dsr_destroy(h, self);                                         // self-delete
+      acc.c[3] += 1;
+      return;
+    }
+    const uint32_t t = *field_ptr<uint32_t>(h, T, 1, b, s);
+    if (t == c) return;
+    uint64_t* at = wt_agent(h, a, t);
+    const uint64_t prey = *at;
+    if (prey && h_is(prey, WT_FISH)) {
+      dsr_destroy(h, prey);                                         // another type
+      *en = a.SS;
+      acc.c[2] += 1;
+    }
+    *wt_agent(h, a, c) = 0;
+    *at = self;
+    *field_ptr<uint32_t>(h, T, 0, b, s) = t;
+    uint32_t* egg = field_ptr<uint32_t>(h, T, 2, b, s);
+    if (*egg >= a.SB) {
+      *egg = 0;
+      *wt_agent(h, a, c) = new_shark(h, c, 0, a.SS);
+      acc.c[1] += 1;
+    }
+  }
+};
+
+struct WtDump {
+  typedef dsr_wator_args Args;
+  DSR_NO_ACC
+  static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args& a, Acc&) {
+    const uint32_t c = *field_ptr<uint32_t>(h, T, 0, b, s);
+    a.out_kind[c] = T == WT_FISH ? 1u : 2u;
+    a.out_egg[c] = *field_ptr<uint32_t>(h, T, 2, b, s);
+    a.out_energy[c] = T == WT_SHARK ? *field_ptr<uint32_t>(h, T, 3, b, s) : 0u;
+  }
+};
+
+bool wt_method_info(uint32_t id, MethodInfo* mi) {
+  switch (id) {
+    case DSR_M_WT_CELL_PREPARE: case DSR_M_WT_FISH_PREPARE: case DSR_M_WT_CELL_DECIDE_FISH:
+    case DSR_M_WT_SHARK_PREPARE: case DSR_M_WT_CELL_DECIDE_SHARK: case DSR_M_WT_DUMP:
+      *mi = {0, sizeof(dsr_wator_args)}; return true;
+    case DSR_M_WT_FISH_UPDATE: case DSR_M_WT_SHARK_UPDATE:
+      *mi = {1, sizeof(dsr_wator_args)}; return true;
+  }
+  return false;
+}
+
+bool wt_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot, const void* args) {
+  switch (id) {
+    case DSR_M_WT_CELL_PREPARE: launch_doall<WtCellPrepare>(c, T, snapshot, args); return true;
+    case DSR_M_WT_FISH_PREPARE: launch_doall<WtFishPrepare>(c, T, snapshot, args); return true;
+    case DSR_M_WT_CELL_DECIDE_FISH: launch_doall<WtCellDecide<PH_FISH_DEC>>(c, T, snapshot, args); return true;
+    case DSR_M_WT_FISH_UPDATE: launch_doall<WtFishUpdate>(c, T, snapshot, args); return true;
+    case DSR_M_WT_SHARK_PREPARE: launch_doall<WtSharkPrepare>(c, T, snapshot, args); return true;
+    case DSR_M_WT_CELL_DECIDE_SHARK: launch_doall<WtCellDecide<PH_SHARK_DEC>>(c, T, snapshot, args); return true;
+    case DSR_M_WT_SHARK_UPDATE: launch_doall<WtSharkUpdate>(c, T, snapshot, args); return true;
+    case DSR_M_WT_DUMP: launch_doall<WtDump>(c, T, snapshot, args); return true;
+  }
+  return false;
+}
+
+bool wt_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* args, size_t bytes, int* ok) {
+  *ok = 1;
+  if (id != DSR_K_WT_INIT_AGENTS) return false;
+  if (bytes != sizeof(dsr_wator_args) || c.h.ntypes < 3) { *ok = 0; return true; }
+  const dsr_wator_args a = *(const dsr_wator_args*)args;
+  if ((uint64_t)a.W * a.H != n) { *ok = 0; return true; }
+  k_wt_init_agents<<<grid_for(c, n), 256, 0, c.st>>>(c.h, n, a);
+  count_launch();
+  return true;
+}
+
+bool wt_ctor_launch(uint32_t id, const LaunchCtx& c, uint32_t T, uint64_t n, const void* args, size_t bytes, int* ok) {
+  *ok = 1;
+  if (id != DSR_C_WT_CELL) return false;
+  if (bytes != sizeof(dsr_wator_args) || T != WT_CELL || c.h.ntypes < 3) { *ok = 0; return true; }
+  const dsr_wator_args a = *(const dsr_wator_args*)args;
+  if ((uint64_t)a.W * a.H != n) { *ok = 0; return true; }
+  k_wt_new_cells<<<grid_for(c, n), 256, 0, c.st>>>(c.h, n, a);
+  count_launch();
+  return true;
+}
+
 }  // namespace dsr

@@ -5,12 +5,14 @@
 // warp-aggregated object allocator (Algs. 1-2 P:375-426, request coalescing
 // and bitmap rotation P:646-654, n-th set bit P:689).
 //
-// Memory model (reading R-MEMORY / C21): every bitmap word is modified with
-// 64-bit relaxed device-scope atomics (atom.global.{or,and}.b64); plain reads
-// of shared words are ld.relaxed.gpu.  initialize_block writes the type id,
-// then fence (__threadfence = fence.sc.gpu), then the object bitmap; a thread
-// whose atomicOr reserved a slot fences before reading the type (Alg. 1 l.10,
-// footnote P:1091) -- fence-fence synchronisation through the bitmap word.
+// Memory model (reading R-MEMORY / C21): bitmap words are modified with 64-bit
+// device-scope atomics; plain reads of shared words are ld.relaxed.gpu.
+// initialize_block stores the type id, then the object bitmap with
+// st.release (the paper's "volatile write; threadfence; volatile write",
+// Alg. 8); slot reservation and invalidation use atom.acquire so the type id
+// and the fields read afterwards are those of the initialised block (Alg. 1
+// l.10, footnote P:1091); a slot free uses atom.release so the freeing lanes'
+// last reads/writes of the objects precede any reuse of the slots.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -85,6 +87,21 @@ __device__ __forceinline__ void st_relaxed_u8(uint8_t* p, uint32_t v) {
 }
 __device__ __forceinline__ uint64_t atom_or(uint64_t* p, uint64_t m) { return atomicOr((ull*)p, (ull)m); }
 __device__ __forceinline__ uint64_t atom_and(uint64_t* p, uint64_t m) { return atomicAnd((ull*)p, (ull)m); }
+// acquire: later reads of the block (type id, fields) are ordered after the RMW
+__device__ __forceinline__ uint64_t atom_or_acquire(uint64_t* p, uint64_t m) {
+  uint64_t old;
+  asm volatile("atom.acquire.gpu.global.or.b64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(m) : "memory");
+  return old;
+}
+// release: earlier reads / writes of the freed objects are ordered before the RMW
+__device__ __forceinline__ uint64_t atom_and_release(uint64_t* p, uint64_t m) {
+  uint64_t old;
+  asm volatile("atom.release.gpu.global.and.b64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(m) : "memory");
+  return old;
+}
+__device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ uint64_t rotr64(uint64_t x, uint32_t r) { return r ? (x >> r) | (x << (64 - r)) : x; }
 __device__ __forceinline__ uint64_t rotl64(uint64_t x, uint32_t r) { return r ? (x << r) | (x >> (64 - r)) : x; }
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
@@ -234,8 +251,7 @@ __device__ __forceinline__ int64_t bm_clear_any(const DevHeap& h, const DevBitma
 // Alg. 8: type <- T; fence; bitmap <- padding mask
 __device__ __forceinline__ void init_block(const DevHeap& h, uint32_t T, uint32_t bid) {
   st_relaxed_u8(h.type + bid, T + 1);
-  __threadfence();
-  st_relaxed(h.alloc_bm + bid, h.types[T].pad);
+  st_release(h.alloc_bm + bid, h.types[T].pad);          // type store ordered before the bitmap store
 }
 
 // Alg. 6 generalised to a coalesced multi-slot reservation: pick up to `need`
@@ -251,7 +267,7 @@ __device__ __forceinline__ uint64_t block_reserve(const DevHeap& h, uint32_t bid
     uint64_t rf = rotr64(fr, rot);
     if ((uint32_t)__popcll(rf) > need) rf &= (2ull << nth_bit(rf, need - 1)) - 1ull;   // first `need` bits
     const uint64_t sel = rotl64(rf, rot);
-    const uint64_t before = atom_or(w, sel);
+    const uint64_t before = atom_or_acquire(w, sel);       // acquire: type id / fields read after
     const uint64_t got = sel & ~before;
     if (got) { *before_out = before; return got; }
     stat_add(h, ST_RESRETRY, 1);
@@ -264,7 +280,7 @@ __device__ __forceinline__ uint64_t block_reserve(const DevHeap& h, uint32_t bid
 __device__ __forceinline__ bool block_invalidate(const DevHeap& h, uint32_t bid) {
   uint64_t* w = h.alloc_bm + bid;
   for (;;) {
-    const uint64_t before = atom_or(w, ~0ull);
+    const uint64_t before = atom_or_acquire(w, ~0ull);
     if (before == ~0ull) return false;
     const uint32_t t = ld_relaxed_u8(h.type + bid) - 1u;   // fixed while we hold invalidated bits
     const uint64_t pad = h.types[t].pad;
@@ -280,7 +296,7 @@ __device__ __forceinline__ bool block_invalidate(const DevHeap& h, uint32_t bid)
 // FIRST iff before == ~0; EMPTY iff the remaining bits are padding only;
 // both at once: activate, then invalidate (reading R-FIRSTEMPTY / C17).
 __device__ __forceinline__ void block_free(const DevHeap& h, uint32_t T, uint32_t bid, uint64_t mask) {
-  const uint64_t before = atom_and(h.alloc_bm + bid, ~mask);
+  const uint64_t before = atom_and_release(h.alloc_bm + bid, ~mask);
   const bool first = before == ~0ull;
   const bool empty = (before & ~mask) == h.types[T].pad;
   if (first) bm_set(h.activebm[T], bid);
@@ -322,7 +338,6 @@ static __device__ __noinline__ uint64_t reserve_chunk(const DevHeap& h, uint32_t
     const uint32_t rot = (uint32_t)(rot_hash(h, who, iter * 16 + 15) >> 58);
     const uint64_t got = block_reserve(h, (uint32_t)bid, need, rot, &before);
     if (!got) continue;                                                       // full or invalidated
-    __threadfence();                                                          // acquire the type id
     const uint32_t t = ld_relaxed_u8(h.type + bid) - 1u;                      // volatile read (Alg. 1 l.10)
     if ((before | got) == ~0ull) bm_clear(h.activebm[t], (uint64_t)bid);      // FULL -> inactive (l.12)
     if (t == T) { *bid_out = (uint32_t)bid; return got; }
@@ -357,6 +372,7 @@ __device__ __forceinline__ uint64_t dsr_new(const DevHeap& h, uint32_t T) {
     done += n;
   }
   if (lane == leader) stat_add(h, ST_ALLOCS, done);
+  __syncwarp(peers);   // the leader's acquire orders the lanes' constructor writes after the reservation
   return mine;
 }
 
@@ -372,6 +388,7 @@ __device__ __forceinline__ void dsr_destroy(const DevHeap& h, uint64_t x) {
   const uint64_t bit = 1ull << h_slot(x);
   const uint32_t lo = __reduce_or_sync(peers, (uint32_t)bit);
   const uint32_t hi = __reduce_or_sync(peers, (uint32_t)(bit >> 32));
+  __syncwarp(peers);   // memory ordering among the lanes: their object accesses precede the leader's release
   if (lane == leader) {
     const uint64_t mask = ((uint64_t)hi << 32) | lo;
     block_free(h, h_type(x), h_bid(x), mask);

@@ -1,0 +1,95 @@
+"""GPU parity of Wa-Tor (BASELINE configs[1]) and N-body with collisions
+(configs[2]) against the oracle."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1810_11765_b200 import build
+    build.build()
+    import paper_1810_11765_b200 as pkg
+    from paper_1810_11765_b200 import inputs, nbody, wator
+    return pkg
+
+
+WT = dict(FB=6, SB=12, SS=6, seed=42)
+
+
+@pytest.mark.parametrize("W,H,seed", [(64, 64, 5), (48, 32, 9), (200, 120, 3)])
+def test_wator_every_step_bit_exact(P, O, W, H, seed):
+    from paper_1810_11765_b200 import inputs as I, wator
+    kind, egg, en = I.wator_init(W, H, seed=seed)
+    sim = wator.WaTor(kind, egg, en, **WT)
+    k, e, n = kind, egg, en
+    prev = [0, 0, 0, 0]
+    for s in range(60):
+        k, e, n, c = O.wator_run(k, e, n, steps=1, step0=s, **WT)
+        sim.step()
+        gk, ge, gn = sim.state()
+        assert np.array_equal(gk, k) and np.array_equal(ge, e) and np.array_equal(gn, n), f"step {s}"
+        cur = sim.read_counters()
+        assert [a - b for a, b in zip(cur, prev)] == [int(c[0, 2]), int(c[0, 3]), int(c[0, 4]), int(c[0, 5])]
+        prev = cur
+        assert sim.heap.live_count(0) == int(c[0, 0]) and sim.heap.live_count(1) == int(c[0, 1])
+    assert sim.heap.poll_error() == 0
+    assert sim.heap.check_invariants() == 0
+
+
+def test_wator_2048_prefix_against_oracle(P, O):
+    """BASELINE configs[1] grid (2048^2, seed 42) for 10 steps."""
+    from paper_1810_11765_b200 import inputs as I, wator
+    kind, egg, en = I.wator_init(2048, 2048, seed=42)
+    sim = wator.WaTor(kind, egg, en, **WT)
+    sim.run(10)
+    gk, ge, gn = sim.state()
+    k, e, n, c = O.wator_run(kind, egg, en, steps=10, **WT)
+    assert np.array_equal(gk, k) and np.array_equal(ge, e) and np.array_equal(gn, n)
+    assert sim.heap.check_invariants() == 0
+
+
+def rel_pos_err(a, b):
+    den = np.maximum(np.maximum(np.abs(a), np.abs(b)), 1e-3)
+    return float(np.max(np.abs(a.astype(np.float64) - b.astype(np.float64)) / den))
+
+
+@pytest.mark.parametrize("n,steps,merges", [(2048, 10, True), (4096, 10, False), (1000, 10, True)])
+def test_nbody_against_oracle(P, O, n, steps, merges):
+    from paper_1810_11765_b200 import inputs as I, nbody
+    st = I.nbody_init(n, seed=7)
+    prm = dict(I.NBODY_PARAMS)
+    prm["R"] = 0.02 if merges else prm["R"]          # denser merging at small n
+    prm["G"] = 1e-7
+    sim = nbody.NBody(st, merges=merges, **prm)
+    sim.run(steps)
+    got = sim.state()
+    want = O.nbody_run(st, merges=merges, steps=steps, **prm)
+    assert np.array_equal(got["alive"], want["alive"])
+    al = want["alive"] == 1
+    for k in ("x", "y"):
+        assert rel_pos_err(got[k][al], want[k][al]) <= 1e-4, k
+    m0 = float(st["m"].astype(np.float64).sum())
+    assert abs(float(got["m"][al].astype(np.float64).sum()) - m0) <= 1e-5 * m0
+    assert sim.heap.live_count(0) == int(al.sum())
+    assert sim.heap.check_invariants() == 0
+
+
+@pytest.mark.slow
+def test_nbody_65536_one_step(P, O):
+    from paper_1810_11765_b200 import inputs as I, nbody
+    st = I.nbody_init(65536, seed=7)
+    prm = dict(I.NBODY_PARAMS)
+    sim = nbody.NBody(st, merges=True, **prm)
+    sim.run(1)
+    got = sim.state()
+    want = O.nbody_run(st, merges=True, steps=1, **prm)
+    assert np.array_equal(got["alive"], want["alive"])
+    assert (want["alive"] == 0).sum() > 100
+    al = want["alive"] == 1
+    assert rel_pos_err(got["x"][al], want["x"][al]) <= 1e-4
+    assert rel_pos_err(got["y"][al], want["y"][al]) <= 1e-4

@@ -1,0 +1,75 @@
+"""GPU parity of the Game of Life workload (BASELINE configs[0] / [3]) against
+the oracle: canonical (cell, kind, is_new, action) records bit-exact every
+generation at 64x64, alive bitmaps against the oracle's dense Life at larger
+sizes, and the heap invariants after the run."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def G():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1810_11765_b200 import build, gol
+    build.build()
+    return gol
+
+
+@pytest.mark.parametrize("name", ["glider", "blinker", "soup1", "soup2", "soup3"])
+def test_gol_64_every_generation_bit_exact(G, O, name):
+    from paper_1810_11765_b200 import inputs as I
+    a0 = I.gol_pattern(name) if not name.startswith("soup") else I.gol_soup(64, 64, 0.3, int(name[-1]))
+    _, want = O.gol_run(a0, 100, dump=True)
+    g = G.GameOfLife(a0)
+    for gen in range(100):
+        g.generation()
+        got = g.records()
+        assert np.array_equal(got, want[gen]), f"generation {gen + 1}"
+    assert g.heap.poll_error() == 0
+    assert g.heap.check_invariants() == 0
+
+
+@pytest.mark.parametrize("W,H,p,seed,gens", [(37, 23, 0.4, 4, 60), (3, 3, 0.5, 6, 10), (512, 384, 0.25, 7, 50)])
+def test_gol_ragged_sizes_against_dense_life(G, O, W, H, p, seed, gens):
+    from paper_1810_11765_b200 import inputs as I
+    a0 = I.gol_soup(W, H, p, seed)
+    g = G.GameOfLife(a0)
+    g.run(gens)
+    assert np.array_equal(g.alive(), O.life_dense(a0, gens))
+    assert g.heap.check_invariants() == 0
+
+
+def test_gol_tiny_heap_forces_block_reuse(G, O):
+    """A heap barely larger than the live set: blocks are freed and re-typed
+    every generation (Alive <-> Candidate), exercising invalidation and rollback."""
+    from paper_1810_11765_b200 import inputs as I
+    a0 = I.gol_soup(64, 64, 0.3, 9)
+    g = G.GameOfLife(a0, heap_bytes=600_000)
+    g.run(100)
+    assert g.heap.poll_error() == 0
+    assert np.array_equal(g.alive(), O.life_dense(a0, 100))
+    assert g.heap.check_invariants() == 0
+
+
+@pytest.mark.slow
+def test_gol_16384_sampled_against_dense(G, O):
+    """BASELINE configs[3] size (16384^2, p = 0.25) for 3 generations: the
+    oracle's dense Life runs on 9 sampled 256x256 windows whose 3-generation
+    light cone is included (border of 3 cells)."""
+    from paper_1810_11765_b200 import inputs as I
+    W = H = 16384
+    a0 = I.gol_soup(W, H, 0.25, 42)
+    g = G.GameOfLife(a0)
+    gens = 3
+    g.run(gens)
+    got = g.alive()
+    rng = np.random.default_rng(0)
+    for _ in range(9):
+        y, x = int(rng.integers(0, H - 300)), int(rng.integers(0, W - 300))
+        win = a0[y:y + 262, x:x + 262]
+        want = O.life_dense(np.ascontiguousarray(win), gens)[3:259, 3:259]   # torus wrap only hits the border
+        assert np.array_equal(got[y + 3:y + 259, x + 3:x + 259], want)
+    assert g.heap.check_invariants() == 0
