@@ -313,21 +313,33 @@ __device__ __forceinline__ void block_free(const DevHeap& h, uint32_t T, uint32_
 
 // Alg. 1 for one coalesced request of `need` slots (leader lane only).
 // Returns the reserved slot mask (0 = OOM) and the block in *bid_out.
-static __device__ __noinline__ uint64_t reserve_chunk(const DevHeap& h, uint32_t T, uint32_t need, uint32_t* bid_out) {
+// An "active block lookup attempt" (Fig. 11) fails when
+// try_find_set FAILs or when the block it returned yields no slot (full or
+// invalidated meanwhile); after r failed attempts the leader takes the slow
+// path (reading R-RETRY).  Sequentially this is exactly Alg. 1.
+static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint32_t T, uint32_t need, uint32_t* bid_out) {
   const uint64_t who = warp_gid();
-  uint32_t oom_tries = 0;
+  uint32_t oom_tries = 0, fails = 0;
   for (uint64_t iter = 0;; ++iter) {
     int64_t bid = -1;
-    for (uint32_t a = 0; a < h.r_attempts && bid < 0; ++a)                  // r attempts
-      bid = bm_try_find_set(h.activebm[T], rot_hash(h, who, iter * 16 + a));
-    if (bid < 0) {                                                            // slow path
-      bid = bm_clear_any(h, h.freebm, who, iter * 16 + 8);
+    if (fails < h.r_attempts) {
+      bid = bm_try_find_set(h.activebm[T], rot_hash(h, who, iter));
+      if (bid < 0) { ++fails; continue; }
+    } else {                                                                  // slow path
+      bid = bm_clear_any(h, h.freebm, who, iter << 8);
       if (bid < 0) {
-        // free bitmap empty (or transiently inconsistent): look for active blocks again
-        if ((h.flags & DSR_F_SPIN_ON_OOM) || ++oom_tries < 64) { uint32_t ns = 128; backoff(ns); continue; }
-        flag_error(h, ERRB_OOM);
-        stat_add(h, ST_OOM, 1);
-        return 0;
+        // FAIL: free bitmap empty, or transiently inconsistent.  Only a
+        // top-level word of 0 counts towards OOM.
+        if (ld_relaxed(h.freebm.lvl[h.freebm.nlevels - 1]) == 0 && !(h.flags & DSR_F_SPIN_ON_OOM) &&
+            ++oom_tries >= 64) {
+          flag_error(h, ERRB_OOM);
+          stat_add(h, ST_OOM, 1);
+          return 0;
+        }
+        uint32_t ns = 128;
+        backoff(ns);
+        fails = 0;                                                            // look for active blocks again
+        continue;
       }
       init_block(h, T, (uint32_t)bid);
       bm_set(h.allocbm[T], (uint64_t)bid);
@@ -335,9 +347,9 @@ static __device__ __noinline__ uint64_t reserve_chunk(const DevHeap& h, uint32_t
       stat_add(h, ST_INITS, 1);
     }
     uint64_t before = 0;
-    const uint32_t rot = (uint32_t)(rot_hash(h, who, iter * 16 + 15) >> 58);
+    const uint32_t rot = (uint32_t)(rot_hash(h, who, iter + 0x1000) >> 58);
     const uint64_t got = block_reserve(h, (uint32_t)bid, need, rot, &before);
-    if (!got) continue;                                                       // full or invalidated
+    if (!got) { ++fails; continue; }                                          // full or invalidated
     const uint32_t t = ld_relaxed_u8(h.type + bid) - 1u;                      // volatile read (Alg. 1 l.10)
     if ((before | got) == ~0ull) bm_clear(h.activebm[t], (uint64_t)bid);      // FULL -> inactive (l.12)
     if (t == T) { *bid_out = (uint32_t)bid; return got; }

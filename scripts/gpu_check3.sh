@@ -1,0 +1,11 @@
+#!/bin/bash
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+timeout -s KILL 1500 python -m pytest tests -m "gpu and not slow" -q --timeout 600 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
+rm -f gpurun_out/prof_mb.log
+for f in 4 0; do timeout -s KILL 120 python scripts/prof_mb.py $f >> gpurun_out/prof_mb.log 2>&1; done
+for r in 1 2 8; do timeout -s KILL 120 python scripts/prof_mb.py 4 $r >> gpurun_out/prof_mb.log 2>&1; done
+timeout -s KILL 120 python scripts/prof_mb.py 6 >> gpurun_out/prof_mb.log 2>&1
+timeout -s KILL 600 ncu --set full --import-source on --clock-control none -k regex:k_mb_new -s 2 -c 1 -o gpurun_out/prof_mbnew3 python scripts/prof_mb.py 0 > gpurun_out/ncu_mbnew.log 2>&1
+timeout -s KILL 300 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1
