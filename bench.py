@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="microbench", choices=["microbench"])
+    ap.add_argument("--workload", default="microbench", choices=["microbench", "wator", "gol", "gol16k", "nbody"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -118,13 +118,15 @@ def dist_init(n):
     return rank, world, local
 
 
-def allreduce(vals, op):
+def reduce_over_ranks(vals, op, device="cuda"):
+    """Sum ("sum") or max ("max") of a list of floats over all ranks (identity
+    without an initialised process group)."""
     import torch
     import torch.distributed as dist
-    if not (dist.is_available() and dist.is_initialized()):
-        return vals
-    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=op)
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return list(vals)
+    t = torch.tensor(vals, dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX)
     return t.tolist()
 
 
@@ -260,8 +262,8 @@ def run_ours(args):
     e2e_ms = e0.elapsed_time(e1) / K
 
     # ---- aggregate over ranks (max time, sum of work)
-    tot_updates, = allreduce([float(updates)], dist.ReduceOp.SUM if world > 1 else None) if world > 1 else [updates]
-    ms_max, e2e_max = (allreduce([ms, e2e_ms], dist.ReduceOp.MAX) if world > 1 else [ms, e2e_ms])
+    tot_updates, = reduce_over_ranks([float(updates)], "sum")
+    ms_max, e2e_max = reduce_over_ranks([ms, e2e_ms], "max")
     value = tot_updates / (ms_max * 1e-3)
     e2e_value = tot_updates / (e2e_max * 1e-3)
 
@@ -304,10 +306,86 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------- per-app lines (not the default)
+def time_steps(step, K, W, stream, per_step=None):
+    """W untimed steps, then K steps between CUDA events on `stream`; returns ms/step."""
+    import torch
+    for _ in range(W):
+        step()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for k in range(K):
+        step()
+        if per_step is not None:
+            per_step(k)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    return t0.elapsed_time(t1) / K
+
+
+def run_app(args):
+    """Object-updates/s of one BASELINE app config at N = 1 (diagnostic lines;
+    the driver's bench line is the microbenchmark)."""
+    import numpy as np
+    import torch
+    from paper_1810_11765_b200 import dsr, inputs as I
+    torch.cuda.set_device(0)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    K, W = args.steps, args.warmup
+    live = torch.zeros(K, 3, dtype=torch.int64, device="cuda")
+    if args.workload == "wator":
+        from paper_1810_11765_b200.wator import WaTor
+        kind, egg, en = I.wator_init(2048, 2048, seed=42)
+        sim = WaTor(kind, egg, en, FB=6, SB=12, SS=6, seed=42, stream=stream)
+
+        def per(k):
+            for t in range(2):
+                sim.heap.live_count_async(t, live[k, t], stream)
+        ms = time_steps(sim.step, K, W, stream, per)
+        lv = live.cpu().numpy()
+        # visits of step k: 4 cell passes + 2 passes over the fish and sharks alive at its start
+        starts = np.vstack([lv[:1] * 0 + lv[0], lv[:-1]])       # approx: counts at the previous step end
+        visits = 4 * 2048 * 2048 * K + 2 * int(starts[:, 0].sum() + starts[:, 1].sum())
+        cfg = {"workload": "wator (BASELINE configs[1]) 2048^2, FB6 SB12 SS6, seed 42"}
+    elif args.workload in ("gol", "gol16k"):
+        from paper_1810_11765_b200.gol import GameOfLife
+        Wd = 64 if args.workload == "gol" else 16384
+        a0 = I.gol_soup(Wd, Wd, 0.3 if Wd == 64 else 0.25, 1 if Wd == 64 else 42)
+        sim = GameOfLife(a0, stream=stream)
+
+        def per(k):
+            for t in range(2):
+                sim.heap.live_count_async(t, live[k, t], stream)
+        ms = time_steps(sim.generation, K, W, stream, per)
+        lv = live.cpu().numpy()
+        visits = 2 * int(lv[:, 0].sum() + lv[:, 1].sum())
+        cfg = {"workload": f"gol {Wd}^2 torus (BASELINE configs[{0 if Wd == 64 else 3}])"}
+    else:
+        from paper_1810_11765_b200.nbody import NBody
+        st = I.nbody_init(65536, seed=7)
+        sim = NBody(st, merges=True, stream=stream, **I.NBODY_PARAMS)
+
+        def per(k):
+            sim.heap.live_count_async(0, live[k, 0], stream)
+        ms = time_steps(sim.step, K, W, stream, per)
+        lv = live.cpu().numpy()
+        visits = 8 * int(lv[:, 0].sum())
+        cfg = {"workload": "nbody with merging (BASELINE configs[2]) 65536 bodies", "pairs_per_step": 2 * 65536 ** 2,
+               "pair_interactions_per_s": 2 * 65536 ** 2 / (ms * 1e-3)}
+    print(json.dumps({"metric": METRIC, "value": visits / K / (ms * 1e-3), "unit": "object-updates/s",
+                      "n_gpus": 1, "steps": K, "warmup": W, "ms_per_step": ms, "higher_is_better": True,
+                      "dtype": "u32" if args.workload != "nbody" else "f32", "data": "synthetic", "config": cfg,
+                      "gpu_launches_per_step": None}), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload != "microbench":
+        run_app(args)
     else:
         run_ours(args)
 

@@ -279,27 +279,34 @@ enum {
 
 /* ---- N-body with collisions (BASELINE configs[2], reading R-NBODY) ----
  * type 0 = Body{x, y, vx, vy, fx, fy, m: f32; id, target, incoming: u32; merged: u8}
- * Snapshot S: id-indexed SOA device arrays of length n (sm = 0 for dead ids). */
+ * Id-indexed device arrays of length n_total shared by all passes (on every
+ * rank of a multi-GPU run; the rank owns ids [id_lo, id_hi)):
+ *   S[4*id + {0,1,2,3}] = (x, y, m, 0) snapshot (m = 0: dead id)
+ *   V[2*id + {0,1}]     = (vx, vy) snapshot
+ *   target[id], incoming[id] (u32, 0xFFFFFFFF = NONE), shandle[id] (local handles only) */
 typedef struct {
-  float *sx, *sy, *sm, *svx, *svy;    /* snapshot arrays */
-  uint64_t* shandle;                  /* id -> handle */
-  const float *x0, *y0, *vx0, *vy0, *m0;  /* init only */
+  float* S;
+  float* V;
+  uint32_t* target;
+  uint32_t* incoming;
+  uint64_t* shandle;
+  const float *x0, *y0, *vx0, *vy0, *m0;  /* init only: id_hi - id_lo bodies */
   float G, dt, eps, R;
-  uint32_t n;
-  uint32_t id_offset;                 /* first id owned by this rank */
-  float* out;                         /* dump: 6 floats per id (x,y,vx,vy,m,alive) */
+  uint32_t n_total, id_lo, id_hi;
+  float* out;                         /* dump: 6 floats per id (x, y, vx, vy, m, alive) */
 } dsr_nbody_args;
 enum {
-  DSR_C_NB_BODY = 30,            /* parallel_new<Body>(n): body i from x0..m0 */
-  DSR_M_NB_SNAPSHOT = 30,        /* S[id] = (x, y, m, vx, vy), shandle[id] = this */
-  DSR_M_NB_FORCE = 31,           /* compute_force: tiled all-pairs over S (device_do) */
+  DSR_C_NB_BODY = 30,            /* parallel_new<Body>(id_hi - id_lo): body i gets id id_lo + i */
+  DSR_M_NB_SNAPSHOT = 30,        /* S[id], V[id] = own state; shandle[id] = this */
+  DSR_M_NB_FORCE = 31,           /* compute_force for own ids: tiled all-pairs over S (device_do) */
   DSR_M_NB_MOVE = 32,
-  DSR_M_NB_PREPARE_MERGE = 33,
-  DSR_M_NB_CLAIM = 34,
+  DSR_M_NB_PREPARE_MERGE = 33,   /* target[id] for own ids over S */
+  DSR_M_NB_CLAIM = 34,           /* over ALL ids (redundant per rank): incoming[target[i]] = min i */
   DSR_M_NB_ABSORB = 35,
-  DSR_M_NB_DELETE_MERGED = 36,
+  DSR_M_NB_DELETE_MERGED = 36,   /* destroy(this) iff incoming[target] == id and target[target] == NONE */
   DSR_M_NB_DUMP = 37,
-  DSR_K_NB_CLEAR_SNAPSHOT = 30   /* n = ids: sm[i] = 0 */
+  DSR_K_NB_CLEAR_SNAPSHOT = 30,  /* n = n_total: S.m = 0, shandle = 0, target = incoming = NONE */
+  DSR_K_NB_CLAIM = 31            /* n = n_total: the claim pass over the (gathered) target array */
 };
 
 #ifdef __cplusplus

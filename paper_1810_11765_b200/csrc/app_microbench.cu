@@ -185,8 +185,8 @@ __global__ void __launch_bounds__(256) k_torture(DevHeap h, uint64_t nthreads, d
 bool mb_method_info(uint32_t id, MethodInfo* mi) {
   switch (id) {
     case DSR_M_MB_REDUCE: *mi = {0, sizeof(dsr_mb_reduce_args)}; return true;
-    case DSR_M_MB_FREE_ODD: *mi = {0, 0}; return true;
-    case DSR_M_MB_FREE_ALL: *mi = {0, 0}; return true;
+    case DSR_M_MB_FREE_ODD: *mi = {1, 0}; return true;      // self-delete
+    case DSR_M_MB_FREE_ALL: *mi = {1, 0}; return true;
     case DSR_M_COLLECT: *mi = {0, sizeof(dsr_collect_args)}; return true;
   }
   return false;

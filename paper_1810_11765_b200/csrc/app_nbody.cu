@@ -4,10 +4,13 @@
 //
 // device_do -- the sequential all-bodies loop inside each
 // body's method -- becomes a tiled all-pairs gather over an id-indexed SOA
-// snapshot S (x, y, m, vx, vy, handle) that a preceding do-all writes: each
-// CTA stages 256 snapshot entries in shared memory and every thread sums its
-// body's interactions tile by tile in id order (same terms as the paper's
-// loop, deterministic order).  Dead ids have m = 0 in S and contribute 0.
+// snapshot S (x, y, m) written by the preceding snapshot do-all: each CTA
+// stages 256 snapshot entries in shared memory and every thread sums its
+// body's interactions tile by tile in id order (the paper's terms, a fixed
+// deterministic order).  Dead ids have m = 0 in S and contribute 0.
+// Merge bookkeeping (target / incoming) lives in id-indexed arrays so that the
+// same kernels serve one GPU and an id-range-sharded multi-GPU run (where S,
+// V and target are all-gathered between passes).
 #include "dsr_host.h"
 
 namespace dsr {
@@ -20,8 +23,11 @@ template <class V>
 __device__ __forceinline__ V& bf(const DevHeap& h, uint32_t b, uint32_t s, int f) {
   return *field_ptr<V>(h, 0, (uint32_t)f, b, s);
 }
+__device__ __forceinline__ float4 s4(const dsr_nbody_args& a, uint32_t id) {
+  return __ldg(reinterpret_cast<const float4*>(a.S) + id);
+}
 
-// ---- parallel_new<Body>(n): body i gets id id_offset + i
+// ---- parallel_new<Body>(n): body i gets id id_lo + i
 __global__ void __launch_bounds__(256) k_nb_new(DevHeap h, uint64_t n, dsr_nbody_args a) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -35,7 +41,7 @@ __global__ void __launch_bounds__(256) k_nb_new(DevHeap h, uint64_t n, dsr_nbody
     bf<float>(h, b, s, NB_FX) = 0.f;
     bf<float>(h, b, s, NB_FY) = 0.f;
     bf<float>(h, b, s, NB_M) = a.m0[i];
-    bf<uint32_t>(h, b, s, NB_ID) = a.id_offset + (uint32_t)i;
+    bf<uint32_t>(h, b, s, NB_ID) = a.id_lo + (uint32_t)i;
     bf<uint32_t>(h, b, s, NB_TARGET) = kNone;
     bf<uint32_t>(h, b, s, NB_INCOMING) = kNone;
     bf<uint8_t>(h, b, s, NB_MERGED) = 0;
@@ -44,8 +50,10 @@ __global__ void __launch_bounds__(256) k_nb_new(DevHeap h, uint64_t n, dsr_nbody
 
 __global__ void k_nb_clear(uint64_t n, dsr_nbody_args a) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    a.sm[i] = 0.f;
+    reinterpret_cast<float4*>(a.S)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     a.shandle[i] = 0;
+    a.target[i] = kNone;
+    a.incoming[i] = kNone;
   }
 }
 
@@ -54,36 +62,34 @@ struct NbSnapshot {
   DSR_NO_ACC
   static __device__ __forceinline__ void run(const DevHeap& h, uint32_t, uint32_t b, uint32_t s, const Args& a, Acc&) {
     const uint32_t id = bf<uint32_t>(h, b, s, NB_ID);
-    a.sx[id] = bf<float>(h, b, s, NB_X);
-    a.sy[id] = bf<float>(h, b, s, NB_Y);
-    a.sm[id] = bf<float>(h, b, s, NB_M);
-    a.svx[id] = bf<float>(h, b, s, NB_VX);
-    a.svy[id] = bf<float>(h, b, s, NB_VY);
+    reinterpret_cast<float4*>(a.S)[id] = make_float4(bf<float>(h, b, s, NB_X), bf<float>(h, b, s, NB_Y),
+                                                     bf<float>(h, b, s, NB_M), 0.f);
+    reinterpret_cast<float2*>(a.V)[id] = make_float2(bf<float>(h, b, s, NB_VX), bf<float>(h, b, s, NB_VY));
     a.shandle[id] = make_handle(0, h.types[0].cap, b, s);
   }
 };
 
-// compute_force: f_i = G m_i sum_j m_j (p_j - p_i) / (|p_j - p_i|^2 + eps^2)^{3/2}
+// compute_force for own ids: f_i = G m_i sum_j m_j (p_j - p_i) / (|p_j - p_i|^2 + eps^2)^{3/2}
 __global__ void __launch_bounds__(kTile) k_nb_force(DevHeap h, dsr_nbody_args a) {
   __shared__ float4 tile[kTile];
-  const uint32_t n = a.n;
+  const uint32_t n = a.n_total, lo = a.id_lo, hi = a.id_hi;
   const float eps2 = a.eps * a.eps;
-  for (uint32_t base = blockIdx.x * kTile; base < n; base += gridDim.x * kTile) {
+  for (uint32_t base = lo + blockIdx.x * kTile; base < hi; base += gridDim.x * kTile) {
     const uint32_t i = base + threadIdx.x;
-    float xi = 0.f, yi = 0.f;
-    uint64_t hi = 0;
-    if (i < n) { hi = a.shandle[i]; xi = a.sx[i]; yi = a.sy[i]; }
+    float4 pi = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint64_t hd = 0;
+    if (i < hi) { hd = a.shandle[i]; pi = s4(a, i); }
     float ax = 0.f, ay = 0.f;
     for (uint32_t j0 = 0; j0 < n; j0 += kTile) {
       __syncthreads();
       const uint32_t j = j0 + threadIdx.x;
-      tile[threadIdx.x] = j < n ? make_float4(a.sx[j], a.sy[j], a.sm[j], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+      tile[threadIdx.x] = j < n ? s4(a, j) : make_float4(0.f, 0.f, 0.f, 0.f);
       __syncthreads();
       const uint32_t lim = (n - j0) < (uint32_t)kTile ? (n - j0) : (uint32_t)kTile;
 #pragma unroll 8
       for (uint32_t k = 0; k < lim; ++k) {
         const float4 p = tile[k];
-        const float dx = p.x - xi, dy = p.y - yi;
+        const float dx = p.x - pi.x, dy = p.y - pi.y;
         const float r2 = fmaf(dx, dx, fmaf(dy, dy, eps2));
         const float inv = rsqrtf(r2);
         const float w = p.z * inv * inv * inv;
@@ -91,8 +97,8 @@ __global__ void __launch_bounds__(kTile) k_nb_force(DevHeap h, dsr_nbody_args a)
         ay = fmaf(dy, w, ay);
       }
     }
-    if (hi) {
-      const uint32_t b = h_bid(hi), s = h_slot(hi);
+    if (hd) {
+      const uint32_t b = h_bid(hd), s = h_slot(hd);
       const float gm = a.G * bf<float>(h, b, s, NB_M);
       bf<float>(h, b, s, NB_FX) = gm * ax;
       bf<float>(h, b, s, NB_FY) = gm * ay;
@@ -117,46 +123,54 @@ struct NbMove {   // semi-implicit Euler, velocity first
   }
 };
 
-// prepare_merge: target_i = argmin_{j : (m_j, j) >lex (m_i, i), d2 < R^2} (d2, j)
+// prepare_merge for own ids: target_i = argmin over j with (m_j, j) >lex (m_i, i) and d2 < R^2 of (d2, j)
 __global__ void __launch_bounds__(kTile) k_nb_merge_search(DevHeap h, dsr_nbody_args a) {
   __shared__ float4 tile[kTile];
-  const uint32_t n = a.n;
+  const uint32_t n = a.n_total, lo = a.id_lo, hi = a.id_hi;
   const float R2 = a.R * a.R;
-  for (uint32_t base = blockIdx.x * kTile; base < n; base += gridDim.x * kTile) {
+  for (uint32_t base = lo + blockIdx.x * kTile; base < hi; base += gridDim.x * kTile) {
     const uint32_t i = base + threadIdx.x;
-    float xi = 0.f, yi = 0.f, mi = 0.f;
-    uint64_t hi = 0;
-    if (i < n) { hi = a.shandle[i]; xi = a.sx[i]; yi = a.sy[i]; mi = a.sm[i]; }
+    float4 pi = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < hi) pi = s4(a, i);
     uint32_t best = kNone;
     float bestd = 0.f;
     for (uint32_t j0 = 0; j0 < n; j0 += kTile) {
       __syncthreads();
       const uint32_t j = j0 + threadIdx.x;
-      tile[threadIdx.x] = j < n ? make_float4(a.sx[j], a.sy[j], a.sm[j], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+      tile[threadIdx.x] = j < n ? s4(a, j) : make_float4(0.f, 0.f, 0.f, 0.f);
       __syncthreads();
-      if (!hi) continue;
+      if (pi.z == 0.f) continue;
       const uint32_t lim = (n - j0) < (uint32_t)kTile ? (n - j0) : (uint32_t)kTile;
       for (uint32_t k = 0; k < lim; ++k) {
         const float4 p = tile[k];
-        const float dx = p.x - xi, dy = p.y - yi;
+        const float dx = p.x - pi.x, dy = p.y - pi.y;
         const float d2 = fmaf(dx, dx, dy * dy);
         const uint32_t jj = j0 + k;
-        const bool heavier = p.z > mi || (p.z == mi && jj > i);
-        if (heavier && p.z > 0.f && d2 < R2 && (best == kNone || d2 < bestd)) { best = jj; bestd = d2; }
+        const bool heavier = p.z > pi.z || (p.z == pi.z && jj > i);
+        if (heavier && d2 < R2 && (best == kNone || d2 < bestd)) { best = jj; bestd = d2; }
       }
     }
-    if (hi) bf<uint32_t>(h, h_bid(hi), h_slot(hi), NB_TARGET) = best;
+    if (i < hi && pi.z != 0.f) {
+      a.target[i] = best;
+      const uint64_t hd = a.shandle[i];
+      bf<uint32_t>(h, h_bid(hd), h_slot(hd), NB_TARGET) = best;
+    }
   }
 }
 
-struct NbClaim {  // at most one absorption per target per step: smallest id wins
+// claim over all ids: at most one absorption per target per step, smallest id wins
+__global__ void k_nb_claim_all(uint64_t n, dsr_nbody_args a) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t t = a.target[i];
+    if (t != kNone) atomicMin(a.incoming + t, (uint32_t)i);
+  }
+}
+struct NbClaim {  // do-all form of the claim (single GPU): incoming[target] = min id
   typedef dsr_nbody_args Args;
   DSR_NO_ACC
   static __device__ __forceinline__ void run(const DevHeap& h, uint32_t, uint32_t b, uint32_t s, const Args& a, Acc&) {
     const uint32_t t = bf<uint32_t>(h, b, s, NB_TARGET);
-    if (t == kNone) return;
-    const uint64_t ht = a.shandle[t];
-    atomicMin(&bf<uint32_t>(h, h_bid(ht), h_slot(ht), NB_INCOMING), bf<uint32_t>(h, b, s, NB_ID));
+    if (t != kNone) atomicMin(a.incoming + t, bf<uint32_t>(h, b, s, NB_ID));
   }
 };
 
@@ -164,25 +178,31 @@ struct NbAbsorb { // perfectly inelastic merge: momentum and centre of mass
   typedef dsr_nbody_args Args;
   DSR_NO_ACC
   static __device__ __forceinline__ void run(const DevHeap& h, uint32_t, uint32_t b, uint32_t s, const Args& a, Acc&) {
-    const uint32_t i = bf<uint32_t>(h, b, s, NB_INCOMING);
-    if (i == kNone || bf<uint32_t>(h, b, s, NB_TARGET) != kNone) return;
-    const float m = bf<float>(h, b, s, NB_M), mi = a.sm[i];
+    const uint32_t id = bf<uint32_t>(h, b, s, NB_ID);
+    const uint32_t i = a.incoming[id];
+    bf<uint32_t>(h, b, s, NB_INCOMING) = i;
+    if (i == kNone || a.target[id] != kNone) return;
+    const float4 pi = s4(a, i);
+    const float2 vi = reinterpret_cast<const float2*>(a.V)[i];
+    const float m = bf<float>(h, b, s, NB_M), mi = pi.z;
     const float mn = m + mi;
-    bf<float>(h, b, s, NB_VX) = (m * bf<float>(h, b, s, NB_VX) + mi * a.svx[i]) / mn;
-    bf<float>(h, b, s, NB_VY) = (m * bf<float>(h, b, s, NB_VY) + mi * a.svy[i]) / mn;
-    bf<float>(h, b, s, NB_X) = (m * bf<float>(h, b, s, NB_X) + mi * a.sx[i]) / mn;
-    bf<float>(h, b, s, NB_Y) = (m * bf<float>(h, b, s, NB_Y) + mi * a.sy[i]) / mn;
+    bf<float>(h, b, s, NB_VX) = (m * bf<float>(h, b, s, NB_VX) + mi * vi.x) / mn;
+    bf<float>(h, b, s, NB_VY) = (m * bf<float>(h, b, s, NB_VY) + mi * vi.y) / mn;
+    bf<float>(h, b, s, NB_X) = (m * bf<float>(h, b, s, NB_X) + mi * pi.x) / mn;
+    bf<float>(h, b, s, NB_Y) = (m * bf<float>(h, b, s, NB_Y) + mi * pi.y) / mn;
     bf<float>(h, b, s, NB_M) = mn;
-    const uint64_t hi = a.shandle[i];
-    bf<uint8_t>(h, h_bid(hi), h_slot(hi), NB_MERGED) = 1;
   }
 };
 
-struct NbDeleteMerged {   // step_6_delete_merged
+struct NbDeleteMerged {   // step_6_delete_merged: merged iff my claim won an absorbing target
   typedef dsr_nbody_args Args;
   DSR_NO_ACC
-  static __device__ __forceinline__ void run(const DevHeap& h, uint32_t, uint32_t b, uint32_t s, const Args&, Acc&) {
-    if (bf<uint8_t>(h, b, s, NB_MERGED)) dsr_destroy(h, make_handle(0, h.types[0].cap, b, s));
+  static __device__ __forceinline__ void run(const DevHeap& h, uint32_t, uint32_t b, uint32_t s, const Args& a, Acc&) {
+    const uint32_t id = bf<uint32_t>(h, b, s, NB_ID);
+    const uint32_t t = a.target[id];
+    const bool merged = t != kNone && a.incoming[t] == id && a.target[t] == kNone;
+    bf<uint8_t>(h, b, s, NB_MERGED) = merged;
+    if (merged) dsr_destroy(h, make_handle(0, h.types[0].cap, b, s));
   }
 };
 
@@ -201,27 +221,28 @@ struct NbDump {
 };
 
 bool nb_method_info(uint32_t id, MethodInfo* mi) {
-  if (id >= DSR_M_NB_SNAPSHOT && id <= DSR_M_NB_DUMP) { *mi = {0, sizeof(dsr_nbody_args)}; return true; }
+  if (id >= DSR_M_NB_SNAPSHOT && id <= DSR_M_NB_DUMP) {
+    *mi = {id == DSR_M_NB_DELETE_MERGED ? 1 : 0, sizeof(dsr_nbody_args)};   // delete_merged self-deletes
+    return true;
+  }
   return false;
+}
+
+static int pair_grid(const LaunchCtx& c, const dsr_nbody_args& a) {
+  const int g = (int)((a.id_hi - a.id_lo + kTile - 1) / kTile);
+  return g < 1 ? 1 : (g < c.sms * 8 ? g : c.sms * 8);
 }
 
 bool nb_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot, const void* args) {
   const dsr_nbody_args& a = *(const dsr_nbody_args*)args;
   switch (id) {
     case DSR_M_NB_SNAPSHOT: launch_doall<NbSnapshot>(c, T, snapshot, args); return true;
-    case DSR_M_NB_FORCE: {
-      const int g = (int)((a.n + kTile - 1) / kTile);
-      k_nb_force<<<g < c.sms * 8 ? g : c.sms * 8, kTile, 0, c.st>>>(c.h, a);
-      count_launch();
-      return true;
-    }
+    case DSR_M_NB_FORCE: k_nb_force<<<pair_grid(c, a), kTile, 0, c.st>>>(c.h, a); count_launch(); return true;
     case DSR_M_NB_MOVE: launch_doall<NbMove>(c, T, snapshot, args); return true;
-    case DSR_M_NB_PREPARE_MERGE: {
-      const int g = (int)((a.n + kTile - 1) / kTile);
-      k_nb_merge_search<<<g < c.sms * 8 ? g : c.sms * 8, kTile, 0, c.st>>>(c.h, a);
+    case DSR_M_NB_PREPARE_MERGE:
+      k_nb_merge_search<<<pair_grid(c, a), kTile, 0, c.st>>>(c.h, a);
       count_launch();
       return true;
-    }
     case DSR_M_NB_CLAIM: launch_doall<NbClaim>(c, T, snapshot, args); return true;
     case DSR_M_NB_ABSORB: launch_doall<NbAbsorb>(c, T, snapshot, args); return true;
     case DSR_M_NB_DELETE_MERGED: launch_doall<NbDeleteMerged>(c, T, snapshot, args); return true;
@@ -232,9 +253,12 @@ bool nb_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot,
 
 bool nb_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* args, size_t bytes, int* ok) {
   *ok = 1;
-  if (id != DSR_K_NB_CLEAR_SNAPSHOT) return false;
+  if (id != DSR_K_NB_CLEAR_SNAPSHOT && id != DSR_K_NB_CLAIM) return false;
   if (bytes != sizeof(dsr_nbody_args)) { *ok = 0; return true; }
-  k_nb_clear<<<grid_for(c, n), 256, 0, c.st>>>(n, *(const dsr_nbody_args*)args);
+  const dsr_nbody_args a = *(const dsr_nbody_args*)args;
+  if (n != a.n_total) { *ok = 0; return true; }
+  if (id == DSR_K_NB_CLEAR_SNAPSHOT) k_nb_clear<<<grid_for(c, n), 256, 0, c.st>>>(n, a);
+  else k_nb_claim_all<<<grid_for(c, n), 256, 0, c.st>>>(n, a);
   count_launch();
   return true;
 }
@@ -243,7 +267,9 @@ bool nb_ctor_launch(uint32_t id, const LaunchCtx& c, uint32_t T, uint64_t n, con
   *ok = 1;
   if (id != DSR_C_NB_BODY) return false;
   if (bytes != sizeof(dsr_nbody_args) || T != 0) { *ok = 0; return true; }
-  k_nb_new<<<grid_for(c, n), 256, 0, c.st>>>(c.h, n, *(const dsr_nbody_args*)args);
+  const dsr_nbody_args a = *(const dsr_nbody_args*)args;
+  if (n != (uint64_t)(a.id_hi - a.id_lo) || a.id_hi > a.n_total) { *ok = 0; return true; }
+  k_nb_new<<<grid_for(c, n), 256, 0, c.st>>>(c.h, n, a);
   count_launch();
   return true;
 }

@@ -255,7 +255,7 @@ extern "C" dsr_status dsr_doall_prologue(dsr_heap* h, uint32_t type, uint32_t me
   CUDA_TRY(cudaMemsetAsync(&h->dev.ctrl[CTRL_RCOUNT], 0, 8, st));
   const uint64_t nwords = (h->L.M + 63) / 64;
   k_compact<<<(int)((nwords + kCompactThreads - 1) / kCompactThreads), kCompactThreads, 0, st>>>(h->dev, type,
-                                                                                                  mi.allocates);
+                                                                                                  mi.snapshot);
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return DSR_OK;
@@ -270,10 +270,10 @@ extern "C" dsr_status dsr_doall_body(dsr_heap* h, uint32_t type, uint32_t method
   static const uint64_t zero_args[16] = {0};
   if (!mi.args_bytes) args = zero_args;
   LaunchCtx c = ctx(h, stream);
-  bool ok = mb_method_launch(method_id, c, type, mi.allocates, args) ||
-            gol_method_launch(method_id, c, type, mi.allocates, args) ||
-            wt_method_launch(method_id, c, type, mi.allocates, args) ||
-            nb_method_launch(method_id, c, type, mi.allocates, args);
+  bool ok = mb_method_launch(method_id, c, type, mi.snapshot, args) ||
+            gol_method_launch(method_id, c, type, mi.snapshot, args) ||
+            wt_method_launch(method_id, c, type, mi.snapshot, args) ||
+            nb_method_launch(method_id, c, type, mi.snapshot, args);
   if (!ok) return DSR_ERR_INVALID;
   CUDA_TRY(cudaGetLastError());
   return DSR_OK;

@@ -15,7 +15,11 @@ struct LaunchCtx {
 };
 
 struct MethodInfo {
-  int allocates;       // 1: the method may allocate (needs the iteration-bitmap snapshot)
+  // 1: the method may allocate or destroy objects, so the pass needs the
+  // iteration-bitmap snapshot.  Without it a visitor could see slots
+  // allocated during the pass, or -- when a block empties and is invalidated
+  // (all bits set, Alg. 9) -- phantom objects in slots that were already dead.
+  int snapshot;
   size_t args_bytes;   // expected sizeof(args)
 };
 

@@ -29,7 +29,7 @@ M_GOL_CAND_PREPARE, M_GOL_ALIVE_PREPARE, M_GOL_CAND_UPDATE, M_GOL_ALIVE_UPDATE, 
 C_WT_CELL, K_WT_INIT_AGENTS = 20, 21
 (M_WT_CELL_PREPARE, M_WT_FISH_PREPARE, M_WT_CELL_DECIDE_FISH, M_WT_FISH_UPDATE, M_WT_SHARK_PREPARE,
  M_WT_CELL_DECIDE_SHARK, M_WT_SHARK_UPDATE, M_WT_DUMP) = range(20, 28)
-C_NB_BODY, K_NB_CLEAR_SNAPSHOT = 30, 30
+C_NB_BODY, K_NB_CLEAR_SNAPSHOT, K_NB_CLAIM = 30, 30, 31
 (M_NB_SNAPSHOT, M_NB_FORCE, M_NB_MOVE, M_NB_PREPARE_MERGE, M_NB_CLAIM, M_NB_ABSORB, M_NB_DELETE_MERGED,
  M_NB_DUMP) = range(30, 38)
 
@@ -113,11 +113,11 @@ class WatorArgs(C.Structure):
 
 
 class NbodyArgs(C.Structure):
-    _fields_ = [("sx", C.c_void_p), ("sy", C.c_void_p), ("sm", C.c_void_p), ("svx", C.c_void_p),
-                ("svy", C.c_void_p), ("shandle", C.c_void_p),
+    _fields_ = [("S", C.c_void_p), ("V", C.c_void_p), ("target", C.c_void_p), ("incoming", C.c_void_p),
+                ("shandle", C.c_void_p),
                 ("x0", C.c_void_p), ("y0", C.c_void_p), ("vx0", C.c_void_p), ("vy0", C.c_void_p),
                 ("m0", C.c_void_p), ("G", C.c_float), ("dt", C.c_float), ("eps", C.c_float), ("R", C.c_float),
-                ("n", C.c_uint32), ("id_offset", C.c_uint32), ("out", C.c_void_p)]
+                ("n_total", C.c_uint32), ("id_lo", C.c_uint32), ("id_hi", C.c_uint32), ("out", C.c_void_p)]
 
 
 class DsrError(RuntimeError):

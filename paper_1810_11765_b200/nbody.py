@@ -1,58 +1,102 @@
 """N-body with collisions driver (Table 1, Listing 1; reading
 R-NBODY).  One step = snapshot S0, compute_force (device_do as a tiled
 all-pairs gather), move, snapshot S1, prepare_merge, claim, absorb,
-delete_merged.  BASELINE configs[2] (65,536 fp32 bodies)."""
+delete_merged.  BASELINE configs[2] (65,536 fp32 bodies).
+
+Multi-GPU (one process per GPU, `group` = a torch.distributed process group):
+rank r owns ids [r n/P, (r+1) n/P) in its own heap; after each snapshot the
+S/V chunks are all-gathered, after prepare_merge the target chunk; the claim
+then runs redundantly over all ids on every rank (O(n)), so absorption and
+deletion need no third exchange and the result does not depend on P.
+"""
 from __future__ import annotations
 
 from . import dsr
 
 NB_TYPES = [[4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 1]]   # x y vx vy fx fy m id target incoming merged
+NONE = 0xFFFFFFFF
+
+
+def id_range(n_total: int, world: int, rank: int):
+    """Ids owned by `rank` (contiguous equal chunks; n_total % world == 0)."""
+    if n_total % world:
+        raise ValueError("n_total must be divisible by the number of ranks")
+    c = n_total // world
+    return rank * c, (rank + 1) * c
+
+
+class Exchange:
+    """All-gathers of the id-indexed arrays between the ranks' heaps."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.group = group
+        self.world = dist.get_world_size(group) if group is not None else 1
+        self.rank = dist.get_rank(group) if group is not None else 0
+
+    def all_gather_rows(self, full, lo, hi):
+        """full: tensor whose first dim is id; rows [lo, hi) are this rank's."""
+        if self.world == 1:
+            return
+        import torch.distributed as dist
+        chunk = full[lo:hi].contiguous()
+        dist.all_gather_into_tensor(full, chunk, group=self.group)
 
 
 class NBody:
-    def __init__(self, state, G, dt, eps, R, merges=True, heap_bytes=None, device=None, stream=None, id_offset=0,
+    def __init__(self, state, G, dt, eps, R, merges=True, heap_bytes=None, device=None, stream=None, group=None,
                  n_total=None):
+        """state: dict of x, y, vx, vy, m for ALL ids (each rank keeps its chunk)."""
         import numpy as np
         import torch
-        n = len(state["x"])
-        self.n = n
-        self.n_total = n_total or n
+        self.xch = Exchange(group)
+        N = n_total or len(state["x"])
+        self.n_total = N
+        self.lo, self.hi = id_range(N, self.xch.world, self.xch.rank)
+        n = self.hi - self.lo
         self.merges = merges
         if heap_bytes is None:
             heap_bytes = max(8 << 20, n * 64 + (8 << 20))
         self.heap = dsr.Heap(NB_TYPES, heap_bytes, device=device, stream=stream)
         dev = self.heap.device
         self.stream = stream
-        f = lambda k: torch.from_numpy(np.ascontiguousarray(state[k], np.float32)).to(dev)
+        f = lambda k: torch.from_numpy(np.ascontiguousarray(state[k][self.lo:self.hi], np.float32)).to(dev)
         self.init = {k: f(k) for k in ("x", "y", "vx", "vy", "m")}
-        N = self.n_total
-        self.S = torch.zeros(5, N, dtype=torch.float32, device=dev)     # x y m vx vy
+        self.S = torch.zeros(N, 4, dtype=torch.float32, device=dev)
+        self.V = torch.zeros(N, 2, dtype=torch.float32, device=dev)
+        self.target = torch.full((N,), -1, dtype=torch.int32, device=dev)
+        self.incoming = torch.full((N,), -1, dtype=torch.int32, device=dev)
         self.shandle = torch.zeros(N, dtype=torch.int64, device=dev)
         self.out = torch.zeros(N, 6, dtype=torch.float32, device=dev)
-        S = self.S
-        self.args = dsr.NbodyArgs(S[0].data_ptr(), S[1].data_ptr(), S[2].data_ptr(), S[3].data_ptr(),
-                                  S[4].data_ptr(), self.shandle.data_ptr(),
-                                  self.init["x"].data_ptr(), self.init["y"].data_ptr(), self.init["vx"].data_ptr(),
-                                  self.init["vy"].data_ptr(), self.init["m"].data_ptr(), G, dt, eps, R, N,
-                                  id_offset, self.out.data_ptr())
+        i = self.init
+        self.args = dsr.NbodyArgs(self.S.data_ptr(), self.V.data_ptr(), self.target.data_ptr(),
+                                  self.incoming.data_ptr(), self.shandle.data_ptr(),
+                                  i["x"].data_ptr(), i["y"].data_ptr(), i["vx"].data_ptr(), i["vy"].data_ptr(),
+                                  i["m"].data_ptr(), G, dt, eps, R, N, self.lo, self.hi, self.out.data_ptr())
         self.heap.parallel_new(0, n, dsr.C_NB_BODY, self.args, stream)
 
-    def snapshot(self, s=None):
+    def _snapshot(self, s):
         h, a = self.heap, self.args
         h.launch(dsr.K_NB_CLEAR_SNAPSHOT, self.n_total, a, s)
         h.parallel_do(0, dsr.M_NB_SNAPSHOT, a, s)
+        self.xch.all_gather_rows(self.S, self.lo, self.hi)
+        self.xch.all_gather_rows(self.V, self.lo, self.hi)
 
     def step(self, stream=None):
         s = stream if stream is not None else self.stream
         h, a = self.heap, self.args
-        self.snapshot(s)                                   # S0
+        self._snapshot(s)                                  # S0
         h.parallel_do(0, dsr.M_NB_FORCE, a, s)
         h.parallel_do(0, dsr.M_NB_MOVE, a, s)
         if not self.merges:
             return
-        self.snapshot(s)                                   # S1
+        self._snapshot(s)                                  # S1
         h.parallel_do(0, dsr.M_NB_PREPARE_MERGE, a, s)
-        h.parallel_do(0, dsr.M_NB_CLAIM, a, s)
+        if self.xch.world > 1:
+            self.xch.all_gather_rows(self.target, self.lo, self.hi)
+            h.launch(dsr.K_NB_CLAIM, self.n_total, a, s)
+        else:
+            h.parallel_do(0, dsr.M_NB_CLAIM, a, s)
         h.parallel_do(0, dsr.M_NB_ABSORB, a, s)
         h.parallel_do(0, dsr.M_NB_DELETE_MERGED, a, s)
 
@@ -61,7 +105,8 @@ class NBody:
             self.step(stream)
 
     def state(self, stream=None):
-        """id-indexed dict x, y, vx, vy, m (float32) and alive (uint8)."""
+        """id-indexed dict x, y, vx, vy, m (float32) and alive (uint8) of this rank's ids
+        (all ids on one GPU)."""
         import numpy as np
         import torch
         s = stream if stream is not None else self.stream

@@ -98,7 +98,9 @@ def test_torture_concurrent_new_destroy(D, flags):
     """Many warps call new/destroy from divergent lanes; afterwards: no canary
     damage, every quiescent invariant holds, the live set equals the ledger."""
     tf = [[4, 4, 4], [4, 4, 4, 4], [4] * 6, [4] * 16, [4, 4]]   # caps 42, 32, 21, 8, 64
-    heap = D.Heap(tf, 1 << 27, flags=flags | D.F_STATS)
+    # NoShift makes every leader hit the same blocks; with failed reservations
+    # counting as failed lookups (R-RETRY) it initialises many more blocks
+    heap = D.Heap(tf, (1 << 27) if not flags & D.F_NO_ROTATE else (1 << 30), flags=flags | D.F_STATS)
     nthreads = 1 << 17
     ledger = torch.zeros(nthreads * 8, dtype=torch.int64, device="cuda")
     errors = torch.zeros(1, dtype=torch.int64, device="cuda")

@@ -1,0 +1,88 @@
+"""world_size-2 gloo tests (CPU) of the multi-GPU host logic: the id-range
+partition, the all-gather exchange of id-indexed arrays used by the sharded
+N-body, and bench.py's max-over-ranks / sum-over-ranks aggregation."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, fn, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        q.put((rank, fn(rank, world)))
+    finally:
+        dist.destroy_process_group()
+
+
+def run_world(fn, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, fn, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return out
+
+
+def _exchange(rank, world):
+    from paper_1810_11765_b200.nbody import Exchange, id_range
+    n = 64
+    lo, hi = id_range(n, world, rank)
+    S = torch.zeros(n, 4)
+    S[lo:hi] = torch.arange(lo, hi, dtype=torch.float32)[:, None] * torch.tensor([1.0, 2.0, 3.0, 0.0])
+    tgt = torch.full((n,), -1, dtype=torch.int32)
+    tgt[lo:hi] = torch.arange(lo, hi, dtype=torch.int32) * 7 % n
+    x = Exchange(dist.group.WORLD)
+    x.all_gather_rows(S, lo, hi)
+    x.all_gather_rows(tgt, lo, hi)
+    return S.numpy(), tgt.numpy(), (lo, hi)
+
+
+def test_id_range_partition_and_exchange():
+    out = run_world(_exchange, 2)
+    n = 64
+    want_S = np.arange(n, dtype=np.float32)[:, None] * np.array([1, 2, 3, 0], np.float32)
+    want_t = (np.arange(n) * 7 % n).astype(np.int32)
+    ranges = sorted(v[2] for v in out.values())
+    assert ranges == [(0, 32), (32, 64)]
+    for S, t, _ in out.values():
+        assert np.array_equal(S, want_S) and np.array_equal(t, want_t)
+
+
+def _aggregate(rank, world):
+    import bench
+    ms = [3.0, 5.0][rank]
+    work = [100.0, 200.0][rank]
+    tot, = bench.reduce_over_ranks([work], "sum", device="cpu")
+    mx, = bench.reduce_over_ranks([ms], "max", device="cpu")
+    return tot, mx
+
+
+def test_bench_aggregation_max_time_sum_work():
+    out = run_world(_aggregate, 2)
+    for tot, mx in out.values():
+        assert tot == 300.0 and mx == 5.0
+
+
+def test_id_range_rejects_uneven():
+    from paper_1810_11765_b200.nbody import id_range
+    with pytest.raises(ValueError):
+        id_range(10, 3, 0)
