@@ -154,7 +154,7 @@ bool gol_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* 
   if (bytes != sizeof(dsr_gol_args) || c.h.ntypes < 2) { *ok = 0; return true; }
   const dsr_gol_args a = *(const dsr_gol_args*)args;
   if ((uint64_t)a.W * a.H != n) { *ok = 0; return true; }
-  k_gol_init<<<grid_for(c, n), 256, 0, c.st>>>(c.h, n, a, id == DSR_K_GOL_INIT_CAND);
+  k_gol_init<<<grid_for(c, n, k_gol_init), 256, 0, c.st>>>(c.h, n, a, id == DSR_K_GOL_INIT_CAND);
   count_launch();
   return true;
 }

@@ -203,13 +203,13 @@ bool mb_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot,
       for (uint32_t f = 0; f < nf; ++f)
         if (c.h.types[T].fsize[f] != 4) return false;
       switch (nf) {
-        case 1: k_mb_reduce<1><<<c.grid, 256, 0, c.st>>>(c.h, T, o); break;
-        case 2: k_mb_reduce<2><<<c.grid, 256, 0, c.st>>>(c.h, T, o); break;
-        case 3: k_mb_reduce<3><<<c.grid, 256, 0, c.st>>>(c.h, T, o); break;
-        case 4: k_mb_reduce<4><<<c.grid, 256, 0, c.st>>>(c.h, T, o); break;
-        case 6: k_mb_reduce<6><<<c.grid, 256, 0, c.st>>>(c.h, T, o); break;
-        case 8: k_mb_reduce<8><<<c.grid, 256, 0, c.st>>>(c.h, T, o); break;
-        case 16: k_mb_reduce<16><<<c.grid, 256, 0, c.st>>>(c.h, T, o); break;
+        case 1: k_mb_reduce<1><<<persistent_grid(c, k_mb_reduce<1>), 256, 0, c.st>>>(c.h, T, o); break;
+        case 2: k_mb_reduce<2><<<persistent_grid(c, k_mb_reduce<2>), 256, 0, c.st>>>(c.h, T, o); break;
+        case 3: k_mb_reduce<3><<<persistent_grid(c, k_mb_reduce<3>), 256, 0, c.st>>>(c.h, T, o); break;
+        case 4: k_mb_reduce<4><<<persistent_grid(c, k_mb_reduce<4>), 256, 0, c.st>>>(c.h, T, o); break;
+        case 6: k_mb_reduce<6><<<persistent_grid(c, k_mb_reduce<6>), 256, 0, c.st>>>(c.h, T, o); break;
+        case 8: k_mb_reduce<8><<<persistent_grid(c, k_mb_reduce<8>), 256, 0, c.st>>>(c.h, T, o); break;
+        case 16: k_mb_reduce<16><<<persistent_grid(c, k_mb_reduce<16>), 256, 0, c.st>>>(c.h, T, o); break;
         default: return false;
       }
       count_launch();
@@ -227,7 +227,7 @@ bool mb_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* a
   switch (id) {
     case DSR_K_MB_NEW: {
       if (bytes != sizeof(dsr_mb_new_args) || c.h.ntypes < 3) { *ok = 0; return true; }
-      k_mb_new<<<grid_for(c, n), 256, 0, c.st>>>(c.h, n, *(const dsr_mb_new_args*)args);
+      k_mb_new<<<grid_for(c, n, k_mb_new), 256, 0, c.st>>>(c.h, n, *(const dsr_mb_new_args*)args);
       count_launch();
       return true;
     }

@@ -257,8 +257,8 @@ bool nb_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* a
   if (bytes != sizeof(dsr_nbody_args)) { *ok = 0; return true; }
   const dsr_nbody_args a = *(const dsr_nbody_args*)args;
   if (n != a.n_total) { *ok = 0; return true; }
-  if (id == DSR_K_NB_CLEAR_SNAPSHOT) k_nb_clear<<<grid_for(c, n), 256, 0, c.st>>>(n, a);
-  else k_nb_claim_all<<<grid_for(c, n), 256, 0, c.st>>>(n, a);
+  if (id == DSR_K_NB_CLEAR_SNAPSHOT) k_nb_clear<<<grid_for(c, n, k_nb_clear), 256, 0, c.st>>>(n, a);
+  else k_nb_claim_all<<<grid_for(c, n, k_nb_claim_all), 256, 0, c.st>>>(n, a);
   count_launch();
   return true;
 }
@@ -269,7 +269,7 @@ bool nb_ctor_launch(uint32_t id, const LaunchCtx& c, uint32_t T, uint64_t n, con
   if (bytes != sizeof(dsr_nbody_args) || T != 0) { *ok = 0; return true; }
   const dsr_nbody_args a = *(const dsr_nbody_args*)args;
   if (n != (uint64_t)(a.id_hi - a.id_lo) || a.id_hi > a.n_total) { *ok = 0; return true; }
-  k_nb_new<<<grid_for(c, n), 256, 0, c.st>>>(c.h, n, a);
+  k_nb_new<<<grid_for(c, n, k_nb_new), 256, 0, c.st>>>(c.h, n, a);
   count_launch();
   return true;
 }

@@ -253,7 +253,7 @@ bool wt_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* a
   if (bytes != sizeof(dsr_wator_args) || c.h.ntypes < 3) { *ok = 0; return true; }
   const dsr_wator_args a = *(const dsr_wator_args*)args;
   if ((uint64_t)a.W * a.H != n) { *ok = 0; return true; }
-  k_wt_init_agents<<<grid_for(c, n), 256, 0, c.st>>>(c.h, n, a);
+  k_wt_init_agents<<<grid_for(c, n, k_wt_init_agents), 256, 0, c.st>>>(c.h, n, a);
   count_launch();
   return true;
 }
@@ -264,7 +264,7 @@ bool wt_ctor_launch(uint32_t id, const LaunchCtx& c, uint32_t T, uint64_t n, con
   if (bytes != sizeof(dsr_wator_args) || T != WT_CELL || c.h.ntypes < 3) { *ok = 0; return true; }
   const dsr_wator_args a = *(const dsr_wator_args*)args;
   if ((uint64_t)a.W * a.H != n) { *ok = 0; return true; }
-  k_wt_new_cells<<<grid_for(c, n), 256, 0, c.st>>>(c.h, n, a);
+  k_wt_new_cells<<<grid_for(c, n, k_wt_new_cells), 256, 0, c.st>>>(c.h, n, a);
   count_launch();
   return true;
 }

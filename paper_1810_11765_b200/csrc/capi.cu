@@ -10,8 +10,24 @@
 #define DSR_BUILD_INFO "sm_100a"
 #endif
 
+#include <mutex>
+#include <unordered_map>
+
 namespace dsr {
 std::atomic<unsigned long long> g_launches{0};
+
+int resident_ctas(const void* kernel, int threads) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = (const void*)((const char*)kernel + threads);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, 0) != cudaSuccess || nb < 1) nb = 1;
+  cache[key] = nb;
+  return nb;
+}
 }
 using namespace dsr;
 

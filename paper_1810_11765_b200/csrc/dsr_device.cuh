@@ -109,11 +109,17 @@ __device__ __forceinline__ uint64_t shfl64(uint32_t mask, uint64_t v, uint32_t s
   uint32_t lo = __shfl_sync(mask, (uint32_t)v, src), hi = __shfl_sync(mask, (uint32_t)(v >> 32), src);
   return ((uint64_t)hi << 32) | lo;
 }
-// 0-based n-th set bit of x ("b <- b & (b-1) ... then ffs"; __fns does it in hardware)
+// 0-based n-th set bit of x (P:689 clears the lowest bit n times, then ffs;
+// here a 6-step popc binary search, branch-free per step)
 __device__ __forceinline__ uint32_t nth_bit(uint64_t x, uint32_t n) {
-  uint32_t lo = (uint32_t)x, c = __popc(lo);
-  if (n < c) return __fns(lo, 0, (int)n + 1);
-  return 32u + __fns((uint32_t)(x >> 32), 0, (int)(n - c) + 1);
+  uint32_t pos = 0, c = __popc((uint32_t)x);
+  if (n >= c) { n -= c; x >>= 32; pos = 32; }
+  uint32_t w = (uint32_t)x;
+  c = __popc(w & 0xFFFFu); if (n >= c) { n -= c; w >>= 16; pos += 16; }
+  c = __popc(w & 0xFFu);   if (n >= c) { n -= c; w >>= 8;  pos += 8; }
+  c = __popc(w & 0xFu);    if (n >= c) { n -= c; w >>= 4;  pos += 4; }
+  c = __popc(w & 0x3u);    if (n >= c) { n -= c; w >>= 2;  pos += 2; }
+  return pos + ((n >= (w & 1u)) ? 1u : 0u);
 }
 __device__ __forceinline__ void backoff(uint32_t& ns) {
   __nanosleep(ns);
@@ -258,9 +264,9 @@ __device__ __forceinline__ void init_block(const DevHeap& h, uint32_t T, uint32_
 // free slots (rotated) and set them with ONE atomicOr; returns the
 // slots this call actually flipped (may be fewer; 0 = block full/invalidated).
 __device__ __forceinline__ uint64_t block_reserve(const DevHeap& h, uint32_t bid, uint32_t need, uint32_t rot,
-                                                  uint64_t* before_out) {
+                                                  uint64_t* before_out, const uint64_t* known = nullptr) {
   uint64_t* w = h.alloc_bm + bid;
-  uint64_t cur = ld_relaxed(w);
+  uint64_t cur = known ? *known : ld_relaxed(w);     // a block we just initialised: its word is known
   for (;;) {
     const uint64_t fr = ~cur;
     if (fr == 0) return 0;
@@ -322,6 +328,7 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
   uint32_t oom_tries = 0, fails = 0;
   for (uint64_t iter = 0;; ++iter) {
     int64_t bid = -1;
+    bool fresh = false;
     if (fails < h.r_attempts) {
       bid = bm_try_find_set(h.activebm[T], rot_hash(h, who, iter));
       if (bid < 0) { ++fails; continue; }
@@ -345,10 +352,11 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
       bm_set(h.allocbm[T], (uint64_t)bid);
       bm_set(h.activebm[T], (uint64_t)bid);
       stat_add(h, ST_INITS, 1);
+      fresh = true;
     }
     uint64_t before = 0;
     const uint32_t rot = (uint32_t)(rot_hash(h, who, iter + 0x1000) >> 58);
-    const uint64_t got = block_reserve(h, (uint32_t)bid, need, rot, &before);
+    const uint64_t got = block_reserve(h, (uint32_t)bid, need, rot, &before, fresh ? &h.types[T].pad : nullptr);
     if (!got) { ++fails; continue; }                                          // full or invalidated
     const uint32_t t = ld_relaxed_u8(h.type + bid) - 1u;                      // volatile read (Alg. 1 l.10)
     if ((before | got) == ~0ull) bm_clear(h.activebm[t], (uint64_t)bid);      // FULL -> inactive (l.12)

@@ -45,18 +45,27 @@ bool nb_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot,
 bool nb_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* args, size_t bytes, int* ok);
 bool nb_ctor_launch(uint32_t id, const LaunchCtx& c, uint32_t T, uint64_t n, const void* args, size_t bytes, int* ok);
 
+// CTAs of `kernel` that are resident on one SM at `threads` threads (cached).
+int resident_ctas(const void* kernel, int threads);
+
+// Persistent grid: exactly one wave of resident CTAs (a multiple of the SM count).
+template <typename K>
+inline int persistent_grid(const LaunchCtx& c, K kernel, int threads = 256) {
+  return resident_ctas((const void*)kernel, threads) * c.sms;
+}
+template <typename K>
+inline int grid_for(const LaunchCtx& c, uint64_t n, K kernel, int threads = 256) {
+  const uint64_t g = (n + threads - 1) / threads;
+  const uint64_t p = (uint64_t)persistent_grid(c, kernel, threads);
+  return (int)(g < 1 ? 1 : (g < p ? g : p));
+}
+
 // launch helper for element-loop method kernels
 template <class Mth>
 inline void launch_doall(const LaunchCtx& c, uint32_t T, int snapshot, const void* args) {
   typename Mth::Args a = *reinterpret_cast<const typename Mth::Args*>(args);
-  k_doall<Mth><<<c.grid, 256, 0, c.st>>>(c.h, T, snapshot, a);
+  k_doall<Mth><<<persistent_grid(c, k_doall<Mth>), 256, 0, c.st>>>(c.h, T, snapshot, a);
   count_launch();
-}
-
-inline int grid_for(const LaunchCtx& c, uint64_t n, int threads = 256) {
-  uint64_t g = (n + threads - 1) / threads;
-  if (g > (uint64_t)c.grid) g = (uint64_t)c.grid;
-  return g ? (int)g : 1;
 }
 
 }  // namespace dsr
