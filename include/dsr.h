@@ -100,6 +100,10 @@ typedef struct {
   uint64_t invalidate_fail;  /* failed / rolled-back invalidations (Alg. 9 l.8) */
   uint64_t reserve_retries;  /* reservations that lost every selected bit (Alg. 6 loop) */
   uint64_t oom;              /* OOM events */
+  /* profiling (DSR_F_STATS): leader requests, active lookups, failed lookups,
+   * zero-slot reservations, and SM cycles summed over leaders spent in the
+   * lookup, the slow path, the reservation (+ FULL handling), whole requests */
+  uint64_t requests, finds, find_fails, reserve_zero, cyc_find, cyc_slow, cyc_reserve, cyc_request;
 } dsr_counters;
 
 typedef struct dsr_heap dsr_heap;   /* opaque, host side, owned by the library */
@@ -294,6 +298,7 @@ typedef struct {
   float G, dt, eps, R;
   uint32_t n_total, id_lo, id_hi;
   float* out;                         /* dump: 6 floats per id (x, y, vx, vy, m, alive) */
+  float* scratch;                     /* all-pairs partials: >= 2 * ceil(n_total/4096) * (id_hi - id_lo) floats */
 } dsr_nbody_args;
 enum {
   DSR_C_NB_BODY = 30,            /* parallel_new<Body>(id_hi - id_lo): body i gets id id_lo + i */

@@ -103,15 +103,26 @@ struct GolAliveUpdate {   // pass 4 (allocates Candidate)
   DSR_NO_ACC
   static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args& a, Acc&) {
     const uint32_t c = *field_ptr<uint32_t>(h, T, 0, b, s);
-    if (*field_ptr<uint8_t>(h, T, 1, b, s)) {            // new Alive: candidates on empty neighbours
+    uint32_t todo = 0;                                   // bit d: create a Candidate at neighbour d; bit 8: at c
+    if (*field_ptr<uint8_t>(h, T, 1, b, s)) {            // new Alive: claim the empty neighbours
       for (int d = 0; d < 8; ++d) {
-        const uint32_t e = gol_nbr(a.W, a.H, c, d);
-        unsigned long long* pe = (unsigned long long*)a.cell + e;
-        if (ld_relaxed((const uint64_t*)pe) == 0 && atomicCAS(pe, 0ull, kReserved) == 0ull) *pe = new_cand(h, e);
+        unsigned long long* pe = (unsigned long long*)a.cell + gol_nbr(a.W, a.H, c, d);
+        if (ld_relaxed((const uint64_t*)pe) == 0 && atomicCAS(pe, 0ull, kReserved) == 0ull) todo |= 1u << d;
       }
     } else if (*field_ptr<uint8_t>(h, T, 2, b, s) == ACT_DIE) {
       dsr_destroy(h, make_handle(T, h.types[T].cap, b, s));
-      a.cell[c] = new_cand(h, c);
+      todo = 1u << 8;
+    }
+    // allocate in warp-synchronous rounds so that every lane's k-th Candidate
+    // is requested together (one coalesced request per round)
+    const uint32_t rounds = __reduce_max_sync(__activemask(), (uint32_t)__popc(todo));
+    for (uint32_t r = 0; r < rounds; ++r) {
+      if (todo) {
+        const int d = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const uint32_t e = d == 8 ? c : gol_nbr(a.W, a.H, c, d);
+        a.cell[e] = new_cand(h, e);
+      }
     }
   }
 };

@@ -17,7 +17,6 @@ namespace dsr {
 
 enum { NB_X = 0, NB_Y, NB_VX, NB_VY, NB_FX, NB_FY, NB_M, NB_ID, NB_TARGET, NB_INCOMING, NB_MERGED };
 constexpr uint32_t kNone = 0xFFFFFFFFu;
-constexpr int kTile = 256;
 
 template <class V>
 __device__ __forceinline__ V& bf(const DevHeap& h, uint32_t b, uint32_t s, int f) {
@@ -69,40 +68,62 @@ struct NbSnapshot {
   }
 };
 
-// compute_force for own ids: f_i = G m_i sum_j m_j (p_j - p_i) / (|p_j - p_i|^2 + eps^2)^{3/2}
-__global__ void __launch_bounds__(kTile) k_nb_force(DevHeap h, dsr_nbody_args a) {
-  __shared__ float4 tile[kTile];
-  const uint32_t n = a.n_total, lo = a.id_lo, hi = a.id_hi;
+// ---- device_do all-pairs gathers (force, merge search) -------------------
+// Grid (i-blocks of 256 own ids, j-chunks of kChunk ids); a 128-thread CTA
+// handles 2 bodies per thread and stages 256 snapshot entries per tile in
+// shared memory.  Each (i, chunk) partial is written to scratch and a second
+// kernel combines the chunks in increasing order: a fixed summation order that
+// does not depend on the launch shape or on the number of GPUs.
+constexpr uint32_t kChunk = 4096;
+constexpr int kPairThreads = 128;
+
+__global__ void __launch_bounds__(kPairThreads) k_nb_force_part(dsr_nbody_args a) {
+  __shared__ float4 tile[256];
+  const uint32_t n = a.n_total, nl = a.id_hi - a.id_lo;
+  const uint32_t i0 = a.id_lo + blockIdx.x * 256 + threadIdx.x, i1 = i0 + 128;
+  const float4 p0 = i0 < a.id_hi ? s4(a, i0) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 p1 = i1 < a.id_hi ? s4(a, i1) : make_float4(0.f, 0.f, 0.f, 0.f);
   const float eps2 = a.eps * a.eps;
-  for (uint32_t base = lo + blockIdx.x * kTile; base < hi; base += gridDim.x * kTile) {
-    const uint32_t i = base + threadIdx.x;
-    float4 pi = make_float4(0.f, 0.f, 0.f, 0.f);
-    uint64_t hd = 0;
-    if (i < hi) { hd = a.shandle[i]; pi = s4(a, i); }
-    float ax = 0.f, ay = 0.f;
-    for (uint32_t j0 = 0; j0 < n; j0 += kTile) {
-      __syncthreads();
-      const uint32_t j = j0 + threadIdx.x;
-      tile[threadIdx.x] = j < n ? s4(a, j) : make_float4(0.f, 0.f, 0.f, 0.f);
-      __syncthreads();
-      const uint32_t lim = (n - j0) < (uint32_t)kTile ? (n - j0) : (uint32_t)kTile;
+  const uint32_t jb = blockIdx.y * kChunk, je = min(jb + kChunk, n);
+  float ax0 = 0.f, ay0 = 0.f, ax1 = 0.f, ay1 = 0.f;
+  for (uint32_t j0 = jb; j0 < je; j0 += 256) {
+    __syncthreads();
+    const uint32_t ja = j0 + threadIdx.x, jc = ja + 128;
+    tile[threadIdx.x] = ja < je ? s4(a, ja) : make_float4(0.f, 0.f, 0.f, 0.f);
+    tile[threadIdx.x + 128] = jc < je ? s4(a, jc) : make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
 #pragma unroll 8
-      for (uint32_t k = 0; k < lim; ++k) {
-        const float4 p = tile[k];
-        const float dx = p.x - pi.x, dy = p.y - pi.y;
-        const float r2 = fmaf(dx, dx, fmaf(dy, dy, eps2));
-        const float inv = rsqrtf(r2);
-        const float w = p.z * inv * inv * inv;
-        ax = fmaf(dx, w, ax);
-        ay = fmaf(dy, w, ay);
-      }
+    for (int k = 0; k < 256; ++k) {
+      const float4 p = tile[k];                      // out-of-range entries have m = 0
+      const float dx0 = p.x - p0.x, dy0 = p.y - p0.y, dx1 = p.x - p1.x, dy1 = p.y - p1.y;
+      const float r0 = fmaf(dx0, dx0, fmaf(dy0, dy0, eps2)), r1 = fmaf(dx1, dx1, fmaf(dy1, dy1, eps2));
+      const float v0 = rsqrtf(r0), v1 = rsqrtf(r1);
+      const float w0 = p.z * v0 * v0 * v0, w1 = p.z * v1 * v1 * v1;
+      ax0 = fmaf(dx0, w0, ax0); ay0 = fmaf(dy0, w0, ay0);
+      ax1 = fmaf(dx1, w1, ax1); ay1 = fmaf(dy1, w1, ay1);
     }
-    if (hd) {
-      const uint32_t b = h_bid(hd), s = h_slot(hd);
-      const float gm = a.G * bf<float>(h, b, s, NB_M);
-      bf<float>(h, b, s, NB_FX) = gm * ax;
-      bf<float>(h, b, s, NB_FY) = gm * ay;
+  }
+  float2* part = reinterpret_cast<float2*>(a.scratch) + (size_t)blockIdx.y * nl;
+  if (i0 < a.id_hi) part[i0 - a.id_lo] = make_float2(ax0, ay0);
+  if (i1 < a.id_hi) part[i1 - a.id_lo] = make_float2(ax1, ay1);
+}
+
+// f_i = G m_i sum_j m_j (p_j - p_i) / (|p_j - p_i|^2 + eps^2)^{3/2}, chunks summed in order
+__global__ void k_nb_force_sum(DevHeap h, dsr_nbody_args a) {
+  const uint32_t nl = a.id_hi - a.id_lo, chunks = (a.n_total + kChunk - 1) / kChunk;
+  for (uint32_t li = blockIdx.x * blockDim.x + threadIdx.x; li < nl; li += gridDim.x * blockDim.x) {
+    const uint64_t hd = a.shandle[a.id_lo + li];
+    if (!hd) continue;
+    float ax = 0.f, ay = 0.f;
+    for (uint32_t c = 0; c < chunks; ++c) {
+      const float2 v = reinterpret_cast<const float2*>(a.scratch)[(size_t)c * nl + li];
+      ax += v.x;
+      ay += v.y;
     }
+    const uint32_t b = h_bid(hd), s = h_slot(hd);
+    const float gm = a.G * bf<float>(h, b, s, NB_M);
+    bf<float>(h, b, s, NB_FX) = gm * ax;
+    bf<float>(h, b, s, NB_FY) = gm * ay;
   }
 }
 
@@ -123,38 +144,55 @@ struct NbMove {   // semi-implicit Euler, velocity first
   }
 };
 
-// prepare_merge for own ids: target_i = argmin over j with (m_j, j) >lex (m_i, i) and d2 < R^2 of (d2, j)
-__global__ void __launch_bounds__(kTile) k_nb_merge_search(DevHeap h, dsr_nbody_args a) {
-  __shared__ float4 tile[kTile];
-  const uint32_t n = a.n_total, lo = a.id_lo, hi = a.id_hi;
+// prepare_merge partials: per (i, chunk) the best (d2, j) with (m_j, j) >lex (m_i, i), d2 < R^2
+__global__ void __launch_bounds__(kPairThreads) k_nb_merge_part(dsr_nbody_args a) {
+  __shared__ float4 tile[256];
+  const uint32_t n = a.n_total, nl = a.id_hi - a.id_lo;
+  const uint32_t i0 = a.id_lo + blockIdx.x * 256 + threadIdx.x, i1 = i0 + 128;
+  const float4 p0 = i0 < a.id_hi ? s4(a, i0) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 p1 = i1 < a.id_hi ? s4(a, i1) : make_float4(0.f, 0.f, 0.f, 0.f);
   const float R2 = a.R * a.R;
-  for (uint32_t base = lo + blockIdx.x * kTile; base < hi; base += gridDim.x * kTile) {
-    const uint32_t i = base + threadIdx.x;
-    float4 pi = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (i < hi) pi = s4(a, i);
-    uint32_t best = kNone;
-    float bestd = 0.f;
-    for (uint32_t j0 = 0; j0 < n; j0 += kTile) {
-      __syncthreads();
-      const uint32_t j = j0 + threadIdx.x;
-      tile[threadIdx.x] = j < n ? s4(a, j) : make_float4(0.f, 0.f, 0.f, 0.f);
-      __syncthreads();
-      if (pi.z == 0.f) continue;
-      const uint32_t lim = (n - j0) < (uint32_t)kTile ? (n - j0) : (uint32_t)kTile;
-      for (uint32_t k = 0; k < lim; ++k) {
-        const float4 p = tile[k];
-        const float dx = p.x - pi.x, dy = p.y - pi.y;
-        const float d2 = fmaf(dx, dx, dy * dy);
-        const uint32_t jj = j0 + k;
-        const bool heavier = p.z > pi.z || (p.z == pi.z && jj > i);
-        if (heavier && d2 < R2 && (best == kNone || d2 < bestd)) { best = jj; bestd = d2; }
+  const uint32_t jb = blockIdx.y * kChunk, je = min(jb + kChunk, n);
+  uint32_t b0 = kNone, b1 = kNone;
+  float d0 = R2, d1 = R2;                              // strict d2 < R^2, ties -> smaller j (j ascends)
+  for (uint32_t j0 = jb; j0 < je; j0 += 256) {
+    __syncthreads();
+    const uint32_t ja = j0 + threadIdx.x, jc = ja + 128;
+    tile[threadIdx.x] = ja < je ? s4(a, ja) : make_float4(0.f, 0.f, 0.f, 0.f);
+    tile[threadIdx.x + 128] = jc < je ? s4(a, jc) : make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+#pragma unroll 4
+    for (int k = 0; k < 256; ++k) {
+      const float4 p = tile[k];
+      const float dx0 = p.x - p0.x, dy0 = p.y - p0.y, dx1 = p.x - p1.x, dy1 = p.y - p1.y;
+      const float e0 = fmaf(dx0, dx0, dy0 * dy0), e1 = fmaf(dx1, dx1, dy1 * dy1);
+      if (e0 < d0 || e1 < d1) {                        // rare: a body within R
+        const uint32_t j = j0 + k;
+        if (e0 < d0 && p.z > 0.f && (p.z > p0.z || (p.z == p0.z && j > i0))) { d0 = e0; b0 = j; }
+        if (e1 < d1 && p.z > 0.f && (p.z > p1.z || (p.z == p1.z && j > i1))) { d1 = e1; b1 = j; }
       }
     }
-    if (i < hi && pi.z != 0.f) {
-      a.target[i] = best;
-      const uint64_t hd = a.shandle[i];
-      bf<uint32_t>(h, h_bid(hd), h_slot(hd), NB_TARGET) = best;
+  }
+  uint2* part = reinterpret_cast<uint2*>(a.scratch) + (size_t)blockIdx.y * nl;
+  if (i0 < a.id_hi) part[i0 - a.id_lo] = make_uint2(__float_as_uint(d0), b0);
+  if (i1 < a.id_hi) part[i1 - a.id_lo] = make_uint2(__float_as_uint(d1), b1);
+}
+
+__global__ void k_nb_merge_pick(DevHeap h, dsr_nbody_args a) {
+  const uint32_t nl = a.id_hi - a.id_lo, chunks = (a.n_total + kChunk - 1) / kChunk;
+  for (uint32_t li = blockIdx.x * blockDim.x + threadIdx.x; li < nl; li += gridDim.x * blockDim.x) {
+    const uint32_t i = a.id_lo + li;
+    const uint64_t hd = a.shandle[i];
+    if (!hd) continue;
+    uint32_t best = kNone;
+    float bd = 0.f;
+    for (uint32_t c = 0; c < chunks; ++c) {
+      const uint2 v = reinterpret_cast<const uint2*>(a.scratch)[(size_t)c * nl + li];
+      const float d = __uint_as_float(v.x);
+      if (v.y != kNone && (best == kNone || d < bd)) { best = v.y; bd = d; }   // chunks ascend in j
     }
+    a.target[i] = best;
+    bf<uint32_t>(h, h_bid(hd), h_slot(hd), NB_TARGET) = best;
   }
 }
 
@@ -228,20 +266,26 @@ bool nb_method_info(uint32_t id, MethodInfo* mi) {
   return false;
 }
 
-static int pair_grid(const LaunchCtx& c, const dsr_nbody_args& a) {
-  const int g = (int)((a.id_hi - a.id_lo + kTile - 1) / kTile);
-  return g < 1 ? 1 : (g < c.sms * 8 ? g : c.sms * 8);
+static dim3 pair_grid(const dsr_nbody_args& a) {
+  return dim3((a.id_hi - a.id_lo + 255) / 256, (a.n_total + kChunk - 1) / kChunk);
 }
 
 bool nb_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot, const void* args) {
   const dsr_nbody_args& a = *(const dsr_nbody_args*)args;
   switch (id) {
     case DSR_M_NB_SNAPSHOT: launch_doall<NbSnapshot>(c, T, snapshot, args); return true;
-    case DSR_M_NB_FORCE: k_nb_force<<<pair_grid(c, a), kTile, 0, c.st>>>(c.h, a); count_launch(); return true;
+    case DSR_M_NB_FORCE:
+      if (a.id_hi <= a.id_lo) return true;
+      k_nb_force_part<<<pair_grid(a), kPairThreads, 0, c.st>>>(a);
+      k_nb_force_sum<<<grid_for(c, a.id_hi - a.id_lo, k_nb_force_sum), 256, 0, c.st>>>(c.h, a);
+      count_launch(2);
+      return true;
     case DSR_M_NB_MOVE: launch_doall<NbMove>(c, T, snapshot, args); return true;
     case DSR_M_NB_PREPARE_MERGE:
-      k_nb_merge_search<<<pair_grid(c, a), kTile, 0, c.st>>>(c.h, a);
-      count_launch();
+      if (a.id_hi <= a.id_lo) return true;
+      k_nb_merge_part<<<pair_grid(a), kPairThreads, 0, c.st>>>(a);
+      k_nb_merge_pick<<<grid_for(c, a.id_hi - a.id_lo, k_nb_merge_pick), 256, 0, c.st>>>(c.h, a);
+      count_launch(2);
       return true;
     case DSR_M_NB_CLAIM: launch_doall<NbClaim>(c, T, snapshot, args); return true;
     case DSR_M_NB_ABSORB: launch_doall<NbAbsorb>(c, T, snapshot, args); return true;

@@ -512,6 +512,14 @@ extern "C" dsr_status dsr_stats(dsr_heap* h, dsr_counters* out, void* stream) {
   out->invalidate_fail = v[ST_INVFAIL];
   out->reserve_retries = v[ST_RESRETRY];
   out->oom = v[ST_OOM];
+  out->requests = v[ST_REQ];
+  out->finds = v[ST_FIND];
+  out->find_fails = v[ST_FINDFAIL];
+  out->reserve_zero = v[ST_RESZERO];
+  out->cyc_find = v[ST_CYC_FIND];
+  out->cyc_slow = v[ST_CYC_SLOW];
+  out->cyc_reserve = v[ST_CYC_RES];
+  out->cyc_request = v[ST_CYC_REQ];
   return DSR_OK;
 }
 extern "C" dsr_status dsr_stats_reset(dsr_heap* h, void* stream) {

@@ -41,7 +41,8 @@ struct DevType {
 // control page word offsets (u64 units) -- DESIGN.md "HBM layout"
 enum { CTRL_ERR = 0, CTRL_RCOUNT = 1, CTRL_SCRATCH = 2, CTRL_STATS = 16, CTRL_AUDIT = 40 };
 enum { ERRB_OOM = 1, ERRB_BUDGET = 2 };
-enum { ST_ALLOCS = 0, ST_FREES, ST_INITS, ST_BFREES, ST_ROLLBACKS, ST_INVFAIL, ST_RESRETRY, ST_OOM, ST_N };
+enum { ST_ALLOCS = 0, ST_FREES, ST_INITS, ST_BFREES, ST_ROLLBACKS, ST_INVFAIL, ST_RESRETRY, ST_OOM,
+       ST_REQ, ST_FIND, ST_FINDFAIL, ST_RESZERO, ST_CYC_FIND, ST_CYC_SLOW, ST_CYC_RES, ST_CYC_REQ, ST_N };
 
 struct DevHeap {
   uint8_t* data;          // M * block_bytes SOA data segments
@@ -325,13 +326,18 @@ __device__ __forceinline__ void block_free(const DevHeap& h, uint32_t T, uint32_
 // path (reading R-RETRY).  Sequentially this is exactly Alg. 1.
 static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint32_t T, uint32_t need, uint32_t* bid_out) {
   const uint64_t who = warp_gid();
+  const bool prof = h.flags & DSR_F_STATS;
   uint32_t oom_tries = 0, fails = 0;
+  long long c0 = prof ? clock64() : 0;
+  if (prof) stat_add(h, ST_REQ, 1);
   for (uint64_t iter = 0;; ++iter) {
     int64_t bid = -1;
     bool fresh = false;
+    long long c1 = prof ? clock64() : 0;
     if (fails < h.r_attempts) {
       bid = bm_try_find_set(h.activebm[T], rot_hash(h, who, iter));
-      if (bid < 0) { ++fails; continue; }
+      if (prof) { stat_add(h, ST_FIND, 1); stat_add(h, ST_CYC_FIND, clock64() - c1); }
+      if (bid < 0) { if (prof) stat_add(h, ST_FINDFAIL, 1); ++fails; continue; }
     } else {                                                                  // slow path
       bid = bm_clear_any(h, h.freebm, who, iter << 8);
       if (bid < 0) {
@@ -352,15 +358,22 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
       bm_set(h.allocbm[T], (uint64_t)bid);
       bm_set(h.activebm[T], (uint64_t)bid);
       stat_add(h, ST_INITS, 1);
+      if (prof) stat_add(h, ST_CYC_SLOW, clock64() - c1);
       fresh = true;
     }
     uint64_t before = 0;
+    long long c2 = prof ? clock64() : 0;
     const uint32_t rot = (uint32_t)(rot_hash(h, who, iter + 0x1000) >> 58);
     const uint64_t got = block_reserve(h, (uint32_t)bid, need, rot, &before, fresh ? &h.types[T].pad : nullptr);
-    if (!got) { ++fails; continue; }                                          // full or invalidated
+    if (!got) { if (prof) stat_add(h, ST_RESZERO, 1); ++fails; continue; }    // full or invalidated
     const uint32_t t = ld_relaxed_u8(h.type + bid) - 1u;                      // volatile read (Alg. 1 l.10)
     if ((before | got) == ~0ull) bm_clear(h.activebm[t], (uint64_t)bid);      // FULL -> inactive (l.12)
-    if (t == T) { *bid_out = (uint32_t)bid; return got; }
+    if (prof) stat_add(h, ST_CYC_RES, clock64() - c2);
+    if (t == T) {
+      if (prof) stat_add(h, ST_CYC_REQ, clock64() - c0);
+      *bid_out = (uint32_t)bid;
+      return got;
+    }
     block_free(h, t, (uint32_t)bid, got);                                     // type changed: rollback (l.14)
     stat_add(h, ST_ROLLBACKS, 1);
   }

@@ -67,7 +67,9 @@ class Config(C.Structure):
 
 class Counters(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("allocs", "frees", "block_inits", "block_frees", "rollbacks",
-                                          "invalidate_fail", "reserve_retries", "oom")]
+                                          "invalidate_fail", "reserve_retries", "oom", "requests", "finds",
+                                          "find_fails", "reserve_zero", "cyc_find", "cyc_slow", "cyc_reserve",
+                                          "cyc_request")]
 
     def to_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -117,7 +119,8 @@ class NbodyArgs(C.Structure):
                 ("shandle", C.c_void_p),
                 ("x0", C.c_void_p), ("y0", C.c_void_p), ("vx0", C.c_void_p), ("vy0", C.c_void_p),
                 ("m0", C.c_void_p), ("G", C.c_float), ("dt", C.c_float), ("eps", C.c_float), ("R", C.c_float),
-                ("n_total", C.c_uint32), ("id_lo", C.c_uint32), ("id_hi", C.c_uint32), ("out", C.c_void_p)]
+                ("n_total", C.c_uint32), ("id_lo", C.c_uint32), ("id_hi", C.c_uint32), ("out", C.c_void_p),
+                ("scratch", C.c_void_p)]
 
 
 class DsrError(RuntimeError):

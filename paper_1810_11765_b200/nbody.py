@@ -68,11 +68,14 @@ class NBody:
         self.incoming = torch.full((N,), -1, dtype=torch.int32, device=dev)
         self.shandle = torch.zeros(N, dtype=torch.int64, device=dev)
         self.out = torch.zeros(N, 6, dtype=torch.float32, device=dev)
+        chunks = (N + 4095) // 4096
+        self.scratch = torch.zeros(2 * chunks * n, dtype=torch.float32, device=dev)
         i = self.init
         self.args = dsr.NbodyArgs(self.S.data_ptr(), self.V.data_ptr(), self.target.data_ptr(),
                                   self.incoming.data_ptr(), self.shandle.data_ptr(),
                                   i["x"].data_ptr(), i["y"].data_ptr(), i["vx"].data_ptr(), i["vy"].data_ptr(),
-                                  i["m"].data_ptr(), G, dt, eps, R, N, self.lo, self.hi, self.out.data_ptr())
+                                  i["m"].data_ptr(), G, dt, eps, R, N, self.lo, self.hi, self.out.data_ptr(),
+                                  self.scratch.data_ptr())
         self.heap.parallel_new(0, n, dsr.C_NB_BODY, self.args, stream)
 
     def _snapshot(self, s):
