@@ -84,6 +84,7 @@ typedef struct {
 #define DSR_F_NO_COALESCE 0x2u  /* one reservation per thread ("NoCoal") */
 #define DSR_F_STATS       0x4u  /* maintain device counters (dsr_stats) */
 #define DSR_F_SPIN_ON_OOM 0x8u  /* paper behaviour: loop forever on OOM */
+#define DSR_F_NO_HINT     0x10u /* no per-warp block hint: every request searches active[T] (paper-exact, replay) */
 
 typedef struct {
   uint32_t active_retries;   /* r: try_find_set attempts before the slow path (Fig. 11); 0 -> 5 */

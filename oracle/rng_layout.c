@@ -46,7 +46,7 @@ static void bitmap_shape(uint64_t n, uint32_t* nlevels, uint64_t* words, uint64_
 /* Byte size of every region for a given M, in the order of DESIGN.md "HBM
  * layout": control page, data, alloc_bm, iter_bm, type, R, bitmaps. */
 static uint64_t layout_for_M(or_layout_t* L, uint64_t M) {
-  uint64_t off = 4096;                          /* control page */
+  uint64_t off = 4096 + 16384 * 8 * 4;          /* control page + warp block-hint table (R-LAYOUT) */
   L->M = M;
   L->off_data = off;       off = align_up(off + M * (uint64_t)L->block_bytes, 256);
   L->off_alloc_bm = off;   off = align_up(off + M * 8, 256);

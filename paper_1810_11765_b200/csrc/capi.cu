@@ -48,6 +48,8 @@ struct dsr_heap {
     }                                                       \
   } while (0)
 
+// control page (4 KiB) + warp block-hint table (16384 hardware warp slots x 8 types x u32)
+static constexpr uint64_t kCtrlBytes = 4096 + 16384 * 8 * 4;
 static uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 // ---------------------------------------------------------------- layout
@@ -69,7 +71,7 @@ static void shape(uint64_t n, uint32_t* nlev, uint64_t* lw, uint64_t* tot) {
   *tot = t;
 }
 static uint64_t place(dsr_layout* L, uint64_t M) {
-  uint64_t off = 4096;
+  uint64_t off = kCtrlBytes;
   L->M = M;
   L->off_data = off;     off = align_up(off + M * L->block_bytes, 256);
   L->off_alloc_bm = off; off = align_up(off + M * 8, 256);
@@ -150,6 +152,7 @@ static dsr_status heap_init(dsr_heap* h, cudaStream_t st) {
   const dsr_layout& L = h->L;
   uint8_t* base = h->dev.data - L.off_data;
   CUDA_TRY(cudaMemsetAsync(base, 0, 4096, st));
+  CUDA_TRY(cudaMemsetAsync(base + 4096, 0xFF, kCtrlBytes - 4096, st));     // warp hints: none
   CUDA_TRY(cudaMemsetAsync(base + L.off_alloc_bm, 0xFF, L.M * 8, st));     // invalidated == uninitialised
   CUDA_TRY(cudaMemsetAsync(base + L.off_type, 0, L.M, st));
   CUDA_TRY(cudaMemsetAsync(base + L.off_bitmaps, 0, (1 + 2 * (uint64_t)L.ntypes) * L.bitmap_words * 8, st));
@@ -202,6 +205,7 @@ extern "C" dsr_status dsr_heap_create(const dsr_type_desc* types, uint32_t ntype
   d.type = base + L.off_type;
   d.R = (uint32_t*)(base + L.off_R);
   d.ctrl = (ull*)base;
+  d.hints = (uint32_t*)(base + 4096);
   d.M = (uint32_t)L.M;
   d.block_bytes = L.block_bytes;
   d.ntypes = ntypes;

@@ -51,6 +51,7 @@ struct DevHeap {
   uint8_t* type;          // type id per block, 1-based, 0 = never initialised
   uint32_t* R;            // do-all block list
   ull* ctrl;              // control page
+  uint32_t* hints;        // per hardware warp slot and type: the block it last allocated from
   uint32_t M;
   uint32_t block_bytes;
   uint32_t ntypes;
@@ -168,6 +169,14 @@ __device__ __forceinline__ uint64_t rot_hash(const DevHeap& h, uint64_t who, uin
 }
 __device__ __forceinline__ uint64_t warp_gid() {
   return ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+}
+// hint table slot of the calling hardware warp (SM id x warp slot; a stale or
+// shared slot only degrades the hint, never correctness)
+__device__ __forceinline__ volatile uint32_t* hint_slot(const DevHeap& h, uint32_t T) {
+  uint32_t smid, wid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+  return h.hints + (((smid << 6) | (wid & 63)) & 16383u) * DSR_MAX_TYPES + T;
 }
 
 // ------------------------------------------------------------------ hierarchical bitmap
@@ -330,11 +339,19 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
   uint32_t oom_tries = 0, fails = 0;
   long long c0 = prof ? clock64() : 0;
   if (prof) stat_add(h, ST_REQ, 1);
+  // Per-warp block hint: the block this hardware warp slot last reserved from
+  // (any active block is a valid choice); tried first, and a
+  // failed try counts as a failed lookup attempt.  Off in paper-exact mode.
+  volatile uint32_t* hs = (h.flags & DSR_F_NO_HINT) ? nullptr : hint_slot(h, T);
+  uint32_t hint = hs ? *hs : 0xFFFFFFFFu;
   for (uint64_t iter = 0;; ++iter) {
     int64_t bid = -1;
     bool fresh = false;
     long long c1 = prof ? clock64() : 0;
-    if (fails < h.r_attempts) {
+    if (hint < h.M) {
+      bid = hint;
+      hint = 0xFFFFFFFFu;
+    } else if (fails < h.r_attempts) {
       bid = bm_try_find_set(h.activebm[T], rot_hash(h, who, iter));
       if (prof) { stat_add(h, ST_FIND, 1); stat_add(h, ST_CYC_FIND, clock64() - c1); }
       if (bid < 0) { if (prof) stat_add(h, ST_FINDFAIL, 1); ++fails; continue; }
@@ -367,9 +384,11 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
     const uint64_t got = block_reserve(h, (uint32_t)bid, need, rot, &before, fresh ? &h.types[T].pad : nullptr);
     if (!got) { if (prof) stat_add(h, ST_RESZERO, 1); ++fails; continue; }    // full or invalidated
     const uint32_t t = ld_relaxed_u8(h.type + bid) - 1u;                      // volatile read (Alg. 1 l.10)
-    if ((before | got) == ~0ull) bm_clear(h.activebm[t], (uint64_t)bid);      // FULL -> inactive (l.12)
+    const bool full = (before | got) == ~0ull;
+    if (full) bm_clear(h.activebm[t], (uint64_t)bid);                         // FULL -> inactive (l.12)
     if (prof) stat_add(h, ST_CYC_RES, clock64() - c2);
     if (t == T) {
+      if (hs) *hs = full ? 0xFFFFFFFFu : (uint32_t)bid;
       if (prof) stat_add(h, ST_CYC_REQ, clock64() - c0);
       *bid_out = (uint32_t)bid;
       return got;

@@ -61,7 +61,7 @@ def test_single_thread_replay_matches_oracle(D, O, sizes, heap_bytes):
     the oracle's words, type ids and handles exactly (Algs. 1-9)."""
     tf = [split_fields(s) for s in sizes]
     rnd = random.Random(sum(sizes))
-    heap = D.Heap(tf, heap_bytes, flags=D.F_NO_ROTATE | D.F_NO_COALESCE)
+    heap = D.Heap(tf, heap_bytes, flags=D.F_NO_ROTATE | D.F_NO_COALESCE | D.F_NO_HINT)
     oh = O.PaperHeap(tf, heap_bytes)
     ops = replay_ops(rnd, len(tf), 3000)
     want = []
@@ -93,7 +93,7 @@ def test_fresh_heap_state_and_invariants(D, O):
     assert heap.fragmentation()[0] == 0.0
 
 
-@pytest.mark.parametrize("flags", [0, 1, 2, 3])
+@pytest.mark.parametrize("flags", [0, 1, 2, 3, 16])
 def test_torture_concurrent_new_destroy(D, flags):
     """Many warps call new/destroy from divergent lanes; afterwards: no canary
     damage, every quiescent invariant holds, the live set equals the ledger."""
