@@ -45,8 +45,16 @@ static void bitmap_shape(uint64_t n, uint32_t* nlevels, uint64_t* words, uint64_
 
 /* Byte size of every region for a given M, in the order of DESIGN.md "HBM
  * layout": control page, data, alloc_bm, iter_bm, type, R, bitmaps. */
-static uint64_t layout_for_M(or_layout_t* L, uint64_t M) {
-  uint64_t off = 4096 + 16384 * 8 * 4;          /* control page + warp block-hint table (R-LAYOUT) */
+/* control page (4 KiB) + per-warp block-hint table of H slots x 8 types x
+ * u32, H = pow2floor(heap_bytes / 64 KiB) clamped to [64, 16384] (R-LAYOUT) */
+static uint64_t ctrl_bytes(uint64_t heap_bytes) {
+  uint64_t h = 64;
+  while (h * 2 <= (heap_bytes >> 16) && h < 16384) h *= 2;
+  return 4096 + h * 8 * 4;
+}
+
+static uint64_t layout_for_M(or_layout_t* L, uint64_t M, uint64_t heap_bytes) {
+  uint64_t off = ctrl_bytes(heap_bytes);
   L->M = M;
   L->off_data = off;       off = align_up(off + M * (uint64_t)L->block_bytes, 256);
   L->off_alloc_bm = off;   off = align_up(off + M * 8, 256);
@@ -106,9 +114,9 @@ int or_layout(uint32_t ntypes, const uint32_t* nfields, const uint32_t* fsizes_f
   if (hi > 0xFFFFFFFFULL) hi = 0xFFFFFFFFULL;
   while (lo < hi) {
     uint64_t mid = lo + (hi - lo + 1) / 2;
-    if (layout_for_M(L, mid) <= heap_bytes) lo = mid; else hi = mid - 1;
+    if (layout_for_M(L, mid, heap_bytes) <= heap_bytes) lo = mid; else hi = mid - 1;
   }
   if (lo == 0) return 3;
-  layout_for_M(L, lo);
+  layout_for_M(L, lo, heap_bytes);
   return 0;
 }

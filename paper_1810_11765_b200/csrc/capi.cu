@@ -48,8 +48,14 @@ struct dsr_heap {
     }                                                       \
   } while (0)
 
-// control page (4 KiB) + warp block-hint table (16384 hardware warp slots x 8 types x u32)
-static constexpr uint64_t kCtrlBytes = 4096 + 16384 * 8 * 4;
+// control page (4 KiB) + warp block-hint table: H hardware-warp slots x 8 types
+// x u32, H = pow2floor(heap_bytes / 64 KiB) clamped to [64, 16384] (R-LAYOUT)
+static uint64_t hint_slots(uint64_t heap_bytes) {
+  uint64_t h = 64;
+  while (h * 2 <= (heap_bytes >> 16) && h < 16384) h *= 2;
+  return h;
+}
+static uint64_t ctrl_bytes(uint64_t heap_bytes) { return 4096 + hint_slots(heap_bytes) * 8 * 4; }
 static uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 // ---------------------------------------------------------------- layout
@@ -70,8 +76,8 @@ static void shape(uint64_t n, uint32_t* nlev, uint64_t* lw, uint64_t* tot) {
   *nlev = l;
   *tot = t;
 }
-static uint64_t place(dsr_layout* L, uint64_t M) {
-  uint64_t off = kCtrlBytes;
+static uint64_t place(dsr_layout* L, uint64_t M, uint64_t heap_bytes) {
+  uint64_t off = ctrl_bytes(heap_bytes);
   L->M = M;
   L->off_data = off;     off = align_up(off + M * L->block_bytes, 256);
   L->off_alloc_bm = off; off = align_up(off + M * 8, 256);
@@ -125,10 +131,10 @@ extern "C" dsr_status dsr_layout_compute(const dsr_type_desc* types, uint32_t nt
   if (hi > 0xFFFFFFFFull) hi = 0xFFFFFFFFull;
   while (lo < hi) {
     const uint64_t mid = lo + (hi - lo + 1) / 2;
-    if (place(L, mid) <= heap_bytes) lo = mid; else hi = mid - 1;
+    if (place(L, mid, heap_bytes) <= heap_bytes) lo = mid; else hi = mid - 1;
   }
   if (lo == 0) return DSR_ERR_INVALID;
-  place(L, lo);
+  place(L, lo, heap_bytes);
   return DSR_OK;
 }
 
@@ -152,7 +158,7 @@ static dsr_status heap_init(dsr_heap* h, cudaStream_t st) {
   const dsr_layout& L = h->L;
   uint8_t* base = h->dev.data - L.off_data;
   CUDA_TRY(cudaMemsetAsync(base, 0, 4096, st));
-  CUDA_TRY(cudaMemsetAsync(base + 4096, 0xFF, kCtrlBytes - 4096, st));     // warp hints: none
+  CUDA_TRY(cudaMemsetAsync(base + 4096, 0xFF, (h->dev.hint_mask + 1) * 8 * 4, st));   // warp hints: none
   CUDA_TRY(cudaMemsetAsync(base + L.off_alloc_bm, 0xFF, L.M * 8, st));     // invalidated == uninitialised
   CUDA_TRY(cudaMemsetAsync(base + L.off_type, 0, L.M, st));
   CUDA_TRY(cudaMemsetAsync(base + L.off_bitmaps, 0, (1 + 2 * (uint64_t)L.ntypes) * L.bitmap_words * 8, st));
@@ -206,6 +212,7 @@ extern "C" dsr_status dsr_heap_create(const dsr_type_desc* types, uint32_t ntype
   d.R = (uint32_t*)(base + L.off_R);
   d.ctrl = (ull*)base;
   d.hints = (uint32_t*)(base + 4096);
+  d.hint_mask = (uint32_t)hint_slots(heap_bytes) - 1;
   d.M = (uint32_t)L.M;
   d.block_bytes = L.block_bytes;
   d.ntypes = ntypes;

@@ -57,7 +57,7 @@ struct DevHeap {
   uint32_t ntypes;
   uint32_t r_attempts;
   uint32_t flags;
-  uint32_t pad_;
+  uint32_t hint_mask;     // hint slots - 1 (power of two)
   uint64_t seed;
   DevBitmap freebm;
   DevBitmap allocbm[DSR_MAX_TYPES];
@@ -176,7 +176,7 @@ __device__ __forceinline__ volatile uint32_t* hint_slot(const DevHeap& h, uint32
   uint32_t smid, wid;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
   asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
-  return h.hints + (((smid << 6) | (wid & 63)) & 16383u) * DSR_MAX_TYPES + T;
+  return h.hints + (((smid << 6) | (wid & 63)) & h.hint_mask) * DSR_MAX_TYPES + T;
 }
 
 // ------------------------------------------------------------------ hierarchical bitmap

@@ -88,7 +88,7 @@ def test_layout_M_is_maximal(O):
     # the next block count would not fit: shrinking the heap by the per-block
     # cost must lose a block
     tf = [[4, 4, 4], [4, 4, 4, 4], [4] * 6]
-    L = O.layout(tf, 1 << 28)
+    L = O.layout(tf, 1 << 31)              # >= 1 GiB: the hint table is at its maximum size
     L2 = O.layout(tf, L["total_bytes"])
     assert L2["M"] == L["M"]
     L3 = O.layout(tf, L["total_bytes"] - 1)
