@@ -54,16 +54,30 @@ __device__ __forceinline__ uint64_t new_cand(const DevHeap& h, uint32_t c) {
 // ---- initial state: Alive for alive cells, Candidate for dead cells with an alive neighbour
 __global__ void __launch_bounds__(256) k_gol_init(DevHeap h, uint64_t n, dsr_gol_args a, int cand) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride) {   // uniform trip count
+    const uint64_t i = base + threadIdx.x;
     const uint32_t c = (uint32_t)i;
-    const bool alive = a.alive0[c];
-    if (!cand) {
-      if (alive) a.cell[c] = new_alive(h, c, 0);
-    } else if (!alive) {
-      bool any = false;
-      for (int d = 0; d < 8; ++d) any |= a.alive0[gol_nbr(a.W, a.H, c, d)] != 0;
-      if (any) a.cell[c] = new_cand(h, c);
+    bool want = false;
+    if (i < n) {
+      const bool alive = a.alive0[c];
+      if (!cand) {
+        want = alive;
+      } else if (!alive) {
+        for (int d = 0; d < 8; ++d) want |= a.alive0[gol_nbr(a.W, a.H, c, d)] != 0;
+      }
     }
+    const uint32_t T = cand ? GOL_CAND : GOL_ALIVE;
+    const uint64_t nh = dsr_new_uniform(h, T, want);
+    if (nh) {
+      *field_ptr<uint32_t>(h, nh, 0) = c;
+      if (!cand) {
+        *field_ptr<uint8_t>(h, nh, 1) = 0;
+        *field_ptr<uint8_t>(h, nh, 2) = ACT_NONE;
+      } else {
+        *field_ptr<uint8_t>(h, nh, 1) = ACT_NONE;
+      }
+    }
+    if (want) a.cell[c] = nh;
   }
 }
 

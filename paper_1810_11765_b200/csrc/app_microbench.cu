@@ -11,10 +11,12 @@ __constant__ uint32_t kMbType[4] = {0, 0, 1, 2};   // [A, A, B, C][t & 3]
 // ---- phase 1 / 4: user kernel, thread t does new [A,A,B,C][t&3] (device new)
 __global__ void __launch_bounds__(256) k_mb_new(DevHeap h, uint64_t n, dsr_mb_new_args a) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+  // uniform trip count: every thread of the CTA reaches dsr_new_uniform together
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const uint64_t i = base + threadIdx.x;
     const uint64_t t = a.t0 + i;
     const uint32_t T = kMbType[t & 3];
-    const uint64_t hd = dsr_new(h, T);
+    const uint64_t hd = (h.flags & DSR_F_WARP_NEW) ? (i < n ? dsr_new(h, T) : 0) : dsr_new_uniform(h, T, i < n);
     if (hd) {
       const uint32_t nf = h.types[T].nfields;
       for (uint32_t k = 0; k < nf; ++k)

@@ -29,8 +29,9 @@ __device__ __forceinline__ float4 s4(const dsr_nbody_args& a, uint32_t id) {
 // ---- parallel_new<Body>(n): body i gets id id_lo + i
 __global__ void __launch_bounds__(256) k_nb_new(DevHeap h, uint64_t n, dsr_nbody_args a) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint64_t nh = dsr_new(h, 0);
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride) {   // uniform trip count
+    const uint64_t i = base + threadIdx.x;
+    const uint64_t nh = dsr_new_uniform(h, 0, i < n);
     if (!nh) continue;
     const uint32_t b = h_bid(nh), s = h_slot(nh);
     bf<float>(h, b, s, NB_X) = a.x0[i];

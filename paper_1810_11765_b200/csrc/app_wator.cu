@@ -57,24 +57,31 @@ __device__ __forceinline__ uint64_t new_shark(const DevHeap& h, uint32_t c, uint
 // ---- parallel_new<Cell>(W*H): constructor i gets id i
 __global__ void __launch_bounds__(256) k_wt_new_cells(DevHeap h, uint64_t n, dsr_wator_args a) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint64_t nh = dsr_new(h, WT_CELL);
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride) {   // uniform trip count
+    const uint64_t i = base + threadIdx.x;
+    const uint64_t nh = dsr_new_uniform(h, WT_CELL, i < n);
     if (nh) {
       *field_ptr<uint32_t>(h, nh, 0) = (uint32_t)i;
       *field_ptr<uint64_t>(h, nh, 1) = 0;
       for (uint32_t k = 0; k < 5; ++k) *field_ptr<uint8_t>(h, nh, 2 + k) = 0;
     }
-    a.cells[i] = nh;
+    if (i < n) a.cells[i] = nh;
   }
 }
 __global__ void __launch_bounds__(256) k_wt_init_agents(DevHeap h, uint64_t n, dsr_wator_args a) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride) {   // uniform trip count
+    const uint64_t i = base + threadIdx.x;
     const uint32_t c = (uint32_t)i;
-    const uint8_t k = a.kind0[c];
-    uint64_t nh = 0;
-    if (k == 1) nh = new_fish(h, c, a.egg0[c]);
-    else if (k == 2) nh = new_shark(h, c, a.egg0[c], a.energy0[c]);
+    const uint8_t k = i < n ? a.kind0[c] : 0;
+    const uint32_t T = k == 2 ? WT_SHARK : WT_FISH;
+    const uint64_t nh = dsr_new_uniform(h, T, k != 0);
+    if (nh) {
+      *field_ptr<uint32_t>(h, nh, 0) = c;
+      *field_ptr<uint32_t>(h, nh, 1) = c;
+      *field_ptr<uint32_t>(h, nh, 2) = a.egg0[c];
+      if (T == WT_SHARK) *field_ptr<uint32_t>(h, nh, 3) = a.energy0[c];
+    }
     if (k) *wt_agent(h, a, c) = nh;
   }
 }

@@ -428,6 +428,64 @@ __device__ __forceinline__ uint64_t dsr_new(const DevHeap& h, uint32_t T) {
   return mine;
 }
 
+// Device new<T> for UNIFORM call sites (every thread of the CTA calls it; a
+// thread that needs no object passes want = false): request coalescing at CTA
+// granularity (an extension of the paper's warp-level coalescing, for
+// bulk constructors such as parallel_new).  Threads rank themselves per
+// type in shared memory; one leader lane per type (warp 0) reserves all slots
+// of its type, possibly over several blocks (partial fills move on to another
+// block); each thread takes the rank-th reserved slot.  Up to 1024
+// threads per CTA.  Returns 0 on OOM (sticky error set by the leader).
+__device__ __forceinline__ uint64_t dsr_new_uniform(const DevHeap& h, uint32_t T, bool want) {
+  __shared__ uint32_t s_cnt[DSR_MAX_TYPES], s_pre[DSR_MAX_TYPES], s_nch[DSR_MAX_TYPES];
+  __shared__ uint32_t s_bid[1024], s_cum[1024];
+  __shared__ uint64_t s_mask[1024];
+  const uint32_t tid = threadIdx.x;
+  if (tid < DSR_MAX_TYPES) s_cnt[tid] = 0;
+  __syncthreads();
+  const uint32_t rank = want ? atomicAdd(&s_cnt[T], 1u) : 0u;
+  __syncthreads();
+  if (tid < 32) {
+    const uint32_t t = tid;
+    uint32_t pre = 0;
+    for (uint32_t u = 0; u < t && u < DSR_MAX_TYPES; ++u) pre += s_cnt[u];
+    if (t < h.ntypes && s_cnt[t] > 0) {
+      const uint32_t need = s_cnt[t];
+      uint32_t k = pre, done = 0;
+      while (done < need) {
+        uint32_t bid = 0;
+        const uint64_t got = reserve_chunk(h, t, need - done, &bid);
+        if (!got) break;                                     // OOM: the rest get null
+        s_bid[k] = bid;
+        s_mask[k] = got;
+        s_cum[k] = done;
+        done += __popcll(got);
+        ++k;
+      }
+      s_pre[t] = pre;
+      s_nch[t] = k - pre;
+      stat_add(h, ST_ALLOCS, done);
+    }
+  }
+  __syncthreads();
+  uint64_t mine = 0;
+  if (want) {
+    const uint32_t b0 = s_pre[T], n = s_nch[T];
+    uint32_t lo = 0, hi = n;                                 // last chunk with s_cum <= rank
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (s_cum[b0 + mid] <= rank) lo = mid; else hi = mid;
+    }
+    if (n) {
+      const uint64_t m = s_mask[b0 + lo];
+      const uint32_t off = rank - s_cum[b0 + lo];
+      if (off < (uint32_t)__popcll(m)) mine = make_handle(T, h.types[T].cap, s_bid[b0 + lo], nth_bit(m, off));
+    }
+  }
+  __syncthreads();   // shared state reused by the next call; orders the leaders' acquire before the writes
+  return mine;
+}
+
 // Device destroy: lanes freeing slots of the same block combine their
 // bits into one atomicAnd (coalesced version of Alg. 7).
 __device__ __forceinline__ void dsr_destroy(const DevHeap& h, uint64_t x) {
