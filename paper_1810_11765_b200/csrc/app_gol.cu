@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256) k_gol_init(DevHeap h, uint64_t n, dsr_gol
       }
     }
     const uint32_t T = cand ? GOL_CAND : GOL_ALIVE;
-    const uint64_t nh = dsr_new_uniform(h, T, want);
+    const uint64_t nh = dsr_new_bulk(h, T, want);
     if (nh) {
       *field_ptr<uint32_t>(h, nh, 0) = c;
       if (!cand) {

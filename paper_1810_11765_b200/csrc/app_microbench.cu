@@ -16,7 +16,7 @@ __global__ void __launch_bounds__(256) k_mb_new(DevHeap h, uint64_t n, dsr_mb_ne
     const uint64_t i = base + threadIdx.x;
     const uint64_t t = a.t0 + i;
     const uint32_t T = kMbType[t & 3];
-    const uint64_t hd = (h.flags & DSR_F_WARP_NEW) ? (i < n ? dsr_new(h, T) : 0) : dsr_new_uniform(h, T, i < n);
+    const uint64_t hd = dsr_new_bulk(h, T, i < n);
     if (hd) {
       const uint32_t nf = h.types[T].nfields;
       for (uint32_t k = 0; k < nf; ++k)

@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(256) k_nb_new(DevHeap h, uint64_t n, dsr_nbody
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride) {   // uniform trip count
     const uint64_t i = base + threadIdx.x;
-    const uint64_t nh = dsr_new_uniform(h, 0, i < n);
+    const uint64_t nh = dsr_new_bulk(h, 0, i < n);
     if (!nh) continue;
     const uint32_t b = h_bid(nh), s = h_slot(nh);
     bf<float>(h, b, s, NB_X) = a.x0[i];

@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(256) k_wt_new_cells(DevHeap h, uint64_t n, dsr
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride) {   // uniform trip count
     const uint64_t i = base + threadIdx.x;
-    const uint64_t nh = dsr_new_uniform(h, WT_CELL, i < n);
+    const uint64_t nh = dsr_new_bulk(h, WT_CELL, i < n);
     if (nh) {
       *field_ptr<uint32_t>(h, nh, 0) = (uint32_t)i;
       *field_ptr<uint64_t>(h, nh, 1) = 0;
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(256) k_wt_init_agents(DevHeap h, uint64_t n, d
     const uint32_t c = (uint32_t)i;
     const uint8_t k = i < n ? a.kind0[c] : 0;
     const uint32_t T = k == 2 ? WT_SHARK : WT_FISH;
-    const uint64_t nh = dsr_new_uniform(h, T, k != 0);
+    const uint64_t nh = dsr_new_bulk(h, T, k != 0);
     if (nh) {
       *field_ptr<uint32_t>(h, nh, 0) = c;
       *field_ptr<uint32_t>(h, nh, 1) = c;

@@ -245,7 +245,23 @@ __device__ __forceinline__ bool bm_get(const DevBitmap& b, uint64_t pos) {
 // bits of `rh` before ffs.  May FAIL spuriously.
 __device__ __forceinline__ int64_t bm_try_find_set(const DevBitmap& b, uint64_t rh) {
   uint64_t cid = 0;
-  for (int l = (int)b.nlevels - 1; l >= 0; --l) {
+  int top = (int)b.nlevels - 1;
+  if (rh != 0 && b.nlevels >= 3) {
+    // Rotation of the upper levels taken to its limit: enter the hierarchy at a
+    // level-1 container picked by the hash instead of re-reading the few
+    // top-level words that every concurrent search shares (one L2 slice each);
+    // an empty pick falls back to the top-down walk.  Any set bit is a valid
+    // result of try_find_set.
+    const uint64_t n1 = ((((uint64_t)b.nbits + 63) >> 6) + 63) >> 6;
+    const uint64_t i1 = __umul64hi(rh, n1);
+    const uint64_t c1 = ld_relaxed(b.lvl[1] + i1);
+    if (c1 != 0) {
+      const uint32_t r = (uint32_t)(rh >> 6) & 63u;
+      cid = i1 * 64 + (((uint32_t)__ffsll((long long)rotr64(c1, r)) - 1u + r) & 63u);
+      top = 0;
+    }
+  }
+  for (int l = top; l >= 0; --l) {
     const uint64_t c = ld_relaxed(b.lvl[l] + cid);
     if (c == 0) return -1;
     const uint32_t r = (uint32_t)(rh >> (6 * l)) & 63u;
@@ -484,6 +500,14 @@ __device__ __forceinline__ uint64_t dsr_new_uniform(const DevHeap& h, uint32_t T
   }
   __syncthreads();   // shared state reused by the next call; orders the leaders' acquire before the writes
   return mine;
+}
+
+// Bulk constructors (uniform call sites): warp-level coalescing by default,
+// CTA-level with DSR_F_CTA_NEW (measured slower on B200: fewer concurrent
+// leaders hide less latency -- kept as an ablation).
+__device__ __forceinline__ uint64_t dsr_new_bulk(const DevHeap& h, uint32_t T, bool want) {
+  if (h.flags & DSR_F_CTA_NEW) return dsr_new_uniform(h, T, want);
+  return want ? dsr_new(h, T) : 0ull;
 }
 
 // Device destroy: lanes freeing slots of the same block combine their
