@@ -243,32 +243,26 @@ __device__ __forceinline__ bool bm_get(const DevBitmap& b, uint64_t pos) {
 
 // Alg. 4 try_find_set, top-down; each level's container is rotated by 6
 // bits of `rh` before ffs.  May FAIL spuriously.
-__device__ __forceinline__ int64_t bm_try_find_set(const DevBitmap& b, uint64_t rh) {
+__device__ __forceinline__ int64_t bm_try_find_set(const DevBitmap& b, uint64_t rh, uint64_t* leaf = nullptr) {
   uint64_t cid = 0;
-  int top = (int)b.nlevels - 1;
-  if (rh != 0 && b.nlevels >= 3) {
-    // Rotation of the upper levels taken to its limit: enter the hierarchy at a
-    // level-1 container picked by the hash instead of re-reading the few
-    // top-level words that every concurrent search shares (one L2 slice each);
-    // an empty pick falls back to the top-down walk.  Any set bit is a valid
-    // result of try_find_set.
-    const uint64_t n1 = ((((uint64_t)b.nbits + 63) >> 6) + 63) >> 6;
-    const uint64_t i1 = __umul64hi(rh, n1);
-    const uint64_t c1 = ld_relaxed(b.lvl[1] + i1);
-    if (c1 != 0) {
-      const uint32_t r = (uint32_t)(rh >> 6) & 63u;
-      cid = i1 * 64 + (((uint32_t)__ffsll((long long)rotr64(c1, r)) - 1u + r) & 63u);
-      top = 0;
-    }
-  }
-  for (int l = top; l >= 0; --l) {
+  for (int l = (int)b.nlevels - 1; l >= 0; --l) {
     const uint64_t c = ld_relaxed(b.lvl[l] + cid);
     if (c == 0) return -1;
     const uint32_t r = (uint32_t)(rh >> (6 * l)) & 63u;
     const uint32_t i = ((uint32_t)__ffsll((long long)rotr64(c, r)) - 1u + r) & 63u;
     cid = cid * 64 + i;
+    if (l == 0 && leaf) *leaf = c;     // the leaf container the result came from
   }
   return (int64_t)cid;
+}
+// next set bit of the leaf container `c` after position pos (cyclic), -1 if none
+__device__ __forceinline__ int64_t leaf_next(uint64_t c, uint64_t pos) {
+  const uint32_t p = (uint32_t)(pos & 63);
+  c &= ~(1ull << p);
+  if (c == 0) return -1;
+  const uint32_t r = (p + 1) & 63u;
+  const uint32_t i = ((uint32_t)__ffsll((long long)rotr64(c, r)) - 1u + r) & 63u;
+  return (int64_t)((pos & ~63ull) | i);
 }
 // clear(): find + try_clear until the clear succeeds (reading R-CLEARANY)
 __device__ __forceinline__ int64_t bm_clear_any(const DevHeap& h, const DevBitmap& b, uint64_t who, uint64_t retry0) {
@@ -368,9 +362,21 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
       bid = hint;
       hint = 0xFFFFFFFFu;
     } else if (fails < h.r_attempts) {
-      bid = bm_try_find_set(h.activebm[T], rot_hash(h, who, iter));
+      uint64_t leaf = 0;
+      bid = bm_try_find_set(h.activebm[T], rot_hash(h, who, iter), &leaf);
       if (prof) { stat_add(h, ST_FIND, 1); stat_add(h, ST_CYC_FIND, clock64() - c1); }
       if (bid < 0) { if (prof) stat_add(h, ST_FINDFAIL, 1); ++fails; continue; }
+      // A block just filled by another warp stays in active[T] until its
+      // filler deactivates it; rather than failing the whole lookup, probe up
+      // to 3 other active blocks of the same leaf container (one load each).
+      if (!(h.flags & DSR_F_NO_ROTATE)) {
+        for (int p = 0; p < 3 && ld_relaxed(h.alloc_bm + bid) == ~0ull; ++p) {
+          leaf &= ~(1ull << (bid & 63));
+          const int64_t nb = leaf_next(leaf | (1ull << (bid & 63)), (uint64_t)bid);
+          if (nb < 0) break;
+          bid = nb;
+        }
+      }
     } else {                                                                  // slow path
       bid = bm_clear_any(h, h.freebm, who, iter << 8);
       if (bid < 0) {
