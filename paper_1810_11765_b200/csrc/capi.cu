@@ -213,6 +213,7 @@ extern "C" dsr_status dsr_heap_create(const dsr_type_desc* types, uint32_t ntype
   d.ctrl = (ull*)base;
   d.hints = (uint32_t*)(base + 4096);
   d.hint_mask = (uint32_t)hint_slots(heap_bytes) - 1;
+  d.sms = (uint32_t)h->sms;
   d.M = (uint32_t)L.M;
   d.block_bytes = L.block_bytes;
   d.ntypes = ntypes;

@@ -58,6 +58,8 @@ struct DevHeap {
   uint32_t r_attempts;
   uint32_t flags;
   uint32_t hint_mask;     // hint slots - 1 (power of two)
+  uint32_t sms;           // SM count (SM-affine rotation)
+  uint32_t pad2_;
   uint64_t seed;
   DevBitmap freebm;
   DevBitmap allocbm[DSR_MAX_TYPES];
@@ -255,6 +257,39 @@ __device__ __forceinline__ int64_t bm_try_find_set(const DevBitmap& b, uint64_t 
   }
   return (int64_t)cid;
 }
+// SM-affine rotation ("rotating-shifted by a value depending on the warp
+// ID and a seed"): the warps of SM s start every search inside their own
+// contiguous range of level-1 containers, so concurrent searches and new
+// blocks of different SMs land in different containers and cache lines.
+__device__ __forceinline__ void home_range(const DevBitmap& b, uint32_t sms, uint32_t* lo, uint32_t* len) {
+  const uint32_t n1 = (uint32_t)(((((uint64_t)b.nbits + 63) >> 6) + 63) >> 6);
+  uint32_t smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  smid %= sms;
+  uint32_t a = (uint32_t)((uint64_t)smid * n1 / sms), e = (uint32_t)((uint64_t)(smid + 1) * n1 / sms);
+  if (e <= a) { a = a < n1 ? a : n1 - 1; e = a + 1; }      // small heaps: SMs share containers
+  *lo = a;
+  *len = e - a;
+}
+// try_find_set restricted to the home range (levels 1 and 0, rotated); -1 if
+// the probed containers are empty (the caller then counts a failed attempt)
+__device__ __forceinline__ int64_t bm_find_home(const DevBitmap& b, uint32_t lo, uint32_t len, uint64_t rh,
+                                                uint64_t* leaf = nullptr) {
+  const uint32_t start = (uint32_t)(rh % len);
+  for (uint32_t k = 0; k < len && k < 8; ++k) {
+    const uint32_t i1 = lo + (start + k) % len;
+    const uint64_t c1 = ld_relaxed(b.lvl[1] + i1);
+    if (!c1) continue;
+    const uint32_t r1 = (uint32_t)(rh >> 8) & 63u;
+    const uint64_t i0 = (uint64_t)i1 * 64 + ((((uint32_t)__ffsll((long long)rotr64(c1, r1))) - 1u + r1) & 63u);
+    const uint64_t c0 = ld_relaxed(b.lvl[0] + i0);
+    if (!c0) continue;
+    const uint32_t r0 = (uint32_t)(rh >> 14) & 63u;
+    if (leaf) *leaf = c0;
+    return (int64_t)(i0 * 64 + ((((uint32_t)__ffsll((long long)rotr64(c0, r0))) - 1u + r0) & 63u));
+  }
+  return -1;
+}
 // next set bit of the leaf container `c` after position pos (cyclic), -1 if none
 __device__ __forceinline__ int64_t leaf_next(uint64_t c, uint64_t pos) {
   const uint32_t p = (uint32_t)(pos & 63);
@@ -354,6 +389,9 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
   // failed try counts as a failed lookup attempt.  Off in paper-exact mode.
   volatile uint32_t* hs = (h.flags & DSR_F_NO_HINT) ? nullptr : hint_slot(h, T);
   uint32_t hint = hs ? *hs : 0xFFFFFFFFu;
+  const bool home = !(h.flags & (DSR_F_NO_ROTATE | DSR_F_GLOBAL_ROT)) && h.freebm.nlevels >= 2;
+  uint32_t hlo = 0, hlen = 1;
+  if (home) home_range(h.freebm, h.sms, &hlo, &hlen);
   for (uint64_t iter = 0;; ++iter) {
     int64_t bid = -1;
     bool fresh = false;
@@ -363,7 +401,8 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
       hint = 0xFFFFFFFFu;
     } else if (fails < h.r_attempts) {
       uint64_t leaf = 0;
-      bid = bm_try_find_set(h.activebm[T], rot_hash(h, who, iter), &leaf);
+      bid = home ? bm_find_home(h.activebm[T], hlo, hlen, rot_hash(h, who, iter), &leaf)
+                 : bm_try_find_set(h.activebm[T], rot_hash(h, who, iter), &leaf);
       if (prof) { stat_add(h, ST_FIND, 1); stat_add(h, ST_CYC_FIND, clock64() - c1); }
       if (bid < 0) { if (prof) stat_add(h, ST_FINDFAIL, 1); ++fails; continue; }
       // A block just filled by another warp stays in active[T] until its
@@ -378,7 +417,13 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
         }
       }
     } else {                                                                  // slow path
-      bid = bm_clear_any(h, h.freebm, who, iter << 8);
+      bid = -1;
+      for (int k = 0; home && bid < 0 && k < 4; ++k) {                        // a free block in the home range
+        const int64_t c = bm_find_home(h.freebm, hlo, hlen, rot_hash(h, who, (iter << 8) + 64 + k));
+        if (c < 0) break;
+        if (bm_try_clear(h.freebm, (uint64_t)c)) bid = c;
+      }
+      if (bid < 0) bid = bm_clear_any(h, h.freebm, who, iter << 8);
       if (bid < 0) {
         // FAIL: free bitmap empty, or transiently inconsistent.  Only a
         // top-level word of 0 counts towards OOM.

@@ -4,6 +4,6 @@ python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 timeout -s KILL 1500 python -m pytest tests -m "gpu and not slow" -q --timeout 600 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
 echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
 rm -f gpurun_out/prof_mb.log
-for a in "0 5" "32 5" "0 1" "0 2" "4 5"; do echo "== $a" >> gpurun_out/prof_mb.log; timeout -s KILL 60 python scripts/prof_mb.py $a >> gpurun_out/prof_mb.log 2>&1; echo "rc $?" >> gpurun_out/prof_mb.log; done
+for a in "0 5" "64 5" "0 1" "0 2" "4 5" "80 5"; do echo "== $a" >> gpurun_out/prof_mb.log; timeout -s KILL 60 python scripts/prof_mb.py $a >> gpurun_out/prof_mb.log 2>&1; echo "rc $?" >> gpurun_out/prof_mb.log; done
 timeout -s KILL 300 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1
 timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1
