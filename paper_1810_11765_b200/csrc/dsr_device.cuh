@@ -389,7 +389,10 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
   // failed try counts as a failed lookup attempt.  Off in paper-exact mode.
   volatile uint32_t* hs = (h.flags & DSR_F_NO_HINT) ? nullptr : hint_slot(h, T);
   uint32_t hint = hs ? *hs : 0xFFFFFFFFu;
-  const bool home = !(h.flags & (DSR_F_NO_ROTATE | DSR_F_GLOBAL_ROT)) && h.freebm.nlevels >= 2;
+  // SM-affine home ranges are an ablation (DSR_F_HOME_ROT): measured slower than
+  // the hashed global rotation (all 64 warps of an SM pile onto the few active
+  // blocks of its range) and it strands active blocks of other ranges near OOM.
+  const bool home = (h.flags & DSR_F_HOME_ROT) && !(h.flags & DSR_F_NO_ROTATE) && h.freebm.nlevels >= 2;
   uint32_t hlo = 0, hlen = 1;
   if (home) home_range(h.freebm, h.sms, &hlo, &hlen);
   for (uint64_t iter = 0;; ++iter) {
