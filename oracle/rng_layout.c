@@ -22,7 +22,6 @@ uint64_t or_key(uint64_t seed, uint64_t step, uint64_t phase, uint64_t idx) {
 }
 
 static uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
-static uint64_t pow2ceil(uint64_t x) { uint64_t p = 1; while (p < x) p <<= 1; return p; }
 
 /* Number of levels and words of a hierarchical bitmap of n bits with 64-bit
  * containers: "an array of size ceil(N/64) of 64-bit containers, and a nested
@@ -95,14 +94,12 @@ int or_layout(uint32_t ntypes, const uint32_t* nfields, const uint32_t* fsizes_f
     uint64_t cap = 64 * smin / size[t];
     if (cap < 1) return 2;                       /* "more than 64 times bigger" P:313 */
     L->cap[t] = (uint32_t)cap;
-    /* SOA columns, each aligned to min(128, pow2 >= N_T*s_f), >= 16 (C20) */
+    /* SOA columns packed back to back, each 16-byte aligned (R-LAYOUT: a
+     * 128-bit vector load per column segment; the block is 128-aligned) */
     uint64_t off = 0, end = 0;
     for (uint32_t f = 0; f < L->nfields[t]; f++) {
       uint64_t colb = cap * L->fsize[t][f];
-      uint64_t a = pow2ceil(colb);
-      if (a > 128) a = 128;
-      if (a < 16) a = 16;
-      off = align_up(end, a);
+      off = align_up(end, 16);
       L->col_off[t][f] = (uint32_t)off;
       end = off + colb;
     }

@@ -118,9 +118,7 @@ extern "C" dsr_status dsr_layout_compute(const dsr_type_desc* types, uint32_t nt
     uint64_t end = 0;
     for (uint32_t f = 0; f < types[t].num_fields; ++f) {
       const uint64_t bytes = cap * types[t].field_bytes[f];
-      uint64_t a = 16;
-      while (a < bytes && a < 128) a <<= 1;                  // min(128, pow2 >= bytes), >= 16
-      const uint64_t off = align_up(end, a);
+      const uint64_t off = align_up(end, 16);                // columns packed, 16-B aligned (R-LAYOUT)
       L->col_off[t][f] = (uint32_t)off;
       end = off + bytes;
     }

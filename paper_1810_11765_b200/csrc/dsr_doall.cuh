@@ -19,7 +19,7 @@
 
 namespace dsr {
 
-constexpr int kCompactThreads = 256;
+constexpr int kCompactThreads = 64;   // small CTAs: ~8 per SM at M = 4.6 M blocks (latency-bound)
 
 static __global__ void __launch_bounds__(kCompactThreads) k_compact(DevHeap h, uint32_t T, int snapshot) {
   __shared__ uint64_t s_word[kCompactThreads];
