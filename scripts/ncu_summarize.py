@@ -27,7 +27,7 @@ for rep in sys.argv[2:]:
     if len(rows) < 3:
         continue
     h, units = rows[0], rows[1]
-    stall_cols = [i for i, n in enumerate(h) if n.startswith("smsp__average_warp_latency_issue_stalled_") and n.endswith(".ratio")]
+    stall_cols = [i for i, n in enumerate(h) if n.startswith("smsp__average_warps_issue_stalled_") and n.endswith("_per_issue_active.ratio")]
     for r in rows[2:]:
         d = {"report": rep.split("/")[-1], "kernel": r[h.index("Kernel Name")][:90]}
         for k, name in KEYS.items():
@@ -41,7 +41,7 @@ for rep in sys.argv[2:]:
         stalls = []
         for i in stall_cols:
             try:
-                stalls.append((float(r[i].replace(",", "")), h[i].replace("smsp__average_warp_latency_issue_stalled_", "").replace(".ratio", "")))
+                stalls.append((float(r[i].replace(",", "")), h[i].replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", "")))
             except ValueError:
                 pass
         d["top_stalls_cycles_per_issue"] = [(n, round(v, 2)) for v, n in sorted(stalls, reverse=True)[:5]]
