@@ -45,14 +45,16 @@ class Exchange:
 
 class NBody:
     def __init__(self, state, G, dt, eps, R, merges=True, heap_bytes=None, device=None, stream=None, group=None,
-                 n_total=None):
-        """state: dict of x, y, vx, vy, m for ALL ids (each rank keeps its chunk)."""
+                 n_total=None, shard=None):
+        """state: dict of x, y, vx, vy, m for ALL ids (each rank keeps its chunk).
+        shard = (rank, world) emulates a rank without a process group (loopback)."""
         import numpy as np
         import torch
         self.xch = Exchange(group)
+        self.rank, self.world = shard if shard is not None else (self.xch.rank, self.xch.world)
         N = n_total or len(state["x"])
         self.n_total = N
-        self.lo, self.hi = id_range(N, self.xch.world, self.xch.rank)
+        self.lo, self.hi = id_range(N, self.world, self.rank)
         n = self.hi - self.lo
         self.merges = merges
         if heap_bytes is None:
@@ -78,30 +80,48 @@ class NBody:
                                   self.scratch.data_ptr())
         self.heap.parallel_new(0, n, dsr.C_NB_BODY, self.args, stream)
 
-    def _snapshot(self, s):
+    # ---- one step as a sequence of local phases ("p") and exchange points ("x")
+    def sequence(self):
+        seq = ["p_snapshot", "x_SV", "p_force_move"]                       # S0, compute_force, move
+        if self.merges:
+            seq += ["p_snapshot", "x_SV", "p_merge_search", "x_target", "p_claim_absorb_delete"]
+        return seq
+
+    def p_snapshot(self, s):
         h, a = self.heap, self.args
         h.launch(dsr.K_NB_CLEAR_SNAPSHOT, self.n_total, a, s)
         h.parallel_do(0, dsr.M_NB_SNAPSHOT, a, s)
-        self.xch.all_gather_rows(self.S, self.lo, self.hi)
-        self.xch.all_gather_rows(self.V, self.lo, self.hi)
 
-    def step(self, stream=None):
-        s = stream if stream is not None else self.stream
+    def p_force_move(self, s):
+        self.heap.parallel_do(0, dsr.M_NB_FORCE, self.args, s)
+        self.heap.parallel_do(0, dsr.M_NB_MOVE, self.args, s)
+
+    def p_merge_search(self, s):
+        self.heap.parallel_do(0, dsr.M_NB_PREPARE_MERGE, self.args, s)
+
+    def p_claim_absorb_delete(self, s):
         h, a = self.heap, self.args
-        self._snapshot(s)                                  # S0
-        h.parallel_do(0, dsr.M_NB_FORCE, a, s)
-        h.parallel_do(0, dsr.M_NB_MOVE, a, s)
-        if not self.merges:
-            return
-        self._snapshot(s)                                  # S1
-        h.parallel_do(0, dsr.M_NB_PREPARE_MERGE, a, s)
-        if self.xch.world > 1:
-            self.xch.all_gather_rows(self.target, self.lo, self.hi)
-            h.launch(dsr.K_NB_CLAIM, self.n_total, a, s)
+        if self.world > 1:
+            h.launch(dsr.K_NB_CLAIM, self.n_total, a, s)       # over the gathered targets of all ids
         else:
             h.parallel_do(0, dsr.M_NB_CLAIM, a, s)
         h.parallel_do(0, dsr.M_NB_ABSORB, a, s)
         h.parallel_do(0, dsr.M_NB_DELETE_MERGED, a, s)
+
+    def x_SV(self):
+        self.xch.all_gather_rows(self.S, self.lo, self.hi)
+        self.xch.all_gather_rows(self.V, self.lo, self.hi)
+
+    def x_target(self):
+        self.xch.all_gather_rows(self.target, self.lo, self.hi)
+
+    def step(self, stream=None):
+        s = stream if stream is not None else self.stream
+        for name in self.sequence():
+            if name.startswith("p_"):
+                getattr(self, name)(s)
+            else:
+                getattr(self, name)()
 
     def run(self, steps, stream=None):
         for _ in range(steps):
@@ -120,3 +140,50 @@ class NBody:
         o = self.out.cpu().numpy()
         return {"x": o[:, 0].copy(), "y": o[:, 1].copy(), "vx": o[:, 2].copy(), "vy": o[:, 3].copy(),
                 "m": o[:, 4].copy(), "alive": (o[:, 5] > 0).astype(np.uint8)}
+
+
+class NBodyLoopback:
+    """P id-range shards of the N-body step on ONE GPU: P heaps, the same
+    kernels and phase order as the multi-GPU run, the all-gathers replaced by
+    device-to-device copies of each shard's rows into every other shard's
+    id-indexed arrays.  Used to test the sharded algorithm without P GPUs."""
+
+    def __init__(self, state, P, **kw):
+        self.shards = [NBody(state, shard=(r, P), **kw) for r in range(P)]
+
+    def _gather(self, attr):
+        src = self.shards
+        for dst in src:
+            for s in src:
+                if s is not dst:
+                    getattr(dst, attr)[s.lo:s.hi].copy_(getattr(s, attr)[s.lo:s.hi])
+
+    def step(self):
+        for name in self.shards[0].sequence():
+            if name.startswith("p_"):
+                for sh in self.shards:
+                    getattr(sh, name)(sh.stream)
+            elif name == "x_SV":
+                self._gather("S")
+                self._gather("V")
+            else:
+                self._gather("target")
+
+    def run(self, steps):
+        for _ in range(steps):
+            self.step()
+
+    def state(self):
+        """Merge the shards' dumps (each shard dumps only its own ids)."""
+        import numpy as np
+        out = None
+        for sh in self.shards:
+            st = sh.state()
+            if out is None:
+                out = {k: v.copy() for k, v in st.items()}
+            else:
+                sel = np.zeros(len(out["x"]), bool)
+                sel[sh.lo:sh.hi] = True
+                for k in out:
+                    out[k][sel] = st[k][sel]
+        return out

@@ -97,3 +97,26 @@ def test_nbody_65536_one_step(P, O):
     al = want["alive"] == 1
     assert rel_pos_err(got["x"][al], want["x"][al]) <= 1e-4
     assert rel_pos_err(got["y"][al], want["y"][al]) <= 1e-4
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_nbody_sharded_loopback_equals_one_gpu(P, O):
+    """The id-range-sharded N-body (P heaps, chunk exchanges) reproduces the
+    single-heap run bit for bit: the all-pairs partials use fixed global
+    j-chunks, so nothing depends on P."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1810_11765_b200 import inputs as I, nbody
+    st = I.nbody_init(8192, seed=11)
+    prm = dict(G=2e-9, dt=0.5, eps=0.01, R=0.02)
+    one = nbody.NBody(st, merges=True, **prm)
+    one.run(6)
+    a = one.state()
+    lb = nbody.NBodyLoopback(st, P, merges=True, **prm)
+    lb.run(6)
+    b = lb.state()
+    assert (a["alive"] == 0).sum() > 10
+    for k in ("x", "y", "vx", "vy", "m", "alive"):
+        assert np.array_equal(a[k], b[k]), k
+    for sh in lb.shards:
+        assert sh.heap.check_invariants() == 0
