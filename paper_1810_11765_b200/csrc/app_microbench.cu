@@ -25,31 +25,24 @@ __global__ void __launch_bounds__(256) k_mb_new(DevHeap h, uint64_t n, dsr_mb_ne
   }
 }
 
-// ---- phase 2 / 5: field reduction (a pure pass: fused do-all, no R list).
-// Each warp takes leaf containers of allocated[T] (nested-level skip)
-// and its lanes walk the container's blocks in 4-slot quads: each field column
-// is read with one 128-bit non-coherent load per quad (16 lanes cover a
-// 64-slot u32 column, so a warp reads two full column segments per field).
+// ---- phase 2 / 5: field reduction.  Vectorised do-all body: one thread per
+// 4 consecutive slots ("quad") of a block; each field column is read with one
+// 128-bit non-coherent load per quad (16 lanes cover a 64-slot u32 column).
 template <int NF>
 __global__ void __launch_bounds__(256) k_mb_reduce(DevHeap h, uint32_t T, unsigned long long* out3) {
-  const DevBitmap& ab = h.allocbm[T];
+  const uint32_t r = ld_relaxed_u32((const uint32_t*)&h.ctrl[CTRL_RCOUNT]);
   const uint32_t Q = h.types[T].cap >> 2;         // caps 64/48/32 are multiples of 4
-  const uint64_t nwords = ((uint64_t)h.M + 63) / 64;
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t total = (uint64_t)r * Q;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint32_t cols[NF];
 #pragma unroll
   for (int f = 0; f < NF; ++f) cols[f] = h.types[T].col_off[f];
   uint64_t cnt = 0, sum = 0;
   uint32_t x = 0;
-  for (uint64_t wi = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < nwords; wi += nwarps) {
-    if (ab.nlevels > 1 && !((__ldg((const unsigned long long*)ab.lvl[1] + (wi >> 6)) >> (wi & 63)) & 1ull)) continue;
-    const uint64_t w = __ldg((const unsigned long long*)ab.lvl[0] + wi);
-    if (!w) continue;
-    const uint32_t total = (uint32_t)__popcll(w) * Q;
-    for (uint32_t j = lane; j < total; j += 32) {
-    const uint32_t k = j / Q, q = j - k * Q;
-    const uint32_t b = (uint32_t)(wi * 64 + nth_bit(w, k));
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const uint32_t bi = (uint32_t)(e / Q);
+    const uint32_t q = (uint32_t)(e - (uint64_t)bi * Q);
+    const uint32_t b = __ldg(h.R + bi);
     const uint32_t m4 = (uint32_t)(__ldg((const unsigned long long*)h.alloc_bm + b) >> (4 * q)) & 0xFu;
     if (!m4) continue;
     const uint8_t* base = h.data + (size_t)b * h.block_bytes + 16u * q;
@@ -63,7 +56,6 @@ __global__ void __launch_bounds__(256) k_mb_reduce(DevHeap h, uint32_t T, unsign
       const uint32_t a2 = (m4 & 4) ? v[f].z : 0u, a3 = (m4 & 8) ? v[f].w : 0u;
       sum += (uint64_t)a0 + a1 + (uint64_t)a2 + a3;
       x ^= a0 ^ a1 ^ a2 ^ a3;
-    }
     }
   }
   // warp then CTA reduction, one atomic per CTA and output

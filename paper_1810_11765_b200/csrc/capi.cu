@@ -277,10 +277,7 @@ extern "C" dsr_status dsr_doall_prologue(dsr_heap* h, uint32_t type, uint32_t me
   MethodInfo mi;
   if (!method_info(method_id, &mi)) return DSR_ERR_UNSUPPORTED;
   cudaStream_t st = (cudaStream_t)stream;
-  // pure passes (no new / destroy) walk allocated[T] inside the fused body:
-  // no block list and no snapshot are needed (k_doall_fused)
-  if (!mi.snapshot) return DSR_OK;
-  // R := compact(allocated[T]) + iteration-bitmap snapshot
+  // R := compact(allocated[T]) (+ iteration-bitmap snapshot when the method may allocate)
   CUDA_TRY(cudaMemsetAsync(&h->dev.ctrl[CTRL_RCOUNT], 0, 8, st));
   const uint64_t nwords = (h->L.M + 63) / 64;
   k_compact<<<(int)((nwords + kCompactThreads - 1) / kCompactThreads), kCompactThreads, 0, st>>>(h->dev, type,

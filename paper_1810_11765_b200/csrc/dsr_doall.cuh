@@ -94,34 +94,6 @@ __global__ void __launch_bounds__(256) k_doall(DevHeap h, uint32_t T, int snapsh
   Mth::flush(acc, a);
 }
 
-// Fused do-all for pure passes (methods that neither allocate nor destroy, so
-// no block can change during the pass and no snapshot / R list is needed):
-// each warp takes leaf containers of allocated[T] (grid-stride), skips empty
-// ones through the nested level, and lets its lanes walk the
-// container's blocks slot by slot (lanes = consecutive slots: coalesced
-// columns).  One launch instead of compaction + body; no R traffic.
-template <class Mth>
-__global__ void __launch_bounds__(256) k_doall_fused(DevHeap h, uint32_t T, typename Mth::Args a) {
-  const DevBitmap& ab = h.allocbm[T];
-  const uint32_t N = h.types[T].cap;
-  const uint64_t nwords = ((uint64_t)h.M + 63) / 64;
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  typename Mth::Acc acc;
-  for (uint64_t wi = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < nwords; wi += nwarps) {
-    if (ab.nlevels > 1 && !((ab.lvl[1][wi >> 6] >> (wi & 63)) & 1ull)) continue;
-    const uint64_t w = ab.lvl[0][wi];
-    if (!w) continue;
-    const uint32_t total = (uint32_t)__popcll(w) * N;
-    for (uint32_t j = lane; j < total; j += 32) {
-      const uint32_t k = j / N, s = j - k * N;
-      const uint32_t b = (uint32_t)(wi * 64 + nth_bit(w, k));
-      if ((h.alloc_bm[b] >> s) & 1ull) Mth::run(h, T, b, s, a, acc);
-    }
-  }
-  Mth::flush(acc, a);
-}
-
 // Method helpers: most methods keep no per-thread accumulator.
 struct NoAcc {};
 #define DSR_NO_ACC                                                        \

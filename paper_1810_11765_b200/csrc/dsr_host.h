@@ -64,8 +64,7 @@ inline int grid_for(const LaunchCtx& c, uint64_t n, K kernel, int threads = 256)
 template <class Mth>
 inline void launch_doall(const LaunchCtx& c, uint32_t T, int snapshot, const void* args) {
   typename Mth::Args a = *reinterpret_cast<const typename Mth::Args*>(args);
-  if (snapshot) k_doall<Mth><<<persistent_grid(c, k_doall<Mth>), 256, 0, c.st>>>(c.h, T, snapshot, a);
-  else k_doall_fused<Mth><<<persistent_grid(c, k_doall_fused<Mth>), 256, 0, c.st>>>(c.h, T, a);   // pure pass
+  k_doall<Mth><<<persistent_grid(c, k_doall<Mth>), 256, 0, c.st>>>(c.h, T, snapshot, a);
   count_launch();
 }
 
