@@ -408,17 +408,6 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
                  : bm_try_find_set(h.activebm[T], rot_hash(h, who, iter), &leaf);
       if (prof) { stat_add(h, ST_FIND, 1); stat_add(h, ST_CYC_FIND, clock64() - c1); }
       if (bid < 0) { if (prof) stat_add(h, ST_FINDFAIL, 1); ++fails; continue; }
-      // A block just filled by another warp stays in active[T] until its
-      // filler deactivates it; rather than failing the whole lookup, probe up
-      // to 3 other active blocks of the same leaf container (one load each).
-      if (!(h.flags & DSR_F_NO_ROTATE)) {
-        for (int p = 0; p < 3 && ld_relaxed(h.alloc_bm + bid) == ~0ull; ++p) {
-          leaf &= ~(1ull << (bid & 63));
-          const int64_t nb = leaf_next(leaf | (1ull << (bid & 63)), (uint64_t)bid);
-          if (nb < 0) break;
-          bid = nb;
-        }
-      }
     } else {                                                                  // slow path
       bid = -1;
       for (int k = 0; home && bid < 0 && k < 4; ++k) {                        // a free block in the home range
@@ -451,7 +440,13 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
     uint64_t before = 0;
     long long c2 = prof ? clock64() : 0;
     const uint32_t rot = (uint32_t)(rot_hash(h, who, iter + 0x1000) >> 58);
-    const uint64_t got = block_reserve(h, (uint32_t)bid, need, rot, &before, fresh ? &h.types[T].pad : nullptr);
+    // The first atomicOr is issued without reading the word first: a fresh
+    // block's word is known, any other block is assumed empty (OR-ing bits that
+    // are already 1 changes nothing, and the returned word gives the real state
+    // for the retry) -- one L2 round trip less per attempt.  Paper-exact mode
+    // (NoShift) keeps Alg. 6's read + ffs.
+    const bool blind = fresh || !(h.flags & DSR_F_NO_ROTATE);
+    const uint64_t got = block_reserve(h, (uint32_t)bid, need, rot, &before, blind ? &h.types[T].pad : nullptr);
     if (!got) { if (prof) stat_add(h, ST_RESZERO, 1); ++fails; continue; }    // full or invalidated
     const uint32_t t = ld_relaxed_u8(h.type + bid) - 1u;                      // volatile read (Alg. 1 l.10)
     const bool full = (before | got) == ~0ull;
