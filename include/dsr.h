@@ -163,6 +163,17 @@ dsr_status dsr_doall_prologue(dsr_heap* h, uint32_t type, uint32_t method_id, vo
 dsr_status dsr_doall_body(dsr_heap* h, uint32_t type, uint32_t method_id, const void* args, size_t args_bytes,
                           void* stream);
 
+/* Bulk slow path ahead of time: initialise up to `nblocks` empty blocks of
+ * `type` (free.clear -> initialize_block -> allocated.set -> active.set, the
+ * slow path of Alg. 1) in one parallel kernel, so that a following
+ * burst of device new finds active blocks on the fast path.  Fewer blocks are
+ * initialised if the free bitmap runs out (no error).  Stream-ordered. */
+dsr_status dsr_reserve_blocks(dsr_heap* h, uint32_t type, uint64_t nblocks, void* stream);
+/* Quiescent: return every allocated block of `type` that holds no object to
+ * the free bitmap (invalidate, active.clear, allocated.clear, free.set; Alg. 2
+ * l.7-11).  Used after dsr_reserve_blocks.  Stream-ordered. */
+dsr_status dsr_trim(dsr_heap* h, uint32_t type, void* stream);
+
 /* Launch a compiled user kernel `kernel_id` over n logical threads that may
  * call device new/destroy -- e.g. the microbenchmark's allocation
  * kernel or the Linux Scalability kernels.  args as above. */

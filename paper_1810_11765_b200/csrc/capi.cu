@@ -346,6 +346,59 @@ extern "C" dsr_status dsr_launch(dsr_heap* h, uint32_t kernel_id, uint64_t n, co
   return DSR_OK;
 }
 
+// ---------------------------------------------------------------- bulk slow path / trim
+__global__ void __launch_bounds__(256) k_reserve_blocks(DevHeap h, uint32_t T, uint64_t nblocks) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nblocks; i += stride) {
+    const int64_t bid = bm_clear_any(h, h.freebm, i * 0x9E3779B97F4A7C15ull + 1, 0);   // rotated per thread
+    if (bid < 0) return;                                                               // heap exhausted
+    init_block(h, T, (uint32_t)bid);
+    bm_set(h.allocbm[T], (uint64_t)bid);
+    bm_set(h.activebm[T], (uint64_t)bid);
+    stat_add(h, ST_INITS, 1);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_trim(DevHeap h, uint32_t T) {
+  const DevBitmap& ab = h.allocbm[T];
+  const uint64_t nwords = ((uint64_t)h.M + 63) / 64;
+  const uint64_t pad = h.types[T].pad;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nwords; i += (uint64_t)gridDim.x * blockDim.x) {
+    if (ab.nlevels > 1 && !((ab.lvl[1][i >> 6] >> (i & 63)) & 1ull)) continue;
+    uint64_t w = ab.lvl[0][i];
+    while (w) {
+      const uint32_t b = (uint32_t)(i * 64 + __ffsll((long long)w) - 1);
+      w &= w - 1;
+      if (h.alloc_bm[b] != pad) continue;                  // holds objects
+      if (block_invalidate(h, b)) {                        // quiescent: succeeds for an empty block
+        bm_clear(h.activebm[T], b);
+        bm_clear(h.allocbm[T], b);
+        bm_set(h.freebm, b);
+        stat_add(h, ST_BFREES, 1);
+      }
+    }
+  }
+}
+
+extern "C" dsr_status dsr_reserve_blocks(dsr_heap* h, uint32_t type, uint64_t nblocks, void* stream) {
+  if (!h || type >= h->L.ntypes) return DSR_ERR_INVALID;
+  if (nblocks == 0) return DSR_OK;
+  LaunchCtx c = ctx(h, stream);
+  k_reserve_blocks<<<grid_for(c, nblocks, k_reserve_blocks), 256, 0, c.st>>>(h->dev, type, nblocks);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DSR_OK;
+}
+
+extern "C" dsr_status dsr_trim(dsr_heap* h, uint32_t type, void* stream) {
+  if (!h || type >= h->L.ntypes) return DSR_ERR_INVALID;
+  LaunchCtx c = ctx(h, stream);
+  k_trim<<<h->sms * 4, 256, 0, c.st>>>(h->dev, type);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DSR_OK;
+}
+
 // ---------------------------------------------------------------- live count / stats
 __global__ void k_live(DevHeap h, uint32_t T, unsigned long long* out) {
   const DevBitmap& ab = h.allocbm[T];

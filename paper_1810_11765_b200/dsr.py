@@ -164,6 +164,10 @@ def lib():
         L.dsr_doall_prologue.argtypes = [vp, C.c_uint32, C.c_uint32, vp]
         L.dsr_doall_body.restype = st
         L.dsr_doall_body.argtypes = [vp, C.c_uint32, C.c_uint32, vp, C.c_size_t, vp]
+        L.dsr_reserve_blocks.restype = st
+        L.dsr_reserve_blocks.argtypes = [vp, C.c_uint32, C.c_uint64, vp]
+        L.dsr_trim.restype = st
+        L.dsr_trim.argtypes = [vp, C.c_uint32, vp]
         L.dsr_launch.restype = st
         L.dsr_launch.argtypes = [vp, C.c_uint32, C.c_uint64, vp, C.c_size_t, vp]
         L.dsr_live_count.restype = st
@@ -301,6 +305,12 @@ class Heap:
     def doall_body(self, type_, method_id, args=None, stream=None):
         p, nb = _args(args)
         check("dsr_doall_body", lib().dsr_doall_body(self.h, type_, method_id, p, nb, self._s(stream)))
+
+    def reserve_blocks(self, type_, nblocks, stream=None):
+        check("dsr_reserve_blocks", lib().dsr_reserve_blocks(self.h, type_, nblocks, self._s(stream)))
+
+    def trim(self, type_, stream=None):
+        check("dsr_trim", lib().dsr_trim(self.h, type_, self._s(stream)))
 
     def launch(self, kernel_id, n, args, stream=None):
         p, nb = _args(args)

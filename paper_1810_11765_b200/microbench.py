@@ -12,15 +12,25 @@ PHASES = ["init", "new1", "reduce2", "free3", "new4", "reduce5", "drain6"]
 
 class Microbench:
     def __init__(self, n1=1 << 26, n2=1 << 25, seed=1, heap_bytes=None, device=None, retries=5, flags=0,
-                 stream=None):
+                 stream=None, reserve=True):
         import torch
         self.n1, self.n2, self.seed = n1, n2, seed
+        self.reserve = reserve      # dsr_reserve_blocks before / dsr_trim after the phase-1 burst
         if heap_bytes is None:
             # room for every object of phase 1 + 4 at the worst per-block fill, x2 for contention slack
             heap_bytes = max(64 << 20, int((n1 + n2) * 24 * 2.0))
         self.heap = dsr.Heap(MB_TYPES, heap_bytes, device=device, retries=retries, flags=flags, stream=stream)
         self.out = torch.zeros(18, dtype=torch.int64, device=self.heap.device)   # u64 bit patterns
         self.stream = stream
+
+    @staticmethod
+    def _counts(t0, n):
+        """objects of A, B, C among threads t0 .. t0+n-1 ([A,A,B,C][t & 3])."""
+        c = [0, 0, 0]
+        for r in range(4):
+            k = len(range((r - t0) % 4, n, 4))
+            c[[0, 0, 1, 2][(t0 + (r - t0) % 4) & 3]] += k
+        return c
 
     def _reduce_args(self, k):
         return dsr.MbReduceArgs(self.out.data_ptr() + 8 * k)
@@ -51,7 +61,16 @@ class Microbench:
         with torch.cuda.stream(s if s is not None else torch.cuda.current_stream()):
             self.out.zero_()
         ev(0, 1)
-        ev(1, 0); h.launch(dsr.K_MB_NEW, self.n1, dsr.MbNewArgs(self.seed, 0), s); ev(1, 1)
+        ev(1, 0)
+        if self.reserve:
+            # bulk slow path ahead of the burst: the blocks phase 1 needs
+            for t, cnt in enumerate(self._counts(0, self.n1)):
+                h.reserve_blocks(t, -(-cnt // self.heap.cap[t]), s)
+        h.launch(dsr.K_MB_NEW, self.n1, dsr.MbNewArgs(self.seed, 0), s)
+        if self.reserve:
+            for t in range(3):
+                h.trim(t, s)
+        ev(1, 1)
         ev(2, 0)
         for t in range(3):
             reduce(t, 3 * t, t)

@@ -4,6 +4,6 @@ python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 timeout -s KILL 1500 python -m pytest tests -m "gpu and not slow" -q --timeout 600 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
 echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
 rm -f gpurun_out/prof_mb.log
-for a in "0 5" "0 5" "16 5" "4 5"; do echo "== $a" >> gpurun_out/prof_mb.log; timeout -s KILL 60 python scripts/prof_mb.py $a >> gpurun_out/prof_mb.log 2>&1; done
+for a in "0 5 1" "0 5 0" "0 5 1" "0 1 1" "4 5 1"; do echo "== $a" >> gpurun_out/prof_mb.log; timeout -s KILL 60 python scripts/prof_mb.py $a >> gpurun_out/prof_mb.log 2>&1; done
 timeout -s KILL 300 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1
 timeout -s KILL 600 python scripts/prof_apps.py gol16k wator > gpurun_out/prof_apps.log 2>&1

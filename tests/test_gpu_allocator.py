@@ -194,3 +194,37 @@ def test_linux_scalability_utilisation(D):
     torch.cuda.synchronize()
     assert heap.live_count(0) == 0
     assert heap.check_invariants() == 0
+
+
+def test_reserve_blocks_and_trim(D):
+    """dsr_reserve_blocks runs the slow path ahead of time (empty active
+    blocks); a following burst of new fills them; dsr_trim returns the blocks
+    that stayed empty, leaving every quiescent invariant intact."""
+    tf = [[4, 4, 4], [4, 4, 4, 4]]
+    heap = D.Heap(tf, 1 << 26)
+    heap.reserve_blocks(0, 1000)
+    heap.reserve_blocks(1, 10)
+    torch.cuda.synchronize()
+    _, blocks = heap.fragmentation()
+    assert blocks == [1000, 10]
+    assert heap.check_invariants() > 0            # empty allocated blocks exist until the trim
+    n = 40000
+    handles = torch.zeros(n, dtype=torch.int64, device="cuda")
+    heap.launch(D.K_LS_ALLOC, n, D.LsArgs(handles.data_ptr(), 1, 0))
+    heap.trim(0)
+    heap.trim(1)
+    torch.cuda.synchronize()
+    assert heap.live_count(0) == n and heap.live_count(1) == 0
+    f, blocks = heap.fragmentation()
+    assert blocks[1] == 0 and blocks[0] >= -(-n // heap.cap[0])
+    assert heap.check_invariants() == 0
+    assert heap.poll_error() == D.OK
+
+
+@pytest.mark.parametrize("reserve,flags", [(False, 0), (True, 0), (True, 32)])
+def test_microbench_variants_match_oracle(D, O, reserve, flags):
+    from paper_1810_11765_b200.microbench import Microbench
+    mb = Microbench(n1=200_000, n2=100_000, seed=5, reserve=reserve, flags=flags)
+    mb.step()
+    assert np.array_equal(mb.results(), O.microbench(5, 200_000, 100_000)[0])
+    assert mb.heap.check_invariants() == 0
