@@ -9,7 +9,8 @@ namespace dsr {
 __constant__ uint32_t kMbType[4] = {0, 0, 1, 2};   // [A, A, B, C][t & 3]
 
 // ---- phase 1 / 4: user kernel, thread t does new [A,A,B,C][t&3] (device new)
-__global__ void __launch_bounds__(256) k_mb_new(DevHeap h, uint64_t n, dsr_mb_new_args a) {
+// (8 CTAs x 256 threads per SM: <= 32 registers, full occupancy -- latency-bound)
+__global__ void __launch_bounds__(256, 8) k_mb_new(DevHeap h, uint64_t n, dsr_mb_new_args a) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   // uniform trip count: every thread of the CTA reaches dsr_new_uniform together
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride) {

@@ -78,7 +78,7 @@ static __global__ void __launch_bounds__(kCompactThreads) k_compact(DevHeap h, u
 
 // Persistent-grid element loop shared by all method kernels.
 template <class Mth>
-__global__ void __launch_bounds__(256) k_doall(DevHeap h, uint32_t T, int snapshot, typename Mth::Args a) {
+__global__ void __launch_bounds__(256, 8) k_doall(DevHeap h, uint32_t T, int snapshot, typename Mth::Args a) {
   const uint32_t r = ld_relaxed_u32((const uint32_t*)&h.ctrl[CTRL_RCOUNT]);
   const uint32_t N = h.types[T].cap;
   const uint64_t total = (uint64_t)r * N;
