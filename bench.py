@@ -386,11 +386,15 @@ def run_app(args):
         Wd = 64 if args.workload == "gol" else 16384
         a0 = I.gol_soup(Wd, Wd, 0.3 if Wd == 64 else 0.25, 1 if Wd == 64 else 42)
         sim = GameOfLife(a0, stream=stream)
+        step_fn = sim.generation
+        if Wd == 64:                       # launch-bound: replay one generation as a CUDA graph
+            sim.capture()
+            step_fn = sim.graph.replay
 
         def per(k):
             for t in range(2):
                 sim.heap.live_count_async(t, live[k, t], stream)
-        ms = time_steps(sim.generation, K, W, stream, per)
+        ms = time_steps(step_fn, K, W, stream, per)
         lv = live.cpu().numpy()
         visits = 2 * int(lv[:, 0].sum() + lv[:, 1].sum())
         cfg = {"workload": f"gol {Wd}^2 torus (BASELINE configs[{0 if Wd == 64 else 3}])"}

@@ -73,3 +73,28 @@ def test_gol_16384_sampled_against_dense(G, O):
         want = O.life_dense(np.ascontiguousarray(win), gens)[3:259, 3:259]   # torus wrap only hits the border
         assert np.array_equal(got[y + 3:y + 259, x + 3:x + 259], want)
     assert g.heap.check_invariants() == 0
+
+
+def test_gol_cuda_graph_replay(G, O):
+    """One generation captured as a CUDA graph (device-side R count, no host
+    sync inside a do-all) and replayed: same result as eager launches."""
+    from paper_1810_11765_b200 import inputs as I
+    a0 = I.gol_soup(64, 64, 0.3, 2)
+    g = G.GameOfLife(a0)
+    g.capture()                      # executes 1 generation (warm-up) + captures one
+    g.run_graph(99)
+    torch.cuda.synchronize()
+    assert g.gen == 100
+    assert np.array_equal(g.alive(), O.life_dense(a0, 100))
+    assert g.heap.check_invariants() == 0
+
+
+def test_gol_empty_grid_and_empty_passes(G, O):
+    """Degenerate inputs: an empty grid has no objects; every do-all visits
+    nothing and the heap stays empty."""
+    import numpy as np
+    g = G.GameOfLife(np.zeros((32, 48), np.uint8))
+    g.run(3)
+    assert g.alive().sum() == 0
+    assert g.heap.live_count(0) == 0 and g.heap.live_count(1) == 0
+    assert g.heap.check_invariants() == 0
