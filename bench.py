@@ -33,6 +33,10 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "object-updates/s per app + do-all HBM GB/s vs 8 TB/s peak; allocs/s"
 N1, N2, SEED = 1 << 26, 1 << 25, 1
+CONFIG = {"workload": "microbench (BASELINE configs[4]): per GPU 2^26 + 2^25 device new over "
+                      "A{3xu32}/B{4xu32}/C{6xu32}, 2 do-all reductions, do-all odd-free, do-all drain",
+          "n1": N1, "n2": N2, "seed": SEED,
+          "l2": "inputs larger than L2 (1.5 GiB live SOA data per step vs 126 MB L2); heap re-initialised every step"}
 
 
 def parse():
@@ -147,19 +151,21 @@ def reduce_over_ranks(vals, op, device="cuda"):
 
 
 # ---------------------------------------------------------------- CPU oracle leg
-def oracle_sample(steps=1, warmup=0):
-    """The oracle (oracle/, plain C, one thread) on the full microbench workload."""
+def oracle_sample(steps=1, warmup=0, n1=N1, n2=N2):
+    """The oracle (oracle/, plain C, one thread) on the microbench workload
+    (n1 / n2 = a bounded sample of it); returns object-updates per step and the
+    per-step wall times."""
     from oracle import oracle as O
     O.build()
     for _ in range(warmup):
-        O.microbench(SEED, N1, N2)
+        O.microbench(SEED, n1, n2)
     ts = []
     for _ in range(steps):
         t0 = time.perf_counter()
-        out, live = O.microbench(SEED, N1, N2)
+        out, live = O.microbench(SEED, n1, n2)
         ts.append(time.perf_counter() - t0)
     ph2, ph5 = int(out[0, :, 0].sum()), int(out[1, :, 0].sum())
-    updates = (N1 + N2) + (ph2 + N2 - ph5 + ph5) + 2 * ph2 + 2 * ph5
+    updates = (n1 + n2) + (ph2 + n2 - ph5 + ph5) + 2 * ph2 + 2 * ph5
     return updates, ts
 
 
@@ -167,17 +173,19 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return
-    updates, ts = oracle_sample(args.steps, args.warmup)
+    # each step: a quarter of the workload (2^24 + 2^23, same phases), so the
+    # default --steps/--warmup run stays within a few minutes on one core
+    updates, ts = oracle_sample(args.steps, args.warmup, N1 // 4, N2 // 4)
     t = sum(ts) / len(ts)
     v = updates / t
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "object-updates/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": "microbench (BASELINE configs[4]): 2^26 + 2^25 device new over A/B/C, 2 reductions, "
-                               "odd-free, drain", "n1": N1, "n2": N2, "seed": SEED},
+        "config": CONFIG,
         "cpu_baseline": {"value": v, "unit": "object-updates/s", "cores": 1, "kind": "oracle",
-                         "sample": "full workload, oracle/ plain C single-threaded object store"},
+                         "sample": f"each step: the microbench phases on n1 = 2^24, n2 = 2^23 (a quarter of the "
+                                   f"workload), oracle/ plain C single-threaded object store, {t:.2f} s/step"},
         "e2e": {"value": v, "unit": "object-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -306,11 +314,8 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "object-updates/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": "microbench (BASELINE configs[4]): per GPU 2^26 + 2^25 device new over "
-                                   "A{3xu32}/B{4xu32}/C{6xu32}, 2 do-all reductions, do-all odd-free, do-all drain",
-                       "n1": N1, "n2": N2, "seed": SEED, "heap_bytes": mb.heap.buf.numel(), "M": mb.heap.M,
-                       "caps": caps, "parallelism": f"{world} independent heaps (one per GPU)",
-                       "l2": "inputs larger than L2 (1.5 GiB live SOA data per step vs 126 MB L2); heap re-initialised every step"},
+            "config": dict(CONFIG, heap_bytes=mb.heap.buf.numel(), M=mb.heap.M, caps=caps,
+                           parallelism=f"{world} independent heaps (one per GPU)"),
             "allocs_per_s": (N1 + N2) * world / (sum(phase_ms[i] for i in (1, 4)) * 1e-3),
             "frees_per_s": counts["frees"] * world / (sum(phase_ms[i] for i in (3, 6)) * 1e-3),
             "scan_gbs": scan_gbs,
@@ -361,8 +366,11 @@ def run_app(args):
     the driver's bench line is the microbenchmark)."""
     import numpy as np
     import torch
+    import torch.distributed as dist
     from paper_1810_11765_b200 import dsr, inputs as I
-    torch.cuda.set_device(0)
+    rank, world, local = dist_init(args.gpus)
+    if world > 1 and args.workload != "nbody":
+        raise SystemExit(f"--workload {args.workload} runs on one GPU (replicas only); use nbody or microbench")
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     K, W = args.steps, args.warmup
@@ -401,19 +409,29 @@ def run_app(args):
     else:
         from paper_1810_11765_b200.nbody import NBody
         st = I.nbody_init(65536, seed=7)
-        sim = NBody(st, merges=True, stream=stream, **I.NBODY_PARAMS)
+        # N > 1: id-range shards, S/V/target all-gathered over NCCL
+        sim = NBody(st, merges=True, stream=stream, group=dist.group.WORLD if world > 1 else None,
+                    **I.NBODY_PARAMS)
 
         def per(k):
             sim.heap.live_count_async(0, live[k, 0], stream)
+        if world > 1:
+            dist.barrier()
         ms = time_steps(sim.step, K, W, stream, per)
         lv = live.cpu().numpy()
         visits = 8 * int(lv[:, 0].sum())
+        visits, = reduce_over_ranks([float(visits)], "sum")
+        ms, = reduce_over_ranks([ms], "max")
         cfg = {"workload": "nbody with merging (BASELINE configs[2]) 65536 bodies", "pairs_per_step": 2 * 65536 ** 2,
-               "pair_interactions_per_s": 2 * 65536 ** 2 / (ms * 1e-3)}
-    print(json.dumps({"metric": METRIC, "value": visits / K / (ms * 1e-3), "unit": "object-updates/s",
-                      "n_gpus": 1, "steps": K, "warmup": W, "ms_per_step": ms, "higher_is_better": True,
-                      "dtype": "u32" if args.workload != "nbody" else "f32", "data": "synthetic", "config": cfg,
-                      "gpu_launches_per_step": None}), flush=True)
+               "pair_interactions_per_s": 2 * 65536 ** 2 / (ms * 1e-3),
+               "parallelism": f"{world} id-range shards, NCCL all-gather of snapshot chunks" if world > 1 else "1 GPU"}
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": visits / K / (ms * 1e-3), "unit": "object-updates/s",
+                          "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms, "higher_is_better": True,
+                          "scaling": "strong", "dtype": "u32" if args.workload != "nbody" else "f32",
+                          "data": "synthetic", "config": cfg}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def main():
