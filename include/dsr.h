@@ -262,10 +262,22 @@ enum { DSR_M_COLLECT = 4 };    /* any type: append every visited handle */
 /* ---- Game of Life (BASELINE configs[0]/[3], reading R-GOL) ----
  * types: 0 = Alive{cell u32, is_new u8, action u8}, 1 = Candidate{cell u32, action u8}
  * cell: device array of W*H handles (0 = empty). */
-typedef struct { uint64_t* cell; uint32_t W, H; const uint8_t* alive0; uint32_t* dump; } dsr_gol_args;
+typedef struct {
+  uint64_t* cell; uint32_t W, H; const uint8_t* alive0; uint32_t* dump;
+  /* Row-sharded mode (ghost = 1): the grid arrays have H + 2 rows,
+   * rows 0 and H + 1 are ghost copies of the neighbour shards' boundary rows
+   * (no wrap in y; the torus closes through the exchange).  halo: 4 x W bytes
+   * (bit 0 next-alive, bit 1 new-alive): [0] my row 1 (to the shard above),
+   * [1] my row H (to the shard below), [2] received for ghost row 0, [3] for
+   * ghost row H + 1. */
+  uint32_t ghost; uint8_t* halo;
+} dsr_gol_args;
 enum {
-  DSR_K_GOL_INIT_ALIVE = 10,     /* n = W*H; Alive(c) for alive0[c] */
-  DSR_K_GOL_INIT_CAND = 11,      /* n = W*H; Candidate(c) for dead c with >= 1 alive neighbour */
+  DSR_K_GOL_INIT_ALIVE = 10,     /* n = W*H (W*(H+2) sharded); Alive(c) for alive0[c] (+ ghost cells) */
+  DSR_K_GOL_INIT_CAND = 11,      /* n as above; Candidate(c) for dead c with >= 1 alive neighbour */
+  DSR_K_GOL_HALO_PACK = 12,      /* n = W: after pass 3, masks of the boundary rows into halo[0], halo[1] */
+  DSR_K_GOL_HALO_APPLY = 13,     /* n = W: before pass 4, ghost rows from halo[2], halo[3]; Candidates on
+                                    empty boundary cells next to a remote new Alive (owner computes) */
   DSR_M_GOL_CAND_PREPARE = 10,   /* type 1 */
   DSR_M_GOL_ALIVE_PREPARE = 11,  /* type 0 */
   DSR_M_GOL_CAND_UPDATE = 12,    /* type 1 (allocates Alive) */

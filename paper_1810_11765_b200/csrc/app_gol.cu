@@ -16,20 +16,30 @@ enum { GOL_ALIVE = 0, GOL_CAND = 1 };
 enum { ACT_NONE = 0, ACT_SPAWN = 1, ACT_DIE = 2 };
 constexpr uint64_t kReserved = 1;   // not a handle: type bits 0
 
-__device__ __forceinline__ uint32_t gol_nbr(uint32_t W, uint32_t H, uint32_t c, int k) {
-  // Moore neighbourhood on the W x H torus, k = 0..7 (row-major order of offsets)
+__device__ __forceinline__ uint32_t gol_nbr(uint32_t W, uint32_t H, uint32_t c, int k, uint32_t ghost = 0) {
+  // Moore neighbourhood, k = 0..7 (row-major order of offsets); x wraps; y wraps
+  // on the W x H torus, or (sharded, ghost rows 0 and H + 1) never leaves rows 0..H+1
   const uint32_t x = c % W, y = c / W;
   const int dx = (k < 3) ? k - 1 : (k == 3 ? -1 : (k == 4 ? 1 : k - 6));
   const int dy = (k < 3) ? -1 : (k < 5 ? 0 : 1);
   const uint32_t nx = dx < 0 ? (x == 0 ? W - 1 : x - 1) : (dx > 0 ? (x + 1 == W ? 0 : x + 1) : x);
-  const uint32_t ny = dy < 0 ? (y == 0 ? H - 1 : y - 1) : (dy > 0 ? (y + 1 == H ? 0 : y + 1) : y);
+  const uint32_t ny = ghost ? (uint32_t)((int)y + dy)
+                            : (dy < 0 ? (y == 0 ? H - 1 : y - 1) : (dy > 0 ? (y + 1 == H ? 0 : y + 1) : y));
   return ny * W + nx;
 }
+__device__ __forceinline__ bool gol_local(const dsr_gol_args& a, uint32_t c) {
+  const uint32_t y = c / a.W;
+  return !a.ghost || (y >= 1 && y <= a.H);
+}
+// a ghost cell holding a neighbour shard's alive cell: a handle value whose
+// type bits say Alive, never dereferenced
+__device__ __forceinline__ uint64_t ghost_alive(const DevHeap& h) { return make_handle(GOL_ALIVE, h.types[GOL_ALIVE].cap, 0, 0); }
 
 __device__ __forceinline__ uint32_t gol_alive_nbrs(const dsr_gol_args& a, uint32_t c) {
   uint32_t k = 0;
 #pragma unroll
-  for (int d = 0; d < 8; ++d) k += h_is(__ldg((const unsigned long long*)a.cell + gol_nbr(a.W, a.H, c, d)), GOL_ALIVE);
+  for (int d = 0; d < 8; ++d)
+    k += h_is(__ldg((const unsigned long long*)a.cell + gol_nbr(a.W, a.H, c, d, a.ghost)), GOL_ALIVE);
   return k;
 }
 
@@ -58,12 +68,14 @@ __global__ void __launch_bounds__(256) k_gol_init(DevHeap h, uint64_t n, dsr_gol
     const uint64_t i = base + threadIdx.x;
     const uint32_t c = (uint32_t)i;
     bool want = false;
-    if (i < n) {
+    if (i < n && !gol_local(a, c)) {
+      if (!cand) a.cell[c] = a.alive0[c] ? ghost_alive(h) : 0ull;   // ghost rows: neighbours' alive cells
+    } else if (i < n) {
       const bool alive = a.alive0[c];
       if (!cand) {
         want = alive;
       } else if (!alive) {
-        for (int d = 0; d < 8; ++d) want |= a.alive0[gol_nbr(a.W, a.H, c, d)] != 0;
+        for (int d = 0; d < 8; ++d) want |= a.alive0[gol_nbr(a.W, a.H, c, d, a.ghost)] != 0;
       }
     }
     const uint32_t T = cand ? GOL_CAND : GOL_ALIVE;
@@ -120,7 +132,9 @@ struct GolAliveUpdate {   // pass 4 (allocates Candidate)
     uint32_t todo = 0;                                   // bit d: create a Candidate at neighbour d; bit 8: at c
     if (*field_ptr<uint8_t>(h, T, 1, b, s)) {            // new Alive: claim the empty neighbours
       for (int d = 0; d < 8; ++d) {
-        unsigned long long* pe = (unsigned long long*)a.cell + gol_nbr(a.W, a.H, c, d);
+        const uint32_t e = gol_nbr(a.W, a.H, c, d, a.ghost);
+        if (!gol_local(a, e)) continue;                  // a neighbour shard's cell: its owner creates it
+        unsigned long long* pe = (unsigned long long*)a.cell + e;
         if (ld_relaxed((const uint64_t*)pe) == 0 && atomicCAS(pe, 0ull, kReserved) == 0ull) todo |= 1u << d;
       }
     } else if (*field_ptr<uint8_t>(h, T, 2, b, s) == ACT_DIE) {
@@ -134,12 +148,57 @@ struct GolAliveUpdate {   // pass 4 (allocates Candidate)
       if (todo) {
         const int d = __ffs(todo) - 1;
         todo &= todo - 1;
-        const uint32_t e = d == 8 ? c : gol_nbr(a.W, a.H, c, d);
+        const uint32_t e = d == 8 ? c : gol_nbr(a.W, a.H, c, d, a.ghost);
         a.cell[e] = new_cand(h, e);
       }
     }
   }
 };
+
+// ---- row sharding: one exchange of boundary masks per generation
+__device__ __forceinline__ uint8_t gol_mask(const DevHeap& h, uint64_t hd) {
+  if (!h_is(hd, GOL_ALIVE)) return 0;
+  const uint8_t is_new = *field_ptr<uint8_t>(h, hd, 1), act = *field_ptr<uint8_t>(h, hd, 2);
+  const bool next_alive = is_new || act != ACT_DIE;          // survives pass 4
+  return (uint8_t)((next_alive ? 1u : 0u) | (is_new ? 2u : 0u));
+}
+// after pass 3: next-alive / new-alive bits of my first and last local row
+__global__ void k_gol_halo_pack(DevHeap h, uint64_t n, dsr_gol_args a) {
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (uint64_t)gridDim.x * blockDim.x) {
+    a.halo[x] = gol_mask(h, a.cell[(uint64_t)1 * a.W + x]);
+    a.halo[a.W + x] = gol_mask(h, a.cell[(uint64_t)a.H * a.W + x]);
+  }
+}
+// before pass 4: ghost rows := the neighbours' next-alive cells (read by the
+// next generation's prepare passes), and a Candidate on every empty boundary
+// cell next to a remote new Alive (the owner computes it; the CAS claim makes
+// it exactly once together with pass 4's local claims)
+__global__ void __launch_bounds__(256) k_gol_halo_apply(DevHeap h, uint64_t n, dsr_gol_args a) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < 2 * n; base += stride) {   // uniform trip count
+    const uint64_t i = base + threadIdx.x;
+    bool want = false;
+    uint32_t e = 0;
+    if (i < 2 * n) {
+      const uint32_t side = (uint32_t)(i / n), x = (uint32_t)(i % n);
+      const uint8_t* m = a.halo + (2 + side) * a.W;                    // received masks
+      const uint32_t grow = side ? a.H + 1 : 0, brow = side ? a.H : 1;   // ghost row, my boundary row
+      a.cell[(uint64_t)grow * a.W + x] = (m[x] & 1) ? ghost_alive(h) : 0ull;
+      const uint32_t xl = x == 0 ? a.W - 1 : x - 1, xr = x + 1 == a.W ? 0 : x + 1;
+      if ((m[xl] | m[x] | m[xr]) & 2) {
+        e = brow * a.W + x;
+        unsigned long long* pe = (unsigned long long*)a.cell + e;
+        want = ld_relaxed((const uint64_t*)pe) == 0 && atomicCAS(pe, 0ull, kReserved) == 0ull;
+      }
+    }
+    const uint64_t nh = dsr_new_bulk(h, GOL_CAND, want);
+    if (nh) {
+      *field_ptr<uint32_t>(h, nh, 0) = e;
+      *field_ptr<uint8_t>(h, nh, 1) = ACT_NONE;
+    }
+    if (want) a.cell[e] = nh;
+  }
+}
 struct GolDump {
   typedef dsr_gol_args Args;
   DSR_NO_ACC
@@ -175,10 +234,19 @@ bool gol_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot
 
 bool gol_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* args, size_t bytes, int* ok) {
   *ok = 1;
-  if (id != DSR_K_GOL_INIT_ALIVE && id != DSR_K_GOL_INIT_CAND) return false;
+  if (id != DSR_K_GOL_INIT_ALIVE && id != DSR_K_GOL_INIT_CAND && id != DSR_K_GOL_HALO_PACK &&
+      id != DSR_K_GOL_HALO_APPLY)
+    return false;
   if (bytes != sizeof(dsr_gol_args) || c.h.ntypes < 2) { *ok = 0; return true; }
   const dsr_gol_args a = *(const dsr_gol_args*)args;
-  if ((uint64_t)a.W * a.H != n) { *ok = 0; return true; }
+  if (id == DSR_K_GOL_HALO_PACK || id == DSR_K_GOL_HALO_APPLY) {
+    if (!a.ghost || !a.halo || n != a.W) { *ok = 0; return true; }
+    if (id == DSR_K_GOL_HALO_PACK) k_gol_halo_pack<<<grid_for(c, n, k_gol_halo_pack), 256, 0, c.st>>>(c.h, n, a);
+    else k_gol_halo_apply<<<grid_for(c, 2 * n, k_gol_halo_apply), 256, 0, c.st>>>(c.h, n, a);
+    count_launch();
+    return true;
+  }
+  if ((uint64_t)a.W * (a.H + (a.ghost ? 2 : 0)) != n) { *ok = 0; return true; }
   k_gol_init<<<grid_for(c, n, k_gol_init), 256, 0, c.st>>>(c.h, n, a, id == DSR_K_GOL_INIT_CAND);
   count_launch();
   return true;

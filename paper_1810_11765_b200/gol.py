@@ -9,34 +9,87 @@ GOL_TYPES = [[4, 1, 1], [4, 1]]      # Alive{cell, is_new, action}, Candidate{ce
 ALIVE, CAND = 0, 1
 
 
+def row_range(H: int, world: int, rank: int):
+    """Rows owned by `rank` (contiguous bands; H % world == 0)."""
+    if H % world:
+        raise ValueError("H must be divisible by the number of shards")
+    b = H // world
+    return rank * b, (rank + 1) * b
+
+
 class GameOfLife:
-    def __init__(self, alive0, heap_bytes=None, device=None, stream=None, retries=5, flags=0):
+    """One heap for the whole torus, or -- with shard=(rank, P) -- one row band
+    of it with two ghost rows: after pass 3 the boundary rows'
+    next-alive / new-alive masks go to the neighbouring shards (`exchange`),
+    which store them as ghost rows and create the Candidates on their own
+    boundary cells next to a remote new Alive.  With P shards the result is the
+    single-heap result bit for bit."""
+
+    def __init__(self, alive0, heap_bytes=None, device=None, stream=None, retries=5, flags=0, shard=None,
+                 exchange=None):
         import numpy as np
         import torch
-        H, W = alive0.shape
-        self.W, self.H, self.N = W, H, W * H
+        Hg, W = alive0.shape
+        self.Hg = Hg
+        self.shard = shard
+        if shard is not None:
+            r, P = shard
+            y0, y1 = row_range(Hg, P, r)
+            self.y0, self.y1 = y0, y1
+            H = y1 - y0
+            rows = [(y0 - 1) % Hg] + list(range(y0, y1)) + [y1 % Hg]
+            grid = np.ascontiguousarray(alive0[rows], dtype=np.uint8)
+            self.grid_rows = H + 2
+        else:
+            self.y0, self.y1, H = 0, Hg, Hg
+            grid = np.ascontiguousarray(alive0, dtype=np.uint8)
+            self.grid_rows = H
+        self.W, self.H, self.N = W, H, W * self.grid_rows
+        self.exchange = exchange
         if heap_bytes is None:
             # every cell could hold an object: 5-6 B per object in 53/64-slot blocks, x2 slack
-            heap_bytes = max(16 << 20, self.N * 2 * 384 // 53 + (8 << 20))
+            heap_bytes = max(16 << 20, W * H * 2 * 384 // 53 + (8 << 20))
         self.heap = dsr.Heap(GOL_TYPES, heap_bytes, device=device, retries=retries, flags=flags, stream=stream)
         dev = self.heap.device
         self.stream = stream
         self.cell = torch.zeros(self.N, dtype=torch.int64, device=dev)
-        self.alive0 = torch.from_numpy(np.ascontiguousarray(alive0, dtype=np.uint8).reshape(-1)).to(dev)
+        self.alive0 = torch.from_numpy(grid.reshape(-1)).to(dev)
         self.dumpbuf = torch.zeros(self.N, dtype=torch.int32, device=dev)
-        self.args = dsr.GolArgs(self.cell.data_ptr(), W, H, self.alive0.data_ptr(), self.dumpbuf.data_ptr())
+        self.halo = torch.zeros(4 * W, dtype=torch.uint8, device=dev)
+        self.args = dsr.GolArgs(self.cell.data_ptr(), W, H, self.alive0.data_ptr(), self.dumpbuf.data_ptr(),
+                                1 if shard is not None else 0, self.halo.data_ptr() if shard is not None else None)
         self.heap.launch(dsr.K_GOL_INIT_ALIVE, self.N, self.args, stream)
         self.heap.launch(dsr.K_GOL_INIT_CAND, self.N, self.args, stream)
         self.gen = 0
 
-    def generation(self, stream=None):
-        s = stream if stream is not None else self.stream
+    # the generation split at the exchange point (sharded mode)
+    def first_half(self, s):
         h, a = self.heap, self.args
         h.parallel_do(CAND, dsr.M_GOL_CAND_PREPARE, a, s)
         h.parallel_do(ALIVE, dsr.M_GOL_ALIVE_PREPARE, a, s)
         h.parallel_do(CAND, dsr.M_GOL_CAND_UPDATE, a, s)
+        if self.shard is not None:
+            h.launch(dsr.K_GOL_HALO_PACK, self.W, a, s)
+
+    def second_half(self, s):
+        h, a = self.heap, self.args
+        if self.shard is not None:
+            h.launch(dsr.K_GOL_HALO_APPLY, self.W, a, s)
         h.parallel_do(ALIVE, dsr.M_GOL_ALIVE_UPDATE, a, s)
         self.gen += 1
+
+    def generation(self, stream=None):
+        s = stream if stream is not None else self.stream
+        self.first_half(s)
+        if self.shard is not None:
+            (self.exchange or self.self_exchange)()
+        self.second_half(s)
+
+    def self_exchange(self):
+        """P = 1 sharded mode: my bottom row is my top ghost row and vice versa."""
+        W = self.W
+        self.halo[2 * W:3 * W].copy_(self.halo[W:2 * W])
+        self.halo[3 * W:4 * W].copy_(self.halo[0:W])
 
     def run(self, gens, stream=None):
         for _ in range(gens):
@@ -73,7 +126,8 @@ class GameOfLife:
         self.heap.parallel_do(ALIVE, dsr.M_GOL_DUMP, self.args, s)
         self.heap.parallel_do(CAND, dsr.M_GOL_DUMP, self.args, s)
         torch.cuda.synchronize()
-        return self.dumpbuf.cpu().numpy().reshape(self.H, self.W)
+        d = self.dumpbuf.cpu().numpy().reshape(self.grid_rows, self.W)
+        return d[1:-1] if self.shard is not None else d       # local rows only
 
     def alive(self, stream=None):
         return ((self.dump(stream) & 0xFF) == 1).astype("uint8")
@@ -86,3 +140,53 @@ class GameOfLife:
         c = np.nonzero(d)[0]
         v = d[c]
         return np.stack([c, v & 0xFF, (v >> 8) & 0xFF, (v >> 16) & 0xFF], axis=1).astype(np.uint32)
+
+
+class NcclHaloExchange:
+    """Halo exchange between row-band shards over torch.distributed (NCCL on
+    GPUs): my first row's masks go to the shard above, my last row's to the
+    shard below (torus of ranks)."""
+
+    def __init__(self, sim, group=None):
+        import torch.distributed as dist
+        self.sim, self.group = sim, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+
+    def __call__(self):
+        import torch.distributed as dist
+        W, h = self.sim.W, self.sim.halo
+        up, down = (self.rank - 1) % self.world, (self.rank + 1) % self.world
+        ops = [dist.P2POp(dist.isend, h[0:W], up, self.group),
+               dist.P2POp(dist.isend, h[W:2 * W], down, self.group),
+               dist.P2POp(dist.irecv, h[2 * W:3 * W], up, self.group),
+               dist.P2POp(dist.irecv, h[3 * W:4 * W], down, self.group)]
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+
+
+class GameOfLifeLoopback:
+    """P row-band shards on ONE GPU (P heaps): the same kernels and exchange
+    points as the multi-GPU run, the messages replaced by device copies."""
+
+    def __init__(self, alive0, P, **kw):
+        self.P = P
+        self.shards = [GameOfLife(alive0, shard=(r, P), **kw) for r in range(P)]
+
+    def generation(self):
+        for s in self.shards:
+            s.first_half(s.stream)
+        W = self.shards[0].W
+        for r, s in enumerate(self.shards):
+            up, down = self.shards[(r - 1) % self.P], self.shards[(r + 1) % self.P]
+            s.halo[2 * W:3 * W].copy_(up.halo[W:2 * W])       # the upper shard's last row
+            s.halo[3 * W:4 * W].copy_(down.halo[0:W])         # the lower shard's first row
+        for s in self.shards:
+            s.second_half(s.stream)
+
+    def run(self, gens):
+        for _ in range(gens):
+            self.generation()
+
+    def alive(self):
+        import numpy as np
+        return np.concatenate([s.alive() for s in self.shards], axis=0)

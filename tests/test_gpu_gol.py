@@ -98,3 +98,26 @@ def test_gol_empty_grid_and_empty_passes(G, O):
     assert g.alive().sum() == 0
     assert g.heap.live_count(0) == 0 and g.heap.live_count(1) == 0
     assert g.heap.check_invariants() == 0
+
+
+@pytest.mark.parametrize("P,W,H,gens", [(1, 64, 64, 60), (2, 64, 64, 60), (4, 48, 40, 80), (8, 128, 64, 30)])
+def test_gol_row_shards_loopback_equal_dense(G, O, P, W, H, gens):
+    """Row-band sharding with ghost rows and one mask exchange per generation
+    (P heaps on one GPU, messages as device copies) gives dense Life exactly."""
+    from paper_1810_11765_b200 import inputs as I
+    from paper_1810_11765_b200.gol import GameOfLifeLoopback
+    a0 = I.gol_soup(W, H, 0.3, P + 20)
+    lb = GameOfLifeLoopback(a0, P)
+    lb.run(gens)
+    assert np.array_equal(lb.alive(), O.life_dense(a0, gens))
+    for s in lb.shards:
+        assert s.heap.check_invariants() == 0
+
+
+def test_gol_glider_crosses_shard_boundaries(G, O):
+    from paper_1810_11765_b200 import inputs as I
+    from paper_1810_11765_b200.gol import GameOfLifeLoopback
+    a0 = I.gol_pattern("glider")
+    lb = GameOfLifeLoopback(a0, 4)                 # bands of 16 rows: the glider crosses all of them
+    lb.run(4 * 64)
+    assert np.array_equal(lb.alive(), a0)
