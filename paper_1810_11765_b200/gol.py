@@ -155,9 +155,15 @@ class NcclHaloExchange:
     def __call__(self):
         import torch.distributed as dist
         W, h = self.sim.W, self.sim.halo
+        if self.world == 1:
+            return self.sim.self_exchange()
         up, down = (self.rank - 1) % self.world, (self.rank + 1) % self.world
-        ops = [dist.P2POp(dist.isend, h[0:W], up, self.group),
-               dist.P2POp(dist.isend, h[W:2 * W], down, self.group),
+        # messages between one pair are matched in posting order (no tags in
+        # NCCL): with two ranks up == down, so the order below pairs "my last
+        # row -> the lower shard's top ghost" before "my first row -> the upper
+        # shard's bottom ghost" on both sides
+        ops = [dist.P2POp(dist.isend, h[W:2 * W], down, self.group),
+               dist.P2POp(dist.isend, h[0:W], up, self.group),
                dist.P2POp(dist.irecv, h[2 * W:3 * W], up, self.group),
                dist.P2POp(dist.irecv, h[3 * W:4 * W], down, self.group)]
         for r in dist.batch_isend_irecv(ops):

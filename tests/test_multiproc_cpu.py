@@ -86,3 +86,31 @@ def test_id_range_rejects_uneven():
     from paper_1810_11765_b200.nbody import id_range
     with pytest.raises(ValueError):
         id_range(10, 3, 0)
+
+
+class _FakeGol:
+    def __init__(self, rank, W):
+        self.W = W
+        self.halo = torch.zeros(4 * W, dtype=torch.uint8)
+        self.halo[0:W] = 10 * rank + 1          # "my first row"
+        self.halo[W:2 * W] = 10 * rank + 2      # "my last row"
+
+
+def _gol_halo(rank, world):
+    from paper_1810_11765_b200.gol import NcclHaloExchange, row_range
+    sim = _FakeGol(rank, 8)
+    NcclHaloExchange(sim)()
+    return sim.halo.numpy().copy(), row_range(48, world, rank)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gol_halo_exchange_routes_rows(world):
+    """Top ghost row <- the upper shard's last row; bottom ghost row <- the
+    lower shard's first row (torus of ranks), also when up == down (2 ranks)."""
+    out = run_world(_gol_halo, world)
+    W = 8
+    for r, (h, band) in out.items():
+        up, down = (r - 1) % world, (r + 1) % world
+        assert (h[2 * W:3 * W] == 10 * up + 2).all()
+        assert (h[3 * W:4 * W] == 10 * down + 1).all()
+        assert band == (r * 48 // world, (r + 1) * 48 // world)
