@@ -25,7 +25,7 @@ F_NO_ROTATE, F_NO_COALESCE, F_STATS, F_SPIN_ON_OOM, F_NO_HINT, F_CTA_NEW, F_HOME
 K_MB_NEW, M_MB_REDUCE, M_MB_FREE_ODD, M_MB_FREE_ALL = 1, 1, 2, 3
 K_LS_ALLOC, K_LS_FREE = 2, 3
 K_REPLAY, K_TORTURE, M_COLLECT = 4, 5, 4
-K_GOL_INIT_ALIVE, K_GOL_INIT_CAND = 10, 11
+K_GOL_INIT_ALIVE, K_GOL_INIT_CAND, K_GOL_HALO_PACK, K_GOL_HALO_APPLY = 10, 11, 12, 13
 M_GOL_CAND_PREPARE, M_GOL_ALIVE_PREPARE, M_GOL_CAND_UPDATE, M_GOL_ALIVE_UPDATE, M_GOL_DUMP = 10, 11, 12, 13, 14
 C_WT_CELL, K_WT_INIT_AGENTS = 20, 21
 (M_WT_CELL_PREPARE, M_WT_FISH_PREPARE, M_WT_CELL_DECIDE_FISH, M_WT_FISH_UPDATE, M_WT_SHARK_PREPARE,
