@@ -369,8 +369,8 @@ def run_app(args):
     import torch.distributed as dist
     from paper_1810_11765_b200 import dsr, inputs as I
     rank, world, local = dist_init(args.gpus)
-    if world > 1 and args.workload != "nbody":
-        raise SystemExit(f"--workload {args.workload} runs on one GPU (replicas only); use nbody or microbench")
+    if world > 1 and args.workload not in ("nbody", "gol16k"):
+        raise SystemExit(f"--workload {args.workload} runs on one GPU (replicas only); use nbody, gol16k or microbench")
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     K, W = args.steps, args.warmup
@@ -390,10 +390,15 @@ def run_app(args):
         visits = 4 * 2048 * 2048 * K + 2 * int(starts[:, 0].sum() + starts[:, 1].sum())
         cfg = {"workload": "wator (BASELINE configs[1]) 2048^2, FB6 SB12 SS6, seed 42"}
     elif args.workload in ("gol", "gol16k"):
-        from paper_1810_11765_b200.gol import GameOfLife
+        from paper_1810_11765_b200.gol import GameOfLife, NcclHaloExchange
         Wd = 64 if args.workload == "gol" else 16384
         a0 = I.gol_soup(Wd, Wd, 0.3 if Wd == 64 else 0.25, 1 if Wd == 64 else 42)
-        sim = GameOfLife(a0, stream=stream)
+        if world > 1:                      # row bands + NCCL exchange of boundary masks
+            sim = GameOfLife(a0, stream=stream, shard=(rank, world))
+            sim.exchange = NcclHaloExchange(sim)
+            dist.barrier()
+        else:
+            sim = GameOfLife(a0, stream=stream)
         step_fn = sim.generation
         if Wd == 64:                       # launch-bound: replay one generation as a CUDA graph
             sim.capture()
@@ -405,7 +410,10 @@ def run_app(args):
         ms = time_steps(step_fn, K, W, stream, per)
         lv = live.cpu().numpy()
         visits = 2 * int(lv[:, 0].sum() + lv[:, 1].sum())
-        cfg = {"workload": f"gol {Wd}^2 torus (BASELINE configs[{0 if Wd == 64 else 3}])"}
+        visits, = reduce_over_ranks([float(visits)], "sum")
+        ms, = reduce_over_ranks([ms], "max")
+        cfg = {"workload": f"gol {Wd}^2 torus (BASELINE configs[{0 if Wd == 64 else 3}])",
+               "parallelism": f"{world} row bands, NCCL P2P halo masks" if world > 1 else "1 GPU"}
     else:
         from paper_1810_11765_b200.nbody import NBody
         st = I.nbody_init(65536, seed=7)
