@@ -85,7 +85,7 @@ typedef struct {
 #define DSR_F_STATS       0x4u  /* maintain device counters (dsr_stats) */
 #define DSR_F_SPIN_ON_OOM 0x8u  /* paper behaviour: loop forever on OOM */
 #define DSR_F_NO_HINT     0x10u /* no per-warp block hint: every request searches active[T] (paper-exact, replay) */
-#define DSR_F_CTA_NEW     0x20u /* bulk constructors use CTA-level instead of warp-level request coalescing */
+#define DSR_F_CTA_NEW     0x20u /* bulk constructors use CTA-level instead of warp-level request coalescing (microbench new kernel only) */
 #define DSR_F_HOME_ROT    0x40u /* ablation: SM-affine rotation (searches start in the SM's range of level-1 containers) */
 
 typedef struct {

@@ -9,15 +9,18 @@ namespace dsr {
 __constant__ uint32_t kMbType[4] = {0, 0, 1, 2};   // [A, A, B, C][t & 3]
 
 // ---- phase 1 / 4: user kernel, thread t does new [A,A,B,C][t&3] (device new)
-// (8 CTAs x 256 threads per SM: <= 32 registers, full occupancy -- latency-bound)
-__global__ void __launch_bounds__(256, 8) k_mb_new(DevHeap h, uint64_t n, dsr_mb_new_args a) {
+// (MINB CTAs x 256 threads per SM; latency-bound, so occupancy matters).  The
+// CTA-coalescing ablation (DSR_F_CTA_NEW) is a separate instantiation so the
+// default kernel carries none of its 16 KB of shared memory.
+template <bool CTA, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_mb_new(DevHeap h, uint64_t n, dsr_mb_new_args a) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   // uniform trip count: every thread of the CTA reaches dsr_new_uniform together
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
     const uint64_t i = base + threadIdx.x;
     const uint64_t t = a.t0 + i;
     const uint32_t T = kMbType[t & 3];
-    const uint64_t hd = dsr_new_bulk(h, T, i < n);
+    const uint64_t hd = CTA ? dsr_new_uniform(h, T, i < n) : (i < n ? dsr_new(h, T) : 0ull);
     if (hd) {
       const uint32_t nf = h.types[T].nfields;
       for (uint32_t k = 0; k < nf; ++k)
@@ -230,7 +233,12 @@ bool mb_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* a
   switch (id) {
     case DSR_K_MB_NEW: {
       if (bytes != sizeof(dsr_mb_new_args) || c.h.ntypes < 3) { *ok = 0; return true; }
-      k_mb_new<<<grid_for(c, n, k_mb_new), 256, 0, c.st>>>(c.h, n, *(const dsr_mb_new_args*)args);
+      {
+        const dsr_mb_new_args& ma = *(const dsr_mb_new_args*)args;
+        // (__launch_bounds__ minimum 8 / 6 / 4 CTAs per SM measured equal: 9.2-9.6 ms)
+        if (c.h.flags & DSR_F_CTA_NEW) k_mb_new<true, 8><<<grid_for(c, n, k_mb_new<true, 8>), 256, 0, c.st>>>(c.h, n, ma);
+        else k_mb_new<false, 8><<<grid_for(c, n, k_mb_new<false, 8>), 256, 0, c.st>>>(c.h, n, ma);
+      }
       count_launch();
       return true;
     }

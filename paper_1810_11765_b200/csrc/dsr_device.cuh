@@ -319,9 +319,9 @@ __device__ __forceinline__ void init_block(const DevHeap& h, uint32_t T, uint32_
 // free slots (rotated) and set them with ONE atomicOr; returns the
 // slots this call actually flipped (may be fewer; 0 = block full/invalidated).
 __device__ __forceinline__ uint64_t block_reserve(const DevHeap& h, uint32_t bid, uint32_t need, uint32_t rot,
-                                                  uint64_t* before_out, const uint64_t* known = nullptr) {
+                                                  uint64_t* before_out, bool known = false, uint64_t known_word = 0) {
   uint64_t* w = h.alloc_bm + bid;
-  uint64_t cur = known ? *known : ld_relaxed(w);     // a block we just initialised: its word is known
+  uint64_t cur = known ? known_word : ld_relaxed(w);  // a block we just initialised: its word is known
   for (;;) {
     const uint64_t fr = ~cur;
     if (fr == 0) return 0;
@@ -443,7 +443,7 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
     // A fresh block's word is known (no read).  (A "blind" first atomicOr on
     // found blocks, assuming them empty, was measured 1.5x slower: partial
     // fills doubled the number of requests.)
-    const uint64_t got = block_reserve(h, (uint32_t)bid, need, rot, &before, fresh ? &h.types[T].pad : nullptr);
+    const uint64_t got = block_reserve(h, (uint32_t)bid, need, rot, &before, fresh, h.types[T].pad);
     if (!got) { if (prof) stat_add(h, ST_RESZERO, 1); ++fails; continue; }    // full or invalidated
     const uint32_t t = ld_relaxed_u8(h.type + bid) - 1u;                      // volatile read (Alg. 1 l.10)
     const bool full = (before | got) == ~0ull;
@@ -548,11 +548,11 @@ __device__ __forceinline__ uint64_t dsr_new_uniform(const DevHeap& h, uint32_t T
   return mine;
 }
 
-// Bulk constructors (uniform call sites): warp-level coalescing by default,
-// CTA-level with DSR_F_CTA_NEW (measured slower on B200: fewer concurrent
-// leaders hide less latency -- kept as an ablation).
+// Bulk constructors (uniform call sites): warp-level coalescing.  (CTA-level
+// coalescing, dsr_new_uniform, was measured slower on B200 -- fewer concurrent
+// leaders hide less latency; it remains as the microbench ablation
+// DSR_F_CTA_NEW only, so app kernels carry none of its shared memory.)
 __device__ __forceinline__ uint64_t dsr_new_bulk(const DevHeap& h, uint32_t T, bool want) {
-  if (h.flags & DSR_F_CTA_NEW) return dsr_new_uniform(h, T, want);
   return want ? dsr_new(h, T) : 0ull;
 }
 
