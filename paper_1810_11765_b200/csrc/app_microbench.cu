@@ -15,6 +15,7 @@ __constant__ uint32_t kMbType[4] = {0, 0, 1, 2};   // [A, A, B, C][t & 3]
 template <bool CTA, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_mb_new(DevHeap h, uint64_t n, dsr_mb_new_args a) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t kp = rng_prefix(a.seed, 0);
   // uniform trip count: every thread of the CTA reaches dsr_new_uniform together
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
     const uint64_t i = base + threadIdx.x;
@@ -24,7 +25,7 @@ __global__ void __launch_bounds__(256, MINB) k_mb_new(DevHeap h, uint64_t n, dsr
     if (hd) {
       const uint32_t nf = h.types[T].nfields;
       for (uint32_t k = 0; k < nf; ++k)
-        *field_ptr<uint32_t>(h, T, k, h_bid(hd), h_slot(hd)) = (uint32_t)rng_key(a.seed, 0, 5, t * 16 + k);
+        *field_ptr<uint32_t>(h, T, k, h_bid(hd), h_slot(hd)) = (uint32_t)rng_key_p(kp, 5, t * 16 + k);
     }
   }
 }

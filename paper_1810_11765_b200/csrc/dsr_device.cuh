@@ -144,6 +144,11 @@ __device__ __forceinline__ uint64_t sm64(uint64_t x) {
 __device__ __forceinline__ uint64_t rng_key(uint64_t seed, uint64_t step, uint64_t phase, uint64_t idx) {
   return sm64(sm64(sm64(seed) ^ step) ^ ((phase << 40) | idx));
 }
+// the same key with the (seed, step) prefix sm64(sm64(seed) ^ step) hoisted out of a loop
+__device__ __forceinline__ uint64_t rng_prefix(uint64_t seed, uint64_t step) { return sm64(sm64(seed) ^ step); }
+__device__ __forceinline__ uint64_t rng_key_p(uint64_t prefix, uint64_t phase, uint64_t idx) {
+  return sm64(prefix ^ ((phase << 40) | idx));
+}
 
 // ------------------------------------------------------------------ handles (Fig. 5, Listing 2)
 __device__ __forceinline__ uint64_t make_handle(uint32_t T, uint32_t cap, uint32_t bid, uint32_t slot) {
@@ -181,6 +186,14 @@ __device__ __forceinline__ volatile uint32_t* hint_slot(const DevHeap& h, uint32
   return h.hints + (((smid << 6) | (wid & 63)) & h.hint_mask) * DSR_MAX_TYPES + T;
 }
 
+// first set bit of c at or after position r, cyclically (c != 0): the same
+// result as ffs(rotr(c, r)) + r mod 64 (the rotated search) without the
+// 64-bit rotate
+__device__ __forceinline__ uint32_t ffs_from(uint64_t c, uint32_t r) {
+  const uint64_t hi = c & (~0ull << r);
+  return (uint32_t)__ffsll((long long)(hi ? hi : c)) - 1u;
+}
+
 // ------------------------------------------------------------------ hierarchical bitmap
 // set(pos) at level l: "switches the bit from 0 to 1, retries until the bit
 // was changed"; cascades set-first upward (Def. P:1129).  Upper
@@ -189,14 +202,11 @@ __device__ __forceinline__ void bm_set_from(const DevBitmap& b, uint32_t l, uint
   for (; l < b.nlevels; ++l) {
     uint64_t* w = b.lvl[l] + (pos >> 6);
     const uint64_t m = 1ull << (pos & 63);
-    uint64_t prev;
+    uint64_t prev = atom_or(w, m);     // first try blind (legal use: the bit is 0)
     uint32_t ns = 32;
-    for (;;) {
-      if (!(ld_relaxed(w) & m)) {
-        prev = atom_or(w, m);
-        if (!(prev & m)) break;
-      }
-      backoff(ns);   // legal use: an in-flight clear of this bit is pending
+    while (prev & m) {
+      backoff(ns);   // an in-flight clear of this bit is pending: wait for it, then retry
+      if (!(ld_relaxed(w) & m)) prev = atom_or(w, m);
     }
     if (prev != 0) return;     // not set-first: upper level already 1
     pos >>= 6;
@@ -206,14 +216,11 @@ __device__ __forceinline__ void bm_clear_from(const DevBitmap& b, uint32_t l, ui
   for (; l < b.nlevels; ++l) {
     uint64_t* w = b.lvl[l] + (pos >> 6);
     const uint64_t m = 1ull << (pos & 63);
-    uint64_t prev;
+    uint64_t prev = atom_and(w, ~m);   // first try blind (legal use: the bit is 1)
     uint32_t ns = 32;
-    for (;;) {
-      if (ld_relaxed(w) & m) {
-        prev = atom_and(w, ~m);
-        if (prev & m) break;
-      }
-      backoff(ns);
+    while (!(prev & m)) {
+      backoff(ns);   // an in-flight set of this bit is pending
+      if (ld_relaxed(w) & m) prev = atom_and(w, ~m);
     }
     if (prev != m) return;     // Alg. 3 l.6: cascade only if popc(prev) = 1
     pos >>= 6;
@@ -251,7 +258,7 @@ __device__ __forceinline__ int64_t bm_try_find_set(const DevBitmap& b, uint64_t 
     const uint64_t c = ld_relaxed(b.lvl[l] + cid);
     if (c == 0) return -1;
     const uint32_t r = (uint32_t)(rh >> (6 * l)) & 63u;
-    const uint32_t i = ((uint32_t)__ffsll((long long)rotr64(c, r)) - 1u + r) & 63u;
+    const uint32_t i = ffs_from(c, r);
     cid = cid * 64 + i;
     if (l == 0 && leaf) *leaf = c;     // the leaf container the result came from
   }
@@ -296,7 +303,7 @@ __device__ __forceinline__ int64_t leaf_next(uint64_t c, uint64_t pos) {
   c &= ~(1ull << p);
   if (c == 0) return -1;
   const uint32_t r = (p + 1) & 63u;
-  const uint32_t i = ((uint32_t)__ffsll((long long)rotr64(c, r)) - 1u + r) & 63u;
+  const uint32_t i = ffs_from(c, r);
   return (int64_t)((pos & ~63ull) | i);
 }
 // clear(): find + try_clear until the clear succeeds (reading R-CLEARANY)

@@ -12,10 +12,11 @@ PHASES = ["init", "new1", "reduce2", "free3", "new4", "reduce5", "drain6"]
 
 class Microbench:
     def __init__(self, n1=1 << 26, n2=1 << 25, seed=1, heap_bytes=None, device=None, retries=5, flags=0,
-                 stream=None, reserve=True):
+                 stream=None, reserve=True, reserve_slack=0.0):
         import torch
         self.n1, self.n2, self.seed = n1, n2, seed
         self.reserve = reserve      # dsr_reserve_blocks before / dsr_trim after the phase-1 burst
+        self.reserve_slack = reserve_slack   # extra fraction of blocks reserved (trimmed afterwards)
         if heap_bytes is None:
             # room for every object of phase 1 + 4 at the worst per-block fill, x2 for contention slack
             heap_bytes = max(64 << 20, int((n1 + n2) * 24 * 2.0))
@@ -65,7 +66,7 @@ class Microbench:
         if self.reserve:
             # bulk slow path ahead of the burst: the blocks phase 1 needs
             for t, cnt in enumerate(self._counts(0, self.n1)):
-                h.reserve_blocks(t, -(-cnt // self.heap.cap[t]), s)
+                h.reserve_blocks(t, int(-(-cnt // self.heap.cap[t]) * (1.0 + self.reserve_slack)), s)
         h.launch(dsr.K_MB_NEW, self.n1, dsr.MbNewArgs(self.seed, 0), s)
         if self.reserve:
             for t in range(3):
