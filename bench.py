@@ -369,16 +369,22 @@ def run_app(args):
     import torch.distributed as dist
     from paper_1810_11765_b200 import dsr, inputs as I
     rank, world, local = dist_init(args.gpus)
-    if world > 1 and args.workload not in ("nbody", "gol16k"):
-        raise SystemExit(f"--workload {args.workload} runs on one GPU (replicas only); use nbody, gol16k or microbench")
+    if world > 1 and args.workload not in ("nbody", "gol16k", "wator"):
+        raise SystemExit(f"--workload {args.workload} runs on one GPU (replicas only); use nbody, gol16k, wator "
+                         "or microbench")
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     K, W = args.steps, args.warmup
     live = torch.zeros(K, 3, dtype=torch.int64, device="cuda")
     if args.workload == "wator":
-        from paper_1810_11765_b200.wator import WaTor
+        from paper_1810_11765_b200.wator import WaTor, NcclHaloExchange as WtExchange
         kind, egg, en = I.wator_init(2048, 2048, seed=42)
-        sim = WaTor(kind, egg, en, FB=6, SB=12, SS=6, seed=42, stream=stream)
+        if world > 1:                      # row bands + NCCL P2P boundary exchanges
+            sim = WaTor(kind, egg, en, FB=6, SB=12, SS=6, seed=42, stream=stream, shard=(rank, world))
+            sim.exchange = WtExchange(sim)
+            dist.barrier()
+        else:
+            sim = WaTor(kind, egg, en, FB=6, SB=12, SS=6, seed=42, stream=stream)
 
         def per(k):
             for t in range(2):
@@ -387,8 +393,12 @@ def run_app(args):
         lv = live.cpu().numpy()
         # visits of step k: 4 cell passes + 2 passes over the fish and sharks alive at its start
         starts = np.vstack([lv[:1] * 0 + lv[0], lv[:-1]])       # approx: counts at the previous step end
-        visits = 4 * 2048 * 2048 * K + 2 * int(starts[:, 0].sum() + starts[:, 1].sum())
-        cfg = {"workload": "wator (BASELINE configs[1]) 2048^2, FB6 SB12 SS6, seed 42"}
+        visits = 4 * sim.W * sim.H * K + 2 * int(starts[:, 0].sum() + starts[:, 1].sum())   # this shard's
+        visits, = reduce_over_ranks([float(visits)], "sum")
+        ms, = reduce_over_ranks([ms], "max")
+        cfg = {"workload": "wator (BASELINE configs[1]) 2048^2, FB6 SB12 SS6, seed 42",
+               "parallelism": f"{world} row bands, NCCL P2P halo (4 exchanges per half step)" if world > 1
+               else "1 GPU"}
     elif args.workload in ("gol", "gol16k"):
         from paper_1810_11765_b200.gol import GameOfLife, NcclHaloExchange
         Wd = 64 if args.workload == "gol" else 16384

@@ -298,10 +298,42 @@ typedef struct {
   const uint8_t* kind0; const uint32_t* egg0; const uint32_t* energy0;   /* init only */
   uint32_t* out_kind; uint32_t* out_egg; uint32_t* out_energy;           /* dump only */
   unsigned long long* counters;   /* [0] fish born, [1] sharks born, [2] eaten, [3] starved */
+  /* Row-sharded mode (ghost = 1): this shard owns global rows
+   * y0 .. y0+H-1 of a W x Hg torus; the cell arrays have H + 2 rows, rows 0 and
+   * H + 1 are ghost cells mirroring the neighbour shards' boundary rows (their
+   * agent field holds a type-only handle, never dereferenced).  Keys use global
+   * cell ids.  halo: DSR_WT_HALO_BYTES(W) bytes, each segment [side][W] with
+   * side 0 = my row 1 / ghost row 0 (the shard above), side 1 = my row H /
+   * ghost row H + 1 (the shard below); "out" segments go to the neighbour,
+   * "in" segments are the neighbour's "out" of the opposite side:
+   *   req  (u8)        requests into the neighbour's boundary cells
+   *   grant (u8)       decisions for the neighbour's boundary agents
+   *   occ  (u8)        agent kind (0 none, 1 fish, 2 shark) of my boundary rows
+   *   mig  (3 x u32)   migrating agents {kind, egg, energy} (kind 0 = none) */
+  uint32_t ghost, y0, Hg;
+  uint8_t* halo;
 } dsr_wator_args;
+#define DSR_WT_HALO_REQ_OUT(W)   0u
+#define DSR_WT_HALO_REQ_IN(W)    (2u * (W))
+#define DSR_WT_HALO_GRANT_OUT(W) (4u * (W))
+#define DSR_WT_HALO_GRANT_IN(W)  (6u * (W))
+#define DSR_WT_HALO_OCC_OUT(W)   (8u * (W))
+#define DSR_WT_HALO_OCC_IN(W)    (10u * (W))
+#define DSR_WT_HALO_MIG_OUT(W)   ((12u * (W) + 15u) & ~15u)
+#define DSR_WT_HALO_MIG_IN(W)    (DSR_WT_HALO_MIG_OUT(W) + 24u * (W))
+#define DSR_WT_HALO_BYTES(W)     (DSR_WT_HALO_MIG_IN(W) + 24u * (W))
 enum {
-  DSR_C_WT_CELL = 20,            /* parallel_new<Cell>(W*H): cells[i] = this */
-  DSR_K_WT_INIT_AGENTS = 21,     /* n = W*H: Fish/Shark from kind0/egg0/energy0 */
+  DSR_C_WT_CELL = 20,            /* parallel_new<Cell>(W*H) (W*(H+2) sharded): cells[i] = this */
+  DSR_K_WT_INIT_AGENTS = 21,     /* n = W*H (W*(H+2)): Fish/Shark from kind0/egg0/energy0 (+ ghost kinds) */
+  /* sharded mode, n = W each, in step order around the exchanges of each half step:
+   * prepare -> REQ_PACK | exchange req | REQ_APPLY -> decide | exchange grant | GRANT_APPLY
+   * -> update | exchange mig | MIG_APPLY -> OCC_PACK | exchange occ | OCC_APPLY */
+  DSR_K_WT_HALO_REQ_PACK = 22,   /* ghost cells' incoming requests -> req out; clears grant/mig out */
+  DSR_K_WT_HALO_REQ_APPLY = 23,  /* req in -> my boundary cells' req[0] (row 1) / req[2] (row H) */
+  DSR_K_WT_HALO_GRANT_APPLY = 24,/* grant in -> target of my boundary agents := the ghost cell */
+  DSR_K_WT_HALO_MIG_APPLY = 25,  /* mig in -> new agents on my boundary cells (a shark eats a fish there) */
+  DSR_K_WT_HALO_OCC_PACK = 26,   /* my boundary rows' agent kinds -> occ out */
+  DSR_K_WT_HALO_OCC_APPLY = 27,  /* occ in -> ghost cells' agent kinds */
   DSR_M_WT_CELL_PREPARE = 20, DSR_M_WT_FISH_PREPARE = 21, DSR_M_WT_CELL_DECIDE_FISH = 22,
   DSR_M_WT_FISH_UPDATE = 23, DSR_M_WT_SHARK_PREPARE = 24, DSR_M_WT_CELL_DECIDE_SHARK = 25,
   DSR_M_WT_SHARK_UPDATE = 26, DSR_M_WT_DUMP = 27

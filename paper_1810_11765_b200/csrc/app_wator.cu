@@ -14,15 +14,40 @@ namespace dsr {
 enum { WT_FISH = 0, WT_SHARK = 1, WT_CELL = 2 };
 enum { PH_FISH_REQ = 1, PH_FISH_DEC = 2, PH_SHARK_REQ = 3, PH_SHARK_DEC = 4 };
 
-__device__ __forceinline__ uint32_t wt_nbr(uint32_t W, uint32_t H, uint32_t c, uint32_t d) {
-  // von Neumann neighbour d in {N, E, S, W} on the torus
+__device__ __forceinline__ uint32_t wt_nbr(uint32_t W, uint32_t H, uint32_t c, uint32_t d, uint32_t ghost = 0) {
+  // von Neumann neighbour d in {N, E, S, W} on the torus; sharded (ghost rows
+  // 0 and H + 1): no wrap in y, a boundary row's N/S neighbour is a ghost cell
   const uint32_t x = c % W, y = c / W;
   switch (d) {
-    case 0: return (y == 0 ? H - 1 : y - 1) * W + x;
+    case 0: return (ghost ? y - 1 : (y == 0 ? H - 1 : y - 1)) * W + x;
     case 1: return y * W + (x + 1 == W ? 0 : x + 1);
-    case 2: return (y + 1 == H ? 0 : y + 1) * W + x;
+    case 2: return (ghost ? y + 1 : (y + 1 == H ? 0 : y + 1)) * W + x;
     default: return y * W + (x == 0 ? W - 1 : x - 1);
   }
+}
+__device__ __forceinline__ uint32_t wt_nbr(const dsr_wator_args& a, uint32_t c, uint32_t d) {
+  return wt_nbr(a.W, a.H, c, d, a.ghost);
+}
+__device__ __forceinline__ bool wt_local(const dsr_wator_args& a, uint32_t c) {
+  const uint32_t y = c / a.W;
+  return !a.ghost || (y >= 1 && y <= a.H);
+}
+// global cell id (the RNG key index): local row y of the shard is global row y0 + y - 1
+__device__ __forceinline__ uint32_t wt_gid(const dsr_wator_args& a, uint32_t c) {
+  if (!a.ghost) return c;
+  const uint32_t y = c / a.W, x = c % a.W;
+  return ((a.y0 + y + a.Hg - 1) % a.Hg) * a.W + x;
+}
+// a ghost cell's agent: a handle whose type bits say Fish / Shark, never dereferenced
+__device__ __forceinline__ uint64_t wt_ghost_agent(const DevHeap& h, uint32_t kind) {
+  return kind ? make_handle(kind - 1, h.types[kind - 1].cap, 0, 0) : 0ull;
+}
+struct WtMig { uint32_t kind, egg, energy; };
+__device__ __forceinline__ uint8_t* wt_halo(const dsr_wator_args& a, uint32_t off, uint32_t side) {
+  return a.halo + off + side * a.W;
+}
+__device__ __forceinline__ WtMig* wt_mig(const dsr_wator_args& a, uint32_t off, uint32_t side) {
+  return reinterpret_cast<WtMig*>(a.halo + off) + side * a.W;
 }
 __device__ __forceinline__ uint64_t* wt_agent(const DevHeap& h, const dsr_wator_args& a, uint32_t c) {
   return field_ptr<uint64_t>(h, a.cells[c], 1);
@@ -73,7 +98,11 @@ __global__ void __launch_bounds__(256) k_wt_init_agents(DevHeap h, uint64_t n, d
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride) {   // uniform trip count
     const uint64_t i = base + threadIdx.x;
     const uint32_t c = (uint32_t)i;
-    const uint8_t k = i < n ? a.kind0[c] : 0;
+    uint8_t k = i < n ? a.kind0[c] : 0;
+    if (k && !wt_local(a, c)) {                   // ghost row: the neighbour shard's agent kind
+      *wt_agent(h, a, c) = wt_ghost_agent(h, k);
+      k = 0;
+    }
     const uint32_t T = k == 2 ? WT_SHARK : WT_FISH;
     const uint64_t nh = dsr_new_bulk(h, T, k != 0);
     if (nh) {
@@ -107,8 +136,14 @@ struct WtCellDecide {
       if (*field_ptr<uint8_t>(h, T, 2 + d, b, s)) D[nd++] = d;
     if (!nd) return;
     const uint32_t id = *field_ptr<uint32_t>(h, T, 0, b, s);
-    const uint32_t d = wt_pick(D, nd, rng_key(a.seed, a.step, PHASE, id));
-    const uint64_t ag = *wt_agent(h, a, wt_nbr(a.W, a.H, id, d));
+    if (!wt_local(a, id)) return;                                   // ghost cell: its owner decides
+    const uint32_t d = wt_pick(D, nd, rng_key(a.seed, a.step, PHASE, wt_gid(a, id)));
+    const uint32_t nb = wt_nbr(a, id, d);
+    if (!wt_local(a, nb)) {                                         // a neighbour shard's agent: grant it
+      wt_halo(a, DSR_WT_HALO_GRANT_OUT(a.W), nb == id - a.W ? 0 : 1)[nb % a.W] = 1;
+      return;
+    }
+    const uint64_t ag = *wt_agent(h, a, nb);
     *field_ptr<uint32_t>(h, ag, 1) = id;                            // Fish/Shark.target (field 1 of both)
   }
 };
@@ -123,10 +158,10 @@ struct WtFishPrepare {
     uint32_t fr[4], nf = 0;
 #pragma unroll
     for (uint32_t d = 0; d < 4; ++d)
-      if (*wt_agent(h, a, wt_nbr(a.W, a.H, c, d)) == 0) fr[nf++] = d;
+      if (*wt_agent(h, a, wt_nbr(a, c, d)) == 0) fr[nf++] = d;
     if (nf) {
-      const uint32_t d = wt_pick(fr, nf, rng_key(a.seed, a.step, PH_FISH_REQ, c));
-      *wt_req(h, a, wt_nbr(a.W, a.H, c, d), d ^ 2) = 1;
+      const uint32_t d = wt_pick(fr, nf, rng_key(a.seed, a.step, PH_FISH_REQ, wt_gid(a, c)));
+      *wt_req(h, a, wt_nbr(a, c, d), d ^ 2) = 1;
     } else {
       *wt_req(h, a, c, 4) = 1;
     }
@@ -141,14 +176,19 @@ struct WtFishUpdate {   // allocates Fish (snapshot pass)
     const uint32_t c = *field_ptr<uint32_t>(h, T, 0, b, s);
     const uint32_t t = *field_ptr<uint32_t>(h, T, 1, b, s);
     if (t == c) return;
+    const bool away = !wt_local(a, t);                              // moves to a neighbour shard
     *wt_agent(h, a, c) = 0;
-    *wt_agent(h, a, t) = make_handle(T, h.types[T].cap, b, s);
+    if (!away) *wt_agent(h, a, t) = make_handle(T, h.types[T].cap, b, s);
     *field_ptr<uint32_t>(h, T, 0, b, s) = t;
     uint32_t* egg = field_ptr<uint32_t>(h, T, 2, b, s);
     if (*egg >= a.FB) {
       *egg = 0;
       *wt_agent(h, a, c) = new_fish(h, c, 0);
       acc.c[0] += 1;
+    }
+    if (away) {                                                     // migrate: the owner re-creates it
+      wt_mig(a, DSR_WT_HALO_MIG_OUT(a.W), t < a.W ? 0 : 1)[t % a.W] = WtMig{1u, *egg, 0u};
+      dsr_destroy(h, make_handle(T, h.types[T].cap, b, s));
     }
   }
 };
@@ -166,17 +206,17 @@ struct WtSharkPrepare {
     uint32_t fd[4], nfd = 0, fr[4], nfr = 0;
 #pragma unroll
     for (uint32_t d = 0; d < 4; ++d) {
-      const uint64_t ag = *wt_agent(h, a, wt_nbr(a.W, a.H, c, d));
+      const uint64_t ag = *wt_agent(h, a, wt_nbr(a, c, d));
       if (ag == 0) fr[nfr++] = d;
       else if (h_is(ag, WT_FISH)) fd[nfd++] = d;
     }
-    const uint64_t key = rng_key(a.seed, a.step, PH_SHARK_REQ, c);
+    const uint64_t key = rng_key(a.seed, a.step, PH_SHARK_REQ, wt_gid(a, c));
     if (nfd) {
       const uint32_t d = wt_pick(fd, nfd, key);
-      *wt_req(h, a, wt_nbr(a.W, a.H, c, d), d ^ 2) = 1;
+      *wt_req(h, a, wt_nbr(a, c, d), d ^ 2) = 1;
     } else if (nfr) {
       const uint32_t d = wt_pick(fr, nfr, key);
-      *wt_req(h, a, wt_nbr(a.W, a.H, c, d), d ^ 2) = 1;
+      *wt_req(h, a, wt_nbr(a, c, d), d ^ 2) = 1;
     } else {
       *wt_req(h, a, c, 4) = 1;
     }
@@ -199,15 +239,18 @@ struct WtSharkUpdate {  // allocates Shark (snapshot pass); destroys Fish and it
     }
     const uint32_t t = *field_ptr<uint32_t>(h, T, 1, b, s);
     if (t == c) return;
-    uint64_t* at = wt_agent(h, a, t);
-    const uint64_t prey = *at;
-    if (prey && h_is(prey, WT_FISH)) {
-      dsr_destroy(h, prey);                                         // another type
-      *en = a.SS;
-      acc.c[2] += 1;
+    const bool away = !wt_local(a, t);                              // moves to a neighbour shard (which
+    uint64_t* at = wt_agent(h, a, t);                               // resolves the prey on arrival)
+    if (!away) {
+      const uint64_t prey = *at;
+      if (prey && h_is(prey, WT_FISH)) {
+        dsr_destroy(h, prey);                                       // another type
+        *en = a.SS;
+        acc.c[2] += 1;
+      }
     }
     *wt_agent(h, a, c) = 0;
-    *at = self;
+    if (!away) *at = self;
     *field_ptr<uint32_t>(h, T, 0, b, s) = t;
     uint32_t* egg = field_ptr<uint32_t>(h, T, 2, b, s);
     if (*egg >= a.SB) {
@@ -215,8 +258,83 @@ struct WtSharkUpdate {  // allocates Shark (snapshot pass); destroys Fish and it
       *wt_agent(h, a, c) = new_shark(h, c, 0, a.SS);
       acc.c[1] += 1;
     }
+    if (away) {
+      wt_mig(a, DSR_WT_HALO_MIG_OUT(a.W), t < a.W ? 0 : 1)[t % a.W] = WtMig{2u, *egg, *en};
+      dsr_destroy(h, self);
+    }
   }
 };
+
+// ---- row sharding: the boundary stages of a half step
+__global__ void k_wt_req_pack(DevHeap h, uint64_t n, dsr_wator_args a) {
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < a.W; x += gridDim.x * blockDim.x) {
+    wt_halo(a, DSR_WT_HALO_REQ_OUT(a.W), 0)[x] = *wt_req(h, a, x, 2);                    // ghost row 0: from my row 1
+    wt_halo(a, DSR_WT_HALO_REQ_OUT(a.W), 1)[x] = *wt_req(h, a, (a.H + 1) * a.W + x, 0);  // ghost row H+1
+    for (uint32_t sd = 0; sd < 2; ++sd) {
+      wt_halo(a, DSR_WT_HALO_GRANT_OUT(a.W), sd)[x] = 0;
+      wt_mig(a, DSR_WT_HALO_MIG_OUT(a.W), sd)[x] = WtMig{0u, 0u, 0u};
+    }
+  }
+}
+__global__ void k_wt_req_apply(DevHeap h, uint64_t n, dsr_wator_args a) {
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < a.W; x += gridDim.x * blockDim.x) {
+    if (wt_halo(a, DSR_WT_HALO_REQ_IN(a.W), 0)[x]) *wt_req(h, a, a.W + x, 0) = 1;        // from the agent above
+    if (wt_halo(a, DSR_WT_HALO_REQ_IN(a.W), 1)[x]) *wt_req(h, a, a.H * a.W + x, 2) = 1;  // from the agent below
+  }
+}
+__global__ void k_wt_grant_apply(DevHeap h, uint64_t n, dsr_wator_args a) {
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < a.W; x += gridDim.x * blockDim.x) {
+    if (wt_halo(a, DSR_WT_HALO_GRANT_IN(a.W), 0)[x])
+      *field_ptr<uint32_t>(h, *wt_agent(h, a, a.W + x), 1) = x;                           // -> ghost row 0
+    if (wt_halo(a, DSR_WT_HALO_GRANT_IN(a.W), 1)[x])
+      *field_ptr<uint32_t>(h, *wt_agent(h, a, a.H * a.W + x), 1) = (a.H + 1) * a.W + x;  // -> ghost row H+1
+  }
+}
+__global__ void __launch_bounds__(256) k_wt_mig_apply(DevHeap h, uint64_t n, dsr_wator_args a) {
+  const uint32_t n2 = 2 * a.W, stride = gridDim.x * blockDim.x;
+  unsigned long long eaten = 0;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < n2; base += stride) {   // uniform trip count
+    const uint32_t i = base + threadIdx.x;
+    WtMig m{0u, 0u, 0u};
+    uint32_t c = 0;
+    if (i < n2) {
+      const uint32_t sd = i / a.W, x = i % a.W;
+      m = wt_mig(a, DSR_WT_HALO_MIG_IN(a.W), sd)[x];
+      c = (sd ? a.H : 1u) * a.W + x;                               // arrival cell on my boundary row
+    }
+    if (m.kind == 2) {
+      const uint64_t prey = *wt_agent(h, a, c);
+      if (prey && h_is(prey, WT_FISH)) {                            // the shark eats on arrival
+        dsr_destroy(h, prey);
+        m.energy = a.SS;
+        ++eaten;
+      }
+    }
+    const uint32_t T = m.kind == 2 ? WT_SHARK : WT_FISH;
+    const uint64_t nh = dsr_new_bulk(h, T, m.kind != 0);
+    if (nh) {
+      *field_ptr<uint32_t>(h, nh, 0) = c;
+      *field_ptr<uint32_t>(h, nh, 1) = c;
+      *field_ptr<uint32_t>(h, nh, 2) = m.egg;
+      if (T == WT_SHARK) *field_ptr<uint32_t>(h, nh, 3) = m.energy;
+    }
+    if (m.kind) *wt_agent(h, a, c) = nh;
+  }
+  if (eaten) atomicAdd(&a.counters[2], eaten);
+}
+__device__ __forceinline__ uint8_t wt_kind(uint64_t ag) { return ag == 0 ? 0 : (h_is(ag, WT_FISH) ? 1 : 2); }
+__global__ void k_wt_occ_pack(DevHeap h, uint64_t n, dsr_wator_args a) {
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < a.W; x += gridDim.x * blockDim.x) {
+    wt_halo(a, DSR_WT_HALO_OCC_OUT(a.W), 0)[x] = wt_kind(*wt_agent(h, a, a.W + x));
+    wt_halo(a, DSR_WT_HALO_OCC_OUT(a.W), 1)[x] = wt_kind(*wt_agent(h, a, a.H * a.W + x));
+  }
+}
+__global__ void k_wt_occ_apply(DevHeap h, uint64_t n, dsr_wator_args a) {
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < a.W; x += gridDim.x * blockDim.x) {
+    *wt_agent(h, a, x) = wt_ghost_agent(h, wt_halo(a, DSR_WT_HALO_OCC_IN(a.W), 0)[x]);
+    *wt_agent(h, a, (a.H + 1) * a.W + x) = wt_ghost_agent(h, wt_halo(a, DSR_WT_HALO_OCC_IN(a.W), 1)[x]);
+  }
+}
 
 struct WtDump {
   typedef dsr_wator_args Args;
@@ -256,11 +374,25 @@ bool wt_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot,
 
 bool wt_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* args, size_t bytes, int* ok) {
   *ok = 1;
-  if (id != DSR_K_WT_INIT_AGENTS) return false;
+  if (id < DSR_K_WT_INIT_AGENTS || id > DSR_K_WT_HALO_OCC_APPLY) return false;
   if (bytes != sizeof(dsr_wator_args) || c.h.ntypes < 3) { *ok = 0; return true; }
   const dsr_wator_args a = *(const dsr_wator_args*)args;
-  if ((uint64_t)a.W * a.H != n) { *ok = 0; return true; }
-  k_wt_init_agents<<<grid_for(c, n, k_wt_init_agents), 256, 0, c.st>>>(c.h, n, a);
+  if (id == DSR_K_WT_INIT_AGENTS) {
+    if ((uint64_t)a.W * (a.H + (a.ghost ? 2 : 0)) != n) { *ok = 0; return true; }
+    k_wt_init_agents<<<grid_for(c, n, k_wt_init_agents), 256, 0, c.st>>>(c.h, n, a);
+    count_launch();
+    return true;
+  }
+  if (!a.ghost || !a.halo || n != a.W || a.H == 0 || a.Hg == 0) { *ok = 0; return true; }
+  switch (id) {
+    case DSR_K_WT_HALO_REQ_PACK: k_wt_req_pack<<<grid_for(c, n, k_wt_req_pack), 256, 0, c.st>>>(c.h, n, a); break;
+    case DSR_K_WT_HALO_REQ_APPLY: k_wt_req_apply<<<grid_for(c, n, k_wt_req_apply), 256, 0, c.st>>>(c.h, n, a); break;
+    case DSR_K_WT_HALO_GRANT_APPLY:
+      k_wt_grant_apply<<<grid_for(c, n, k_wt_grant_apply), 256, 0, c.st>>>(c.h, n, a); break;
+    case DSR_K_WT_HALO_MIG_APPLY: k_wt_mig_apply<<<grid_for(c, 2 * n, k_wt_mig_apply), 256, 0, c.st>>>(c.h, n, a); break;
+    case DSR_K_WT_HALO_OCC_PACK: k_wt_occ_pack<<<grid_for(c, n, k_wt_occ_pack), 256, 0, c.st>>>(c.h, n, a); break;
+    default: k_wt_occ_apply<<<grid_for(c, n, k_wt_occ_apply), 256, 0, c.st>>>(c.h, n, a); break;
+  }
   count_launch();
   return true;
 }
@@ -270,7 +402,7 @@ bool wt_ctor_launch(uint32_t id, const LaunchCtx& c, uint32_t T, uint64_t n, con
   if (id != DSR_C_WT_CELL) return false;
   if (bytes != sizeof(dsr_wator_args) || T != WT_CELL || c.h.ntypes < 3) { *ok = 0; return true; }
   const dsr_wator_args a = *(const dsr_wator_args*)args;
-  if ((uint64_t)a.W * a.H != n) { *ok = 0; return true; }
+  if ((uint64_t)a.W * (a.H + (a.ghost ? 2 : 0)) != n) { *ok = 0; return true; }
   k_wt_new_cells<<<grid_for(c, n, k_wt_new_cells), 256, 0, c.st>>>(c.h, n, a);
   count_launch();
   return true;

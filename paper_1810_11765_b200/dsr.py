@@ -28,6 +28,15 @@ K_REPLAY, K_TORTURE, M_COLLECT = 4, 5, 4
 K_GOL_INIT_ALIVE, K_GOL_INIT_CAND, K_GOL_HALO_PACK, K_GOL_HALO_APPLY = 10, 11, 12, 13
 M_GOL_CAND_PREPARE, M_GOL_ALIVE_PREPARE, M_GOL_CAND_UPDATE, M_GOL_ALIVE_UPDATE, M_GOL_DUMP = 10, 11, 12, 13, 14
 C_WT_CELL, K_WT_INIT_AGENTS = 20, 21
+(K_WT_HALO_REQ_PACK, K_WT_HALO_REQ_APPLY, K_WT_HALO_GRANT_APPLY, K_WT_HALO_MIG_APPLY, K_WT_HALO_OCC_PACK,
+ K_WT_HALO_OCC_APPLY) = range(22, 28)
+
+
+def wt_halo_layout(W: int) -> dict:
+    """Byte offsets of the Wa-Tor halo segments (dsr.h DSR_WT_HALO_*): name -> (out, in, bytes per side)."""
+    mig_out = (12 * W + 15) & ~15
+    return {"req": (0, 2 * W, W), "grant": (4 * W, 6 * W, W), "occ": (8 * W, 10 * W, W),
+            "mig": (mig_out, mig_out + 24 * W, 12 * W), "bytes": mig_out + 48 * W}
 (M_WT_CELL_PREPARE, M_WT_FISH_PREPARE, M_WT_CELL_DECIDE_FISH, M_WT_FISH_UPDATE, M_WT_SHARK_PREPARE,
  M_WT_CELL_DECIDE_SHARK, M_WT_SHARK_UPDATE, M_WT_DUMP) = range(20, 28)
 C_NB_BODY, K_NB_CLEAR_SNAPSHOT, K_NB_CLAIM = 30, 30, 31
@@ -112,7 +121,8 @@ class WatorArgs(C.Structure):
                 ("SB", C.c_uint32), ("SS", C.c_uint32), ("seed", C.c_uint64), ("step", C.c_uint32),
                 ("kind0", C.c_void_p), ("egg0", C.c_void_p), ("energy0", C.c_void_p),
                 ("out_kind", C.c_void_p), ("out_egg", C.c_void_p), ("out_energy", C.c_void_p),
-                ("counters", C.c_void_p)]
+                ("counters", C.c_void_p), ("ghost", C.c_uint32), ("y0", C.c_uint32), ("Hg", C.c_uint32),
+                ("halo", C.c_void_p)]
 
 
 class NbodyArgs(C.Structure):

@@ -53,6 +53,31 @@ def test_wator_2048_prefix_against_oracle(P, O):
     assert sim.heap.check_invariants() == 0
 
 
+@pytest.mark.parametrize("Pn,W,H,seed,steps", [(1, 64, 64, 5, 40), (2, 64, 64, 5, 40), (4, 48, 32, 9, 40),
+                                                (8, 64, 64, 11, 30), (2, 200, 120, 3, 25)])
+def test_wator_row_shards_loopback_bit_exact(P, O, Pn, W, H, seed, steps):
+    """Row-band sharding (ghost rows, 4 boundary exchanges per half step,
+    agents migrating between heaps) equals the single-heap oracle every step,
+    including the event counters summed over shards.  Pn = 8 at H = 64 gives
+    8-row bands, so agents cross several bands over the run."""
+    from paper_1810_11765_b200 import inputs as I, wator
+    kind, egg, en = I.wator_init(W, H, seed=seed)
+    lb = wator.WaTorLoopback(kind, egg, en, Pn, **WT)
+    k, e, n = kind, egg, en
+    tot = np.zeros(4, dtype=np.int64)
+    for s in range(steps):
+        k, e, n, c = O.wator_run(k, e, n, steps=1, step0=s, **WT)
+        tot += np.array([int(c[0, 2]), int(c[0, 3]), int(c[0, 4]), int(c[0, 5])])
+        lb.step()
+        gk, ge, gn = lb.state()
+        assert np.array_equal(gk, k) and np.array_equal(ge, e) and np.array_equal(gn, n), f"step {s}"
+        assert lb.read_counters() == tot.tolist(), f"step {s}"
+        assert sum(sh.heap.live_count(0) for sh in lb.shards) == int(c[0, 0])
+    for sh in lb.shards:
+        assert sh.heap.poll_error() == 0
+        assert sh.heap.check_invariants() == 0
+
+
 def rel_pos_err(a, b):
     den = np.maximum(np.maximum(np.abs(a), np.abs(b)), 1e-3)
     return float(np.max(np.abs(a.astype(np.float64) - b.astype(np.float64)) / den))

@@ -114,3 +114,40 @@ def test_gol_halo_exchange_routes_rows(world):
         assert (h[2 * W:3 * W] == 10 * up + 2).all()
         assert (h[3 * W:4 * W] == 10 * down + 1).all()
         assert band == (r * 48 // world, (r + 1) * 48 // world)
+
+
+class _FakeWaTor:
+    def __init__(self, rank, W):
+        from paper_1810_11765_b200 import dsr
+        self.W = W
+        self.halo_layout = dsr.wt_halo_layout(W)
+        self.halo = torch.zeros(self.halo_layout["bytes"], dtype=torch.uint8)
+        for seg in ("req", "grant", "occ", "mig"):
+            o, i, n = self.halo_layout[seg]
+            self.halo[o:o + n] = 10 * rank + 1           # side 0: towards the shard above
+            self.halo[o + n:o + 2 * n] = 10 * rank + 2   # side 1: towards the shard below
+
+
+def _wt_halo(rank, world):
+    from paper_1810_11765_b200.wator import NcclHaloExchange
+    sim = _FakeWaTor(rank, 8)
+    x = NcclHaloExchange(sim)
+    for seg in ("req", "grant", "mig", "occ"):
+        x(seg)
+    return sim.halo.numpy().copy()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_wator_halo_exchange_routes_segments(world):
+    """in[0] <- the upper shard's side-1 out, in[1] <- the lower shard's side-0
+    out, for every segment (the migrant records are 12 B per column)."""
+    from paper_1810_11765_b200 import dsr
+    out = run_world(_wt_halo, world)
+    L = dsr.wt_halo_layout(8)
+    for r, h in out.items():
+        up, down = (r - 1) % world, (r + 1) % world
+        for seg in ("req", "grant", "occ", "mig"):
+            o, i, n = L[seg]
+            assert (h[i:i + n] == 10 * up + 2).all(), seg
+            assert (h[i + n:i + 2 * n] == 10 * down + 1).all(), seg
+            assert (h[o:o + n] == 10 * r + 1).all()              # out segments untouched
