@@ -58,10 +58,16 @@ typedef uint64_t dsr_handle;
 #define DSR_MAX_LEVELS 6
 
 /* One object type: its fields in declaration order (inherited fields first,
- * P:293).  field_bytes[f] in {1, 2, 4, 8, 16}. */
+ * P:293).  field_bytes[f] in {1, 2, 4, 8, 16}.  parent: 0 = no base type;
+ * k = the type derives from type k - 1, which must be declared earlier and
+ * whose fields must be this type's first fields (the inherited SOA columns
+ * precede the newly introduced ones).  A base field f is then column f
+ * of every subtype, addressed through any handle with the capacity of the
+ * handle's runtime type (handle bits 50-55). */
 typedef struct {
   uint32_t num_fields;
   uint32_t field_bytes[DSR_MAX_FIELDS];
+  uint32_t parent;
 } dsr_type_desc;
 
 /* Heap layout in the caller's device buffer.  All
@@ -148,7 +154,9 @@ dsr_status dsr_parallel_new(dsr_heap* h, uint32_t type, uint64_t n, uint32_t cto
 /* parallel_do<T, method>(args): snapshot the iteration bitmaps
  * (P:291), compact allocated[T] into the block list R with warp ballots and
  * prefix sums, then run `method_id` on every object of
- * T that exists at launch.  Objects created during the pass are not visited.
+ * T and of T's subtypes that exists at launch -- one body kernel per type, in
+ * type order (P:123 footnote); the block lists of all of them are built
+ * before the first body runs.  Objects created during the pass are not visited.
  * The method may allocate any type, destroy objects of other types, and
  * destroy only `this` among T.  No host synchronisation. */
 dsr_status dsr_parallel_do(dsr_heap* h, uint32_t type, uint32_t method_id, const void* args, size_t args_bytes,
@@ -258,6 +266,24 @@ typedef struct {
 enum { DSR_K_REPLAY = 4, DSR_K_TORTURE = 5 };
 typedef struct { uint64_t* out; uint64_t* count; } dsr_collect_args;   /* out[atomic++] = this */
 enum { DSR_M_COLLECT = 4 };    /* any type: append every visited handle */
+
+/* ---- inheritance test kernels ----
+ * Types of a hierarchy whose root has fields {u32 id, u32 acc} (every
+ * subtype inherits them as fields 0 and 1; further fields f >= 2 are the
+ * subtype's own, each set to (id * (f + 1)) truncated to its size). */
+typedef struct {
+  uint64_t* handles;             /* K_INH_NEW: handles[i] = the new object of thread i */
+  uint32_t ntypes;               /* K_INH_NEW: thread i creates type i % ntypes */
+  uint32_t spawn_id0;            /* M_INH_SPAWN: id offset of the spawned objects */
+  unsigned long long* out;       /* M_INH_SUM: out[2T] += 1, out[2T+1] += acc + own fields; M_INH_SPAWN: out[0] += 1 */
+  uint64_t* vals;                /* K_INH_READ: vals[i] = acc | is_a(handles[i], k) << (32 + k) */
+} dsr_inh_args;
+enum {
+  DSR_K_INH_NEW = 6, DSR_K_INH_READ = 7,
+  DSR_M_INH_BUMP = 5,            /* acc = 3 acc + id, through the inherited columns */
+  DSR_M_INH_SUM = 6,             /* per runtime type: count and checksum */
+  DSR_M_INH_SPAWN = 7            /* out[0] += 1; new object of the next type (i % ntypes + 1) */
+};
 
 /* ---- Game of Life (BASELINE configs[0]/[3], reading R-GOL) ----
  * types: 0 = Alive{cell u32, is_new u8, action u8}, 1 = Candidate{cell u32, action u8}

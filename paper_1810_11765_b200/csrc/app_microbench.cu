@@ -188,6 +188,83 @@ __global__ void __launch_bounds__(256) k_torture(DevHeap h, uint64_t nthreads, d
   if (errs && a.errors) atomicAdd((unsigned long long*)a.errors, (unsigned long long)errs);
 }
 
+// ---- inheritance: a hierarchy rooted at {u32 id, u32 acc}
+// a subtype's own field f (f >= 2) holds (id * (f + 1)) truncated to its size
+__device__ __forceinline__ uint64_t inh_own(uint32_t id, uint32_t f, uint32_t bytes) {
+  const uint64_t v = (uint64_t)id * (f + 1);
+  return bytes >= 8 ? v : (v & ((1ull << (8 * bytes)) - 1ull));
+}
+__device__ __forceinline__ void inh_store(const DevHeap& h, uint64_t hd, uint32_t f, uint64_t v) {
+  switch (h.types[h_type(hd)].fsize[f]) {
+    case 1: *field_ptr<uint8_t>(h, hd, f) = (uint8_t)v; break;
+    case 2: *field_ptr<uint16_t>(h, hd, f) = (uint16_t)v; break;
+    case 4: *field_ptr<uint32_t>(h, hd, f) = (uint32_t)v; break;
+    default: *field_ptr<uint64_t>(h, hd, f) = v; break;
+  }
+}
+__device__ __forceinline__ uint64_t inh_load(const DevHeap& h, uint32_t T, uint32_t f, uint32_t b, uint32_t s) {
+  switch (h.types[T].fsize[f]) {
+    case 1: return *field_ptr<uint8_t>(h, T, f, b, s);
+    case 2: return *field_ptr<uint16_t>(h, T, f, b, s);
+    case 4: return *field_ptr<uint32_t>(h, T, f, b, s);
+    default: return *field_ptr<uint64_t>(h, T, f, b, s);
+  }
+}
+__device__ __forceinline__ uint64_t inh_construct(const DevHeap& h, uint32_t T, uint32_t id, bool want) {
+  const uint64_t hd = dsr_new_bulk(h, T, want);
+  if (hd) {
+    *field_ptr<uint32_t>(h, hd, 0) = id;              // inherited columns 0, 1
+    *field_ptr<uint32_t>(h, hd, 1) = 0;
+    for (uint32_t f = 2; f < h.types[T].nfields; ++f) inh_store(h, hd, f, inh_own(id, f, h.types[T].fsize[f]));
+  }
+  return hd;
+}
+__global__ void __launch_bounds__(256) k_inh_new(DevHeap h, uint64_t n, dsr_inh_args a) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride) {   // uniform trip count
+    const uint64_t i = base + threadIdx.x;
+    const uint64_t hd = inh_construct(h, (uint32_t)(i % a.ntypes), (uint32_t)i, i < n);
+    if (i < n) a.handles[i] = hd;
+  }
+}
+// reads through "base-typed" handles: the column of an inherited field is
+// found from the handle's runtime type alone
+__global__ void k_inh_read(DevHeap h, uint64_t n, dsr_inh_args a) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t hd = a.handles[i];
+    uint64_t v = hd ? *field_ptr<uint32_t>(h, hd, 1) : 0;
+    for (uint32_t k = 0; k < h.ntypes; ++k) v |= (uint64_t)dsr_is_a(h, hd, k) << (32 + k);
+    a.vals[i] = v;
+  }
+}
+struct InhBump {   // acc = 3 acc + id, inherited fields only
+  typedef dsr_inh_args Args;
+  DSR_NO_ACC
+  static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args&, Acc&) {
+    uint32_t* acc = field_ptr<uint32_t>(h, T, 1, b, s);
+    *acc = 3u * *acc + *field_ptr<uint32_t>(h, T, 0, b, s);
+  }
+};
+struct InhSum {    // per runtime type: count, acc + own fields
+  typedef dsr_inh_args Args;
+  DSR_NO_ACC
+  static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args& a, Acc&) {
+    unsigned long long v = *field_ptr<uint32_t>(h, T, 1, b, s);
+    for (uint32_t f = 2; f < h.types[T].nfields; ++f) v += inh_load(h, T, f, b, s);
+    atomicAdd(a.out + 2 * T, 1ull);
+    atomicAdd(a.out + 2 * T + 1, v);
+  }
+};
+struct InhSpawn {  // visits the pre-pass objects only, although it creates objects of the whole subtree
+  typedef dsr_inh_args Args;
+  DSR_NO_ACC
+  static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args& a, Acc&) {
+    atomicAdd(a.out, 1ull);
+    const uint32_t id = *field_ptr<uint32_t>(h, T, 0, b, s);
+    inh_construct(h, (T + 1) % h.ntypes, a.spawn_id0 + id, true);
+  }
+};
+
 // ------------------------------------------------------------------ tables
 bool mb_method_info(uint32_t id, MethodInfo* mi) {
   switch (id) {
@@ -195,6 +272,8 @@ bool mb_method_info(uint32_t id, MethodInfo* mi) {
     case DSR_M_MB_FREE_ODD: *mi = {1, 0}; return true;      // self-delete
     case DSR_M_MB_FREE_ALL: *mi = {1, 0}; return true;
     case DSR_M_COLLECT: *mi = {0, sizeof(dsr_collect_args)}; return true;
+    case DSR_M_INH_BUMP: case DSR_M_INH_SUM: *mi = {0, sizeof(dsr_inh_args)}; return true;
+    case DSR_M_INH_SPAWN: *mi = {1, sizeof(dsr_inh_args)}; return true;
   }
   return false;
 }
@@ -203,6 +282,7 @@ bool mb_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot,
   static const uint64_t zero[2] = {0, 0};
   switch (id) {
     case DSR_M_MB_REDUCE: {
+      if (c.rk >= 0) return false;                       // single-type passes only
       const dsr_mb_reduce_args* a = (const dsr_mb_reduce_args*)args;
       const uint32_t nf = c.h.types[T].nfields;
       unsigned long long* o = (unsigned long long*)a->out3;
@@ -225,6 +305,13 @@ bool mb_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot,
     case DSR_M_MB_FREE_ODD: launch_doall<MbFreeOdd>(c, T, snapshot, zero); return true;
     case DSR_M_MB_FREE_ALL: launch_doall<MbFreeAll>(c, T, snapshot, zero); return true;
     case DSR_M_COLLECT: launch_doall<Collect>(c, T, snapshot, args); return true;
+    case DSR_M_INH_BUMP: case DSR_M_INH_SUM: case DSR_M_INH_SPAWN:
+      for (uint32_t t = 0; t < c.h.ntypes; ++t)       // every type derives from a root {u32 id, u32 acc}
+        if (c.h.types[t].nfields < 2 || c.h.types[t].fsize[0] != 4 || c.h.types[t].fsize[1] != 4) return false;
+      if (id == DSR_M_INH_BUMP) launch_doall<InhBump>(c, T, snapshot, args);
+      else if (id == DSR_M_INH_SUM) launch_doall<InhSum>(c, T, snapshot, args);
+      else launch_doall<InhSpawn>(c, T, snapshot, args);
+      return true;
   }
   return false;
 }
@@ -251,6 +338,22 @@ bool mb_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* a
       const int g = (int)((n + 255) / 256);
       if (id == DSR_K_LS_ALLOC) k_ls_alloc<<<g, 256, 0, c.st>>>(c.h, n, a);
       else k_ls_free<<<g, 256, 0, c.st>>>(c.h, n, a);
+      count_launch();
+      return true;
+    }
+    case DSR_K_INH_NEW:
+    case DSR_K_INH_READ: {
+      if (bytes != sizeof(dsr_inh_args)) { *ok = 0; return true; }
+      const dsr_inh_args a = *(const dsr_inh_args*)args;
+      for (uint32_t t = 0; t < c.h.ntypes; ++t)       // every type derives from a root {u32 id, u32 acc}
+        if (c.h.types[t].nfields < 2 || c.h.types[t].fsize[0] != 4 || c.h.types[t].fsize[1] != 4) { *ok = 0; return true; }
+      if (id == DSR_K_INH_NEW) {
+        if (a.ntypes < 1 || a.ntypes > c.h.ntypes || !a.handles) { *ok = 0; return true; }
+        k_inh_new<<<grid_for(c, n, k_inh_new), 256, 0, c.st>>>(c.h, n, a);
+      } else {
+        if (!a.handles || !a.vals) { *ok = 0; return true; }
+        k_inh_read<<<grid_for(c, n, k_inh_read), 256, 0, c.st>>>(c.h, n, a);
+      }
       count_launch();
       return true;
     }

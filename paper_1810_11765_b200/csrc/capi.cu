@@ -102,6 +102,13 @@ extern "C" dsr_status dsr_layout_compute(const dsr_type_desc* types, uint32_t nt
   for (uint32_t t = 0; t < ntypes; ++t) {
     const dsr_type_desc& d = types[t];
     if (d.num_fields < 1 || d.num_fields > DSR_MAX_FIELDS) return DSR_ERR_INVALID;
+    if (d.parent) {                                           // inherited fields first
+      if (d.parent > t) return DSR_ERR_INVALID;               // the base is declared earlier
+      const dsr_type_desc& b = types[d.parent - 1];
+      if (b.num_fields > d.num_fields) return DSR_ERR_INVALID;
+      for (uint32_t f = 0; f < b.num_fields; ++f)
+        if (b.field_bytes[f] != d.field_bytes[f]) return DSR_ERR_INVALID;
+    }
     sz[t] = 0;
     for (uint32_t f = 0; f < d.num_fields; ++f) {
       const uint32_t b = d.field_bytes[f];
@@ -223,6 +230,7 @@ extern "C" dsr_status dsr_heap_create(const dsr_type_desc* types, uint32_t ntype
     DevType& ty = d.types[t];
     ty.cap = L.cap[t];
     ty.nfields = types[t].num_fields;
+    ty.parent = types[t].parent;
     ty.valid = ty.cap == 64 ? ~0ull : ((1ull << ty.cap) - 1ull);
     ty.pad = ~ty.valid;
     for (uint32_t f = 0; f < ty.nfields; ++f) {
@@ -287,8 +295,8 @@ extern "C" dsr_status dsr_doall_prologue(dsr_heap* h, uint32_t type, uint32_t me
   return DSR_OK;
 }
 
-extern "C" dsr_status dsr_doall_body(dsr_heap* h, uint32_t type, uint32_t method_id, const void* args,
-                                     size_t args_bytes, void* stream) {
+static dsr_status doall_body(dsr_heap* h, uint32_t type, uint32_t method_id, const void* args, size_t args_bytes,
+                             void* stream, int rk) {
   if (!h || type >= h->L.ntypes) return DSR_ERR_INVALID;
   MethodInfo mi;
   if (!method_info(method_id, &mi)) return DSR_ERR_UNSUPPORTED;
@@ -296,6 +304,7 @@ extern "C" dsr_status dsr_doall_body(dsr_heap* h, uint32_t type, uint32_t method
   static const uint64_t zero_args[16] = {0};
   if (!mi.args_bytes) args = zero_args;
   LaunchCtx c = ctx(h, stream);
+  c.rk = rk;
   bool ok = mb_method_launch(method_id, c, type, mi.snapshot, args) ||
             gol_method_launch(method_id, c, type, mi.snapshot, args) ||
             wt_method_launch(method_id, c, type, mi.snapshot, args) ||
@@ -305,15 +314,58 @@ extern "C" dsr_status dsr_doall_body(dsr_heap* h, uint32_t type, uint32_t method
   return DSR_OK;
 }
 
+extern "C" dsr_status dsr_doall_body(dsr_heap* h, uint32_t type, uint32_t method_id, const void* args,
+                                     size_t args_bytes, void* stream) {
+  return doall_body(h, type, method_id, args, args_bytes, stream, -1);
+}
+
+// T and its subtypes, in type order (subtypes are declared after their base)
+static uint32_t subtree(const dsr_heap* h, uint32_t type, uint32_t* out) {
+  uint32_t n = 0;
+  for (uint32_t t = 0; t < h->L.ntypes; ++t) {
+    uint32_t u = t;
+    for (int k = 0; k <= DSR_MAX_TYPES; ++k) {
+      if (u == type) { out[n++] = t; break; }
+      if (!h->types[u].parent) break;
+      u = h->types[u].parent - 1;
+    }
+  }
+  return n;
+}
+
 extern "C" dsr_status dsr_parallel_do(dsr_heap* h, uint32_t type, uint32_t method_id, const void* args,
                                       size_t args_bytes, void* stream) {
   MethodInfo mi;
   if (!h || type >= h->L.ntypes) return DSR_ERR_INVALID;
   if (!method_info(method_id, &mi)) return DSR_ERR_UNSUPPORTED;
   if (mi.args_bytes && (args_bytes != mi.args_bytes || !args)) return DSR_ERR_INVALID;
-  dsr_status s = dsr_doall_prologue(h, type, method_id, stream);
-  if (s != DSR_OK) return s;
-  return dsr_doall_body(h, type, method_id, args, args_bytes, stream);
+  uint32_t sub[DSR_MAX_TYPES];
+  const uint32_t ns = subtree(h, type, sub);
+  if (ns == 1) {
+    dsr_status s = dsr_doall_prologue(h, type, method_id, stream);
+    if (s != DSR_OK) return s;
+    return dsr_doall_body(h, type, method_id, args, args_bytes, stream);
+  }
+  // Subtypes: one body per type, but every type's snapshot and block
+  // range of R are taken before the first body runs, so objects a body
+  // creates -- of any type of the subtree -- are not visited by this pass.
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemsetAsync(&h->dev.ctrl[CTRL_RCOUNT], 0, 8, st));
+  CUDA_TRY(cudaMemsetAsync(&h->dev.ctrl[CTRL_RBEG], 0, 8, st));
+  const uint64_t nwords = (h->L.M + 63) / 64;
+  for (uint32_t k = 0; k < ns; ++k) {
+    k_compact<<<(int)((nwords + kCompactThreads - 1) / kCompactThreads), kCompactThreads, 0, st>>>(h->dev, sub[k],
+                                                                                                    mi.snapshot);
+    count_launch();
+    CUDA_TRY(cudaMemcpyAsync(&h->dev.ctrl[CTRL_RBEG + k + 1], &h->dev.ctrl[CTRL_RCOUNT], 8, cudaMemcpyDeviceToDevice,
+                             st));
+  }
+  CUDA_TRY(cudaGetLastError());
+  for (uint32_t k = 0; k < ns; ++k) {
+    dsr_status s = doall_body(h, sub[k], method_id, args, args_bytes, stream, (int)k);
+    if (s != DSR_OK) return s;
+  }
+  return DSR_OK;
 }
 
 extern "C" dsr_status dsr_parallel_new(dsr_heap* h, uint32_t type, uint64_t n, uint32_t ctor_id, const void* args,

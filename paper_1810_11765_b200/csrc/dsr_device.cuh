@@ -32,6 +32,8 @@ struct DevBitmap {
 struct DevType {
   uint32_t cap;                    // N_T
   uint32_t nfields;
+  uint32_t parent;                 // 0 = none, k = derives from type k - 1
+  uint32_t pad_;
   uint64_t valid;                  // low N_T bits
   uint64_t pad;                    // ~valid: padding bits kept at 1
   uint32_t fsize[DSR_MAX_FIELDS];
@@ -39,7 +41,8 @@ struct DevType {
 };
 
 // control page word offsets (u64 units) -- DESIGN.md "HBM layout"
-enum { CTRL_ERR = 0, CTRL_RCOUNT = 1, CTRL_SCRATCH = 2, CTRL_STATS = 16, CTRL_AUDIT = 40 };
+// CTRL_RBEG + k: begin of the k-th type's range of R in a subtree do-all (k <= DSR_MAX_TYPES)
+enum { CTRL_ERR = 0, CTRL_RCOUNT = 1, CTRL_SCRATCH = 2, CTRL_RBEG = 4, CTRL_STATS = 16, CTRL_AUDIT = 40 };
 enum { ERRB_OOM = 1, ERRB_BUDGET = 2 };
 enum { ST_ALLOCS = 0, ST_FREES, ST_INITS, ST_BFREES, ST_ROLLBACKS, ST_INVFAIL, ST_RESRETRY, ST_OOM,
        ST_REQ, ST_FIND, ST_FINDFAIL, ST_RESZERO, ST_CYC_FIND, ST_CYC_SLOW, ST_CYC_RES, ST_CYC_REQ, ST_N };
@@ -167,6 +170,22 @@ __device__ __forceinline__ V* field_ptr(const DevHeap& h, uint32_t T, uint32_t f
 template <class V>
 __device__ __forceinline__ V* field_ptr(const DevHeap& h, uint64_t hd, uint32_t f) {
   return field_ptr<V>(h, h_type(hd), f, h_bid(hd), h_slot(hd));
+}
+
+// instance-of: the runtime type from the handle bits, then up the
+// parent chain (inheritance).  A base field is the same column index
+// in every subtype, so field_ptr(h, handle, f) reads it through any handle.
+__device__ __forceinline__ bool dsr_is_a(const DevHeap& h, uint64_t hd, uint32_t T) {
+  if (hd == 0) return false;
+  uint32_t t = h_type(hd);
+#pragma unroll 1
+  for (int k = 0; k < DSR_MAX_TYPES; ++k) {
+    if (t == T) return true;
+    const uint32_t p = h.types[t].parent;
+    if (!p) return false;
+    t = p - 1;
+  }
+  return false;
 }
 
 // ------------------------------------------------------------------ rotation (reading R-ROT / C3)

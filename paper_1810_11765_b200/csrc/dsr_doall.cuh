@@ -76,18 +76,27 @@ static __global__ void __launch_bounds__(kCompactThreads) k_compact(DevHeap h, u
   }
 }
 
-// Persistent-grid element loop shared by all method kernels.
+// Persistent-grid element loop shared by all method kernels.  rk < 0: the
+// whole of R; rk = k: the k-th type's range of a subtree do-all
+// (ctrl[CTRL_RBEG + k] .. ctrl[CTRL_RBEG + k + 1]).
 template <class Mth>
-__global__ void __launch_bounds__(256, 8) k_doall(DevHeap h, uint32_t T, int snapshot, typename Mth::Args a) {
-  const uint32_t r = ld_relaxed_u32((const uint32_t*)&h.ctrl[CTRL_RCOUNT]);
+__global__ void __launch_bounds__(256, 8) k_doall(DevHeap h, uint32_t T, int snapshot, int rk, typename Mth::Args a) {
+  uint32_t rb = 0, re;
+  if (rk < 0) {
+    re = ld_relaxed_u32((const uint32_t*)&h.ctrl[CTRL_RCOUNT]);
+  } else {
+    rb = ld_relaxed_u32((const uint32_t*)&h.ctrl[CTRL_RBEG + rk]);
+    re = ld_relaxed_u32((const uint32_t*)&h.ctrl[CTRL_RBEG + rk + 1]);
+  }
+  const uint32_t* R = h.R + rb;
   const uint32_t N = h.types[T].cap;
-  const uint64_t total = (uint64_t)r * N;
+  const uint64_t total = (uint64_t)(re - rb) * N;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   typename Mth::Acc acc;
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
     const uint32_t bi = (uint32_t)(e / N);
     const uint32_t s = (uint32_t)(e - (uint64_t)bi * N);
-    const uint32_t b = h.R[bi];
+    const uint32_t b = R[bi];
     const uint64_t w = snapshot ? h.iter_bm[b] : ld_relaxed(h.alloc_bm + b);
     if ((w >> s) & 1ull) Mth::run(h, T, b, s, a, acc);
   }

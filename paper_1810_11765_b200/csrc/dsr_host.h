@@ -12,6 +12,7 @@ struct LaunchCtx {
   cudaStream_t st;
   int grid;            // persistent grid size for element loops (multiple of #SMs)
   int sms;
+  int rk = -1;         // do-all body: range of R (-1 = all; k = k-th type of a subtree do-all)
 };
 
 struct MethodInfo {
@@ -64,7 +65,7 @@ inline int grid_for(const LaunchCtx& c, uint64_t n, K kernel, int threads = 256)
 template <class Mth>
 inline void launch_doall(const LaunchCtx& c, uint32_t T, int snapshot, const void* args) {
   typename Mth::Args a = *reinterpret_cast<const typename Mth::Args*>(args);
-  k_doall<Mth><<<persistent_grid(c, k_doall<Mth>), 256, 0, c.st>>>(c.h, T, snapshot, a);
+  k_doall<Mth><<<persistent_grid(c, k_doall<Mth>), 256, 0, c.st>>>(c.h, T, snapshot, c.rk, a);
   count_launch();
 }
 

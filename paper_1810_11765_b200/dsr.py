@@ -25,6 +25,7 @@ F_NO_ROTATE, F_NO_COALESCE, F_STATS, F_SPIN_ON_OOM, F_NO_HINT, F_CTA_NEW, F_HOME
 K_MB_NEW, M_MB_REDUCE, M_MB_FREE_ODD, M_MB_FREE_ALL = 1, 1, 2, 3
 K_LS_ALLOC, K_LS_FREE = 2, 3
 K_REPLAY, K_TORTURE, M_COLLECT = 4, 5, 4
+K_INH_NEW, K_INH_READ, M_INH_BUMP, M_INH_SUM, M_INH_SPAWN = 6, 7, 5, 6, 7
 K_GOL_INIT_ALIVE, K_GOL_INIT_CAND, K_GOL_HALO_PACK, K_GOL_HALO_APPLY = 10, 11, 12, 13
 M_GOL_CAND_PREPARE, M_GOL_ALIVE_PREPARE, M_GOL_CAND_UPDATE, M_GOL_ALIVE_UPDATE, M_GOL_DUMP = 10, 11, 12, 13, 14
 C_WT_CELL, K_WT_INIT_AGENTS = 20, 21
@@ -45,7 +46,7 @@ C_NB_BODY, K_NB_CLEAR_SNAPSHOT, K_NB_CLAIM = 30, 30, 31
 
 
 class TypeDesc(C.Structure):
-    _fields_ = [("num_fields", C.c_uint32), ("field_bytes", C.c_uint32 * MAX_FIELDS)]
+    _fields_ = [("num_fields", C.c_uint32), ("field_bytes", C.c_uint32 * MAX_FIELDS), ("parent", C.c_uint32)]
 
 
 class Layout(C.Structure):
@@ -92,6 +93,11 @@ class MbNewArgs(C.Structure):
 
 class MbReduceArgs(C.Structure):
     _fields_ = [("out3", C.c_void_p)]
+
+
+class InhArgs(C.Structure):
+    _fields_ = [("handles", C.c_void_p), ("ntypes", C.c_uint32), ("spawn_id0", C.c_uint32), ("out", C.c_void_p),
+                ("vals", C.c_void_p)]
 
 
 class LsArgs(C.Structure):
@@ -219,7 +225,8 @@ def kernel_launches() -> int:
     return lib().dsr_kernel_launches()
 
 
-def type_descs(type_fields):
+def type_descs(type_fields, parents=None):
+    """parents[t]: index of t's base type, or None / -1 (no base)."""
     arr = (TypeDesc * len(type_fields))()
     for t, fields in enumerate(type_fields):
         if not 1 <= len(fields) <= MAX_FIELDS:
@@ -227,13 +234,15 @@ def type_descs(type_fields):
         arr[t].num_fields = len(fields)
         for f, b in enumerate(fields):
             arr[t].field_bytes[f] = b
+        p = parents[t] if parents is not None else None
+        arr[t].parent = 0 if p is None or p < 0 else p + 1
     return arr
 
 
-def layout_compute(type_fields, heap_bytes) -> dict:
+def layout_compute(type_fields, heap_bytes, parents=None) -> dict:
     L = Layout()
-    check("dsr_layout_compute", lib().dsr_layout_compute(type_descs(type_fields), len(type_fields), heap_bytes,
-                                                          C.byref(L)))
+    check("dsr_layout_compute", lib().dsr_layout_compute(type_descs(type_fields, parents), len(type_fields),
+                                                          heap_bytes, C.byref(L)))
     return L.to_dict()
 
 
@@ -253,7 +262,8 @@ class Heap:
     """A DynaSOAr heap in a torch-owned device buffer (the host handle
     allocates one large buffer on the GPU)."""
 
-    def __init__(self, type_fields, heap_bytes, device=None, retries=5, flags=0, seed=0x5EED, stream=None):
+    def __init__(self, type_fields, heap_bytes, device=None, retries=5, flags=0, seed=0x5EED, stream=None,
+                 parents=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("no CUDA device: the DynaSOAr hot path runs only on the GPU")
@@ -265,7 +275,7 @@ class Heap:
         self.stream = stream
         h = C.c_void_p()
         with torch.cuda.device(self.device):
-            check("dsr_heap_create", lib().dsr_heap_create(type_descs(type_fields), self.ntypes,
+            check("dsr_heap_create", lib().dsr_heap_create(type_descs(type_fields, parents), self.ntypes,
                                                            C.c_void_p(self.buf.data_ptr()), heap_bytes,
                                                            C.byref(self.cfg), self._s(), C.byref(h)))
         self.h = h

@@ -57,6 +57,32 @@ def test_layout_equals_oracle(L, O):
                     assert a[k] == v, (k, tf, heap)
 
 
+def test_inheritance_layout_is_the_flattened_layout(L, O):
+    """a subtype's data segment begins with the SOA columns of its
+    inherited fields, then its own; so a hierarchy lays out exactly like the
+    flattened field lists (the oracle has no notion of a base type)."""
+    tf = [[4, 4], [4, 4, 8], [4, 4, 1], [4, 4, 8, 4], [4, 4, 8, 4, 2, 2]]
+    parents = [None, 0, 0, 1, 3]
+    for heap in (1 << 20, 1 << 28):
+        a = L.layout_compute(tf, heap, parents)
+        b = O.layout(tf, heap)
+        assert a == L.layout_compute(tf, heap)
+        for k, v in b.items():
+            if k == "col_off":
+                assert [a[k][t][:len(tf[t])] for t in range(len(tf))] == v
+            else:
+                assert a[k] == v
+
+
+def test_inheritance_rejects_invalid(L):
+    with pytest.raises(L.DsrError):
+        L.layout_compute([[4, 4], [4, 8, 8]], 1 << 20, [None, 0])      # inherited prefix differs
+    with pytest.raises(L.DsrError):
+        L.layout_compute([[4, 4, 8], [4, 4]], 1 << 20, [1, None])      # base declared later
+    with pytest.raises(L.DsrError):
+        L.layout_compute([[4, 4]], 1 << 20, [0])                       # own base
+
+
 def test_layout_rejects_invalid(L):
     with pytest.raises(ValueError):
         L.layout_compute([[4], [16] * 16 + [4]], 1 << 20)        # > 16 fields (binding)
