@@ -81,7 +81,10 @@ def one_wator(cfg):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     f, b = agent_frag(sim.heap, [FISH, SHARK])
+    from paper_1810_11765_b200 import dsr
+    err = sim.heap.poll_error()
     return {"ms_per_step": round(ms, 4), "steps": steps, "agent_frag": f, "agent_blocks": b,
+            "device_error": dsr.status_str(err),
             "fish": sim.heap.live_count(FISH), "sharks": sim.heap.live_count(SHARK)}
 
 
@@ -111,6 +114,9 @@ def one_ls(cfg):
 
 
 def runs():
+    if os.environ.get("ABL_ONLY") == "wator-noshift":
+        return [("wator", {"name": n, "flags": FLAGS[n], "r": 5, **hb}) for n in ("NoShift", "NoCoal-NoShift")
+                for hb in ({}, {"heap_bytes": 4 << 30})]
     out = []
     for name in ["default", "NoShift", "NoCoal", "NoCoal-NoShift", "NoHint"]:
         out.append(("mb", {"name": name, "flags": FLAGS[name], "r": 5, "reserve": True}))
