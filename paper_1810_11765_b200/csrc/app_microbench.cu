@@ -44,9 +44,14 @@ __global__ void __launch_bounds__(256) k_mb_reduce(DevHeap h, uint32_t T, unsign
   for (int f = 0; f < NF; ++f) cols[f] = h.types[T].col_off[f];
   uint64_t cnt = 0, sum = 0;
   uint32_t x = 0;
-  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
-    const uint32_t bi = (uint32_t)(e / Q);
-    const uint32_t q = (uint32_t)(e - (uint64_t)bi * Q);
+  // quad e -> (block index, quad) = (e / Q, e % Q), advanced incrementally by the grid stride
+  uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t bi = e / Q;
+  uint32_t q = (uint32_t)(e - bi * Q);
+  const uint64_t dbi = stride / Q;
+  const uint32_t dq = (uint32_t)(stride - dbi * Q);
+  for (; e < total; e += stride, bi += dbi, q += dq) {
+    if (q >= Q) { q -= Q; ++bi; }
     const uint32_t b = __ldg(h.R + bi);
     const uint32_t m4 = (uint32_t)(__ldg((const unsigned long long*)h.alloc_bm + b) >> (4 * q)) & 0xFu;
     if (!m4) continue;

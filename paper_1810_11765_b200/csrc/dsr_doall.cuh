@@ -93,12 +93,20 @@ __global__ void __launch_bounds__(256, 8) k_doall(DevHeap h, uint32_t T, int sna
   const uint64_t total = (uint64_t)(re - rb) * N;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   typename Mth::Acc acc;
-  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
-    const uint32_t bi = (uint32_t)(e / N);
-    const uint32_t s = (uint32_t)(e - (uint64_t)bi * N);
+  // element e -> (block index bi, slot s) = (e / N, e % N), advanced
+  // incrementally by the grid stride (two divisions per thread, not per element)
+  uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t bi = e / N;
+  uint32_t s = (uint32_t)(e - bi * N);
+  const uint64_t dbi = stride / N;
+  const uint32_t ds = (uint32_t)(stride - dbi * N);
+  for (; e < total; e += stride) {
     const uint32_t b = R[bi];
     const uint64_t w = snapshot ? h.iter_bm[b] : ld_relaxed(h.alloc_bm + b);
     if ((w >> s) & 1ull) Mth::run(h, T, b, s, a, acc);
+    bi += dbi;
+    s += ds;
+    if (s >= N) { s -= N; ++bi; }
   }
   Mth::flush(acc, a);
 }
