@@ -113,6 +113,7 @@ typedef struct {
    * zero-slot reservations, and SM cycles summed over leaders spent in the
    * lookup, the slow path, the reservation (+ FULL handling), whole requests */
   uint64_t requests, finds, find_fails, reserve_zero, cyc_find, cyc_slow, cyc_reserve, cyc_request;
+  uint64_t hint_zero;        /* zero-slot reservations on the warp's hinted block (part of reserve_zero) */
 } dsr_counters;
 
 typedef struct dsr_heap dsr_heap;   /* opaque, host side, owned by the library */

@@ -635,6 +635,7 @@ extern "C" dsr_status dsr_stats(dsr_heap* h, dsr_counters* out, void* stream) {
   out->cyc_slow = v[ST_CYC_SLOW];
   out->cyc_reserve = v[ST_CYC_RES];
   out->cyc_request = v[ST_CYC_REQ];
+  out->hint_zero = v[ST_HINTZERO];
   return DSR_OK;
 }
 extern "C" dsr_status dsr_stats_reset(dsr_heap* h, void* stream) {

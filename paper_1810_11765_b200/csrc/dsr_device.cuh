@@ -45,7 +45,8 @@ struct DevType {
 enum { CTRL_ERR = 0, CTRL_RCOUNT = 1, CTRL_SCRATCH = 2, CTRL_RBEG = 4, CTRL_STATS = 16, CTRL_AUDIT = 40 };
 enum { ERRB_OOM = 1, ERRB_BUDGET = 2 };
 enum { ST_ALLOCS = 0, ST_FREES, ST_INITS, ST_BFREES, ST_ROLLBACKS, ST_INVFAIL, ST_RESRETRY, ST_OOM,
-       ST_REQ, ST_FIND, ST_FINDFAIL, ST_RESZERO, ST_CYC_FIND, ST_CYC_SLOW, ST_CYC_RES, ST_CYC_REQ, ST_N };
+       ST_REQ, ST_FIND, ST_FINDFAIL, ST_RESZERO, ST_CYC_FIND, ST_CYC_SLOW, ST_CYC_RES, ST_CYC_REQ, ST_HINTZERO,
+       ST_N };
 
 struct DevHeap {
   uint8_t* data;          // M * block_bytes SOA data segments
@@ -423,11 +424,12 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
   if (home) home_range(h.freebm, h.sms, &hlo, &hlen);
   for (uint64_t iter = 0;; ++iter) {
     int64_t bid = -1;
-    bool fresh = false;
+    bool fresh = false, hinted = false;
     long long c1 = prof ? clock64() : 0;
     if (hint < h.M) {
       bid = hint;
       hint = 0xFFFFFFFFu;
+      hinted = true;
     } else if (fails < h.r_attempts) {
       uint64_t leaf = 0;
       bid = home ? bm_find_home(h.activebm[T], hlo, hlen, rot_hash(h, who, iter), &leaf)
@@ -470,7 +472,11 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
     // found blocks, assuming them empty, was measured 1.5x slower: partial
     // fills doubled the number of requests.)
     const uint64_t got = block_reserve(h, (uint32_t)bid, need, rot, &before, fresh, h.types[T].pad);
-    if (!got) { if (prof) stat_add(h, ST_RESZERO, 1); ++fails; continue; }    // full or invalidated
+    if (!got) {                                                               // full or invalidated
+      if (prof) { stat_add(h, ST_RESZERO, 1); if (hinted) stat_add(h, ST_HINTZERO, 1); }
+      ++fails;
+      continue;
+    }
     const uint32_t t = ld_relaxed_u8(h.type + bid) - 1u;                      // volatile read (Alg. 1 l.10)
     const bool full = (before | got) == ~0ull;
     if (full) bm_clear(h.activebm[t], (uint64_t)bid);                         // FULL -> inactive (l.12)

@@ -80,7 +80,7 @@ class Counters(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("allocs", "frees", "block_inits", "block_frees", "rollbacks",
                                           "invalidate_fail", "reserve_retries", "oom", "requests", "finds",
                                           "find_fails", "reserve_zero", "cyc_find", "cyc_slow", "cyc_reserve",
-                                          "cyc_request")]
+                                          "cyc_request", "hint_zero")]
 
     def to_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
