@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="microbench", choices=["microbench", "wator", "gol", "gol16k", "nbody"])
+    ap.add_argument("--workload", default="microbench", choices=["microbench", "wator", "gol", "gol16k", "gol16k-bits", "nbody"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -369,7 +369,7 @@ def run_app(args):
     import torch.distributed as dist
     from paper_1810_11765_b200 import dsr, inputs as I
     rank, world, local = dist_init(args.gpus)
-    if world > 1 and args.workload not in ("nbody", "gol16k", "wator"):
+    if world > 1 and args.workload not in ("nbody", "gol16k", "gol16k-bits", "wator"):
         raise SystemExit(f"--workload {args.workload} runs on one GPU (replicas only); use nbody, gol16k, wator "
                          "or microbench")
     stream = torch.cuda.Stream()
@@ -399,16 +399,16 @@ def run_app(args):
         cfg = {"workload": "wator (BASELINE configs[1]) 2048^2, FB6 SB12 SS6, seed 42",
                "parallelism": f"{world} row bands, NCCL P2P halo (4 exchanges per half step)" if world > 1
                else "1 GPU"}
-    elif args.workload in ("gol", "gol16k"):
+    elif args.workload in ("gol", "gol16k", "gol16k-bits"):
         from paper_1810_11765_b200.gol import GameOfLife, NcclHaloExchange
         Wd = 64 if args.workload == "gol" else 16384
         a0 = I.gol_soup(Wd, Wd, 0.3 if Wd == 64 else 0.25, 1 if Wd == 64 else 42)
         if world > 1:                      # row bands + NCCL exchange of boundary masks
-            sim = GameOfLife(a0, stream=stream, shard=(rank, world))
+            sim = GameOfLife(a0, stream=stream, shard=(rank, world), bit_mirror=args.workload.endswith("bits"))
             sim.exchange = NcclHaloExchange(sim)
             dist.barrier()
         else:
-            sim = GameOfLife(a0, stream=stream)
+            sim = GameOfLife(a0, stream=stream, bit_mirror=args.workload.endswith("bits"))
         step_fn = sim.generation
         if Wd == 64:                       # launch-bound: replay one generation as a CUDA graph
             sim.capture()
@@ -422,7 +422,8 @@ def run_app(args):
         visits = 2 * int(lv[:, 0].sum() + lv[:, 1].sum())
         visits, = reduce_over_ranks([float(visits)], "sum")
         ms, = reduce_over_ranks([ms], "max")
-        cfg = {"workload": f"gol {Wd}^2 torus (BASELINE configs[{0 if Wd == 64 else 3}])",
+        cfg = {"workload": f"gol {Wd}^2 torus (BASELINE configs[{0 if Wd == 64 else 3}])"
+                           + (", alive-bit mirror variant" if args.workload.endswith("bits") else ""),
                "parallelism": f"{world} row bands, NCCL P2P halo masks" if world > 1 else "1 GPU"}
     else:
         from paper_1810_11765_b200.nbody import NBody

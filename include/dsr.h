@@ -298,6 +298,13 @@ typedef struct {
    * [1] my row H (to the shard below), [2] received for ghost row 0, [3] for
    * ghost row H + 1. */
   uint32_t ghost; uint8_t* halo;
+  /* Optional alive-bit mirror (variant; NULL = off): 1 bit per cell (ghost rows
+   * included), row pitch ceil(W / 32) u32 words, zeroed by the caller before
+   * DSR_K_GOL_INIT_ALIVE.  Kept equal to "the cell holds an Alive" at every
+   * pass boundary (set on spawn, cleared on death, ghost rows from the halo);
+   * the prepare passes then count neighbours from it instead of loading 8
+   * handles (SURVEY D4 "state-grid mirror" design knob). */
+  uint32_t* bits;
 } dsr_gol_args;
 enum {
   DSR_K_GOL_INIT_ALIVE = 10,     /* n = W*H (W*(H+2) sharded); Alive(c) for alive0[c] (+ ghost cells) */

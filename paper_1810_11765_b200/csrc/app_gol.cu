@@ -35,7 +35,35 @@ __device__ __forceinline__ bool gol_local(const dsr_gol_args& a, uint32_t c) {
 // type bits say Alive, never dereferenced
 __device__ __forceinline__ uint64_t ghost_alive(const DevHeap& h) { return make_handle(GOL_ALIVE, h.types[GOL_ALIVE].cap, 0, 0); }
 
+// ---- optional alive-bit mirror (a.bits): 1 bit per cell, row pitch ceil(W/32) words
+__device__ __forceinline__ uint32_t gol_pitch(const dsr_gol_args& a) { return (a.W + 31) >> 5; }
+__device__ __forceinline__ void gol_bit_set(const dsr_gol_args& a, uint32_t c, bool v) {
+  const uint32_t x = c % a.W, y = c / a.W;
+  uint32_t* w = a.bits + (size_t)y * gol_pitch(a) + (x >> 5);
+  const uint32_t m = 1u << (x & 31);
+  if (v) atomicOr(w, m); else atomicAnd(w, ~m);
+}
+__device__ __forceinline__ uint32_t gol_bit(const uint32_t* row, uint32_t x) {
+  return (__ldg(row + (x >> 5)) >> (x & 31)) & 1u;
+}
+// alive cells among x-1, x, x+1 (torus in x) of one row
+__device__ __forceinline__ uint32_t gol_row3(const dsr_gol_args& a, const uint32_t* row, uint32_t x) {
+  const uint32_t o = x & 31;
+  if (o != 0 && o != 31 && x + 1 < a.W) return __popc((__ldg(row + (x >> 5)) >> (o - 1)) & 7u);
+  const uint32_t xl = x == 0 ? a.W - 1 : x - 1, xr = x + 1 == a.W ? 0 : x + 1;
+  return gol_bit(row, xl) + gol_bit(row, x) + gol_bit(row, xr);
+}
+__device__ __forceinline__ uint32_t gol_alive_nbrs_bits(const dsr_gol_args& a, uint32_t c) {
+  const uint32_t x = c % a.W, y = c / a.W, P = gol_pitch(a);
+  const uint32_t ym = a.ghost ? y - 1 : (y == 0 ? a.H - 1 : y - 1);
+  const uint32_t yp = a.ghost ? y + 1 : (y + 1 == a.H ? 0 : y + 1);
+  const uint32_t* r = a.bits + (size_t)y * P;
+  return gol_row3(a, a.bits + (size_t)ym * P, x) + gol_row3(a, r, x) + gol_row3(a, a.bits + (size_t)yp * P, x) -
+         gol_bit(r, x);
+}
+
 __device__ __forceinline__ uint32_t gol_alive_nbrs(const dsr_gol_args& a, uint32_t c) {
+  if (a.bits) return gol_alive_nbrs_bits(a, c);
   uint32_t k = 0;
 #pragma unroll
   for (int d = 0; d < 8; ++d)
@@ -68,6 +96,7 @@ __global__ void __launch_bounds__(256) k_gol_init(DevHeap h, uint64_t n, dsr_gol
     const uint64_t i = base + threadIdx.x;
     const uint32_t c = (uint32_t)i;
     bool want = false;
+    if (i < n && !cand && a.bits && a.alive0[c]) gol_bit_set(a, c, true);
     if (i < n && !gol_local(a, c)) {
       if (!cand) a.cell[c] = a.alive0[c] ? ghost_alive(h) : 0ull;   // ghost rows: neighbours' alive cells
     } else if (i < n) {
@@ -122,6 +151,7 @@ struct GolCandUpdate {    // pass 3 (allocates Alive)
     dsr_destroy(h, make_handle(T, h.types[T].cap, b, s));
     if (act == ACT_SPAWN) a.cell[c] = new_alive(h, c, 1);
     else a.cell[c] = 0;
+    if (act == ACT_SPAWN && a.bits) gol_bit_set(a, c, true);
   }
 };
 struct GolAliveUpdate {   // pass 4 (allocates Candidate)
@@ -139,6 +169,7 @@ struct GolAliveUpdate {   // pass 4 (allocates Candidate)
       }
     } else if (*field_ptr<uint8_t>(h, T, 2, b, s) == ACT_DIE) {
       dsr_destroy(h, make_handle(T, h.types[T].cap, b, s));
+      if (a.bits) gol_bit_set(a, c, false);
       todo = 1u << 8;
     }
     // allocate in warp-synchronous rounds so that every lane's k-th Candidate
@@ -184,6 +215,7 @@ __global__ void __launch_bounds__(256) k_gol_halo_apply(DevHeap h, uint64_t n, d
       const uint8_t* m = a.halo + (2 + side) * a.W;                    // received masks
       const uint32_t grow = side ? a.H + 1 : 0, brow = side ? a.H : 1;   // ghost row, my boundary row
       a.cell[(uint64_t)grow * a.W + x] = (m[x] & 1) ? ghost_alive(h) : 0ull;
+      if (a.bits) gol_bit_set(a, grow * a.W + x, m[x] & 1);
       const uint32_t xl = x == 0 ? a.W - 1 : x - 1, xr = x + 1 == a.W ? 0 : x + 1;
       if ((m[xl] | m[x] | m[xr]) & 2) {
         e = brow * a.W + x;

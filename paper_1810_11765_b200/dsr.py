@@ -119,7 +119,7 @@ class CollectArgs(C.Structure):
 
 class GolArgs(C.Structure):
     _fields_ = [("cell", C.c_void_p), ("W", C.c_uint32), ("H", C.c_uint32), ("alive0", C.c_void_p),
-                ("dump", C.c_void_p), ("ghost", C.c_uint32), ("halo", C.c_void_p)]
+                ("dump", C.c_void_p), ("ghost", C.c_uint32), ("halo", C.c_void_p), ("bits", C.c_void_p)]
 
 
 class WatorArgs(C.Structure):

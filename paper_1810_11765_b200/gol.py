@@ -26,7 +26,7 @@ class GameOfLife:
     single-heap result bit for bit."""
 
     def __init__(self, alive0, heap_bytes=None, device=None, stream=None, retries=5, flags=0, shard=None,
-                 exchange=None):
+                 exchange=None, bit_mirror=False):
         import numpy as np
         import torch
         Hg, W = alive0.shape
@@ -56,8 +56,12 @@ class GameOfLife:
         self.alive0 = torch.from_numpy(grid.reshape(-1)).to(dev)
         self.dumpbuf = torch.zeros(self.N, dtype=torch.int32, device=dev)
         self.halo = torch.zeros(4 * W, dtype=torch.uint8, device=dev)
+        # variant: alive-bit mirror read by the prepare passes (1 bit per cell instead of 8-B handles)
+        self.bits = torch.zeros(self.grid_rows * ((W + 31) // 32), dtype=torch.int32, device=dev) if bit_mirror \
+            else None
         self.args = dsr.GolArgs(self.cell.data_ptr(), W, H, self.alive0.data_ptr(), self.dumpbuf.data_ptr(),
-                                1 if shard is not None else 0, self.halo.data_ptr() if shard is not None else None)
+                                1 if shard is not None else 0, self.halo.data_ptr() if shard is not None else None,
+                                self.bits.data_ptr() if bit_mirror else None)
         self.heap.launch(dsr.K_GOL_INIT_ALIVE, self.N, self.args, stream)
         self.heap.launch(dsr.K_GOL_INIT_CAND, self.N, self.args, stream)
         self.gen = 0

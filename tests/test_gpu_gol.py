@@ -121,3 +121,36 @@ def test_gol_glider_crosses_shard_boundaries(G, O):
     lb = GameOfLifeLoopback(a0, 4)                 # bands of 16 rows: the glider crosses all of them
     lb.run(4 * 64)
     assert np.array_equal(lb.alive(), a0)
+
+
+@pytest.mark.parametrize("name", ["glider", "soup1"])
+def test_gol_bit_mirror_variant_bit_exact(G, O, name):
+    """The alive-bit mirror variant (prepare passes count neighbours from a
+    1-bit-per-cell grid) yields the same records every generation."""
+    from paper_1810_11765_b200 import inputs as I
+    a0 = I.gol_pattern(name) if name == "glider" else I.gol_soup(64, 64, 0.3, 1)
+    _, want = O.gol_run(a0, 60, dump=True)
+    g = G.GameOfLife(a0, bit_mirror=True)
+    for gen in range(60):
+        g.generation()
+        assert np.array_equal(g.records(), want[gen]), f"generation {gen + 1}"
+    bits = g.bits.cpu().numpy().view(np.uint32)
+    P = (64 + 31) // 32
+    alive = np.array([[(bits[y * P + x // 32] >> (x % 32)) & 1 for x in range(64)] for y in range(64)], np.uint8)
+    assert np.array_equal(alive, g.alive())                      # the mirror equals the object state
+    assert g.heap.check_invariants() == 0
+
+
+@pytest.mark.parametrize("W,H,P", [(45, 37, 1), (33, 40, 4), (31, 16, 2), (100, 64, 8)])
+def test_gol_bit_mirror_ragged_and_sharded(G, O, W, H, P):
+    """Widths that are not multiples of 32 (the x-1..x+1 window straddles
+    words and the torus seam), alone and in row-band shards."""
+    from paper_1810_11765_b200 import inputs as I
+    from paper_1810_11765_b200.gol import GameOfLifeLoopback
+    a0 = I.gol_soup(W, H, 0.35, W + H)
+    if H % P == 0 and P > 1:
+        sim = GameOfLifeLoopback(a0, P, bit_mirror=True)
+    else:
+        sim = G.GameOfLife(a0, bit_mirror=True)
+    sim.run(40)
+    assert np.array_equal(sim.alive(), O.life_dense(a0, 40))
