@@ -78,6 +78,25 @@ struct NbSnapshot {
 constexpr uint32_t kChunk = 4096;
 constexpr int kPairThreads = 128;
 
+// Blackwell packed FP32 (f32x2: FADD2 / FMUL2 / FFMA2 on sm_100a): the two
+// bodies of a thread go through one instruction per step; element-wise the
+// operations and their order are exactly the scalar ones below, so results
+// are bit-identical to a scalar evaluation.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float a, float b) {
+  f32x2 r; asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b)); return r;
+}
+__device__ __forceinline__ void upk2(f32x2 r, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r)); }
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
+  f32x2 r; asm("sub.rn.ftz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+  f32x2 r; asm("mul.rn.ftz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 r; asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c)); return r;
+}
+
 __global__ void __launch_bounds__(kPairThreads) k_nb_force_part(dsr_nbody_args a) {
   __shared__ float4 tile[256];
   const uint32_t n = a.n_total, nl = a.id_hi - a.id_lo;
@@ -85,8 +104,9 @@ __global__ void __launch_bounds__(kPairThreads) k_nb_force_part(dsr_nbody_args a
   const float4 p0 = i0 < a.id_hi ? s4(a, i0) : make_float4(0.f, 0.f, 0.f, 0.f);
   const float4 p1 = i1 < a.id_hi ? s4(a, i1) : make_float4(0.f, 0.f, 0.f, 0.f);
   const float eps2 = a.eps * a.eps;
+  const f32x2 PX = pk2(p0.x, p1.x), PY = pk2(p0.y, p1.y), E2 = pk2(eps2, eps2);
   const uint32_t jb = blockIdx.y * kChunk, je = min(jb + kChunk, n);
-  float ax0 = 0.f, ay0 = 0.f, ax1 = 0.f, ay1 = 0.f;
+  f32x2 AX = pk2(0.f, 0.f), AY = pk2(0.f, 0.f);
   for (uint32_t j0 = jb; j0 < je; j0 += 256) {
     __syncthreads();
     const uint32_t ja = j0 + threadIdx.x, jc = ja + 128;
@@ -96,14 +116,21 @@ __global__ void __launch_bounds__(kPairThreads) k_nb_force_part(dsr_nbody_args a
 #pragma unroll 8
     for (int k = 0; k < 256; ++k) {
       const float4 p = tile[k];                      // out-of-range entries have m = 0
-      const float dx0 = p.x - p0.x, dy0 = p.y - p0.y, dx1 = p.x - p1.x, dy1 = p.y - p1.y;
-      const float r0 = fmaf(dx0, dx0, fmaf(dy0, dy0, eps2)), r1 = fmaf(dx1, dx1, fmaf(dy1, dy1, eps2));
-      const float v0 = rsqrtf(r0), v1 = rsqrtf(r1);
-      const float w0 = p.z * v0 * v0 * v0, w1 = p.z * v1 * v1 * v1;
-      ax0 = fmaf(dx0, w0, ax0); ay0 = fmaf(dy0, w0, ay0);
-      ax1 = fmaf(dx1, w1, ax1); ay1 = fmaf(dy1, w1, ay1);
+      // per body: dx = x_j - x_i, r = dx^2 + (dy^2 + eps^2), w = ((m_j v) v) v with
+      // v = rsqrt(r), a += dx w  (P:171-174 with Plummer softening, R-NBODY)
+      const f32x2 DX = sub2(pk2(p.x, p.x), PX), DY = sub2(pk2(p.y, p.y), PY);
+      const f32x2 R = fma2(DX, DX, fma2(DY, DY, E2));
+      float r0, r1;
+      upk2(R, r0, r1);
+      const f32x2 V = pk2(rsqrtf(r0), rsqrtf(r1));
+      const f32x2 W = mul2(mul2(mul2(pk2(p.z, p.z), V), V), V);
+      AX = fma2(DX, W, AX);
+      AY = fma2(DY, W, AY);
     }
   }
+  float ax0, ax1, ay0, ay1;
+  upk2(AX, ax0, ax1);
+  upk2(AY, ay0, ay1);
   float2* part = reinterpret_cast<float2*>(a.scratch) + (size_t)blockIdx.y * nl;
   if (i0 < a.id_hi) part[i0 - a.id_lo] = make_float2(ax0, ay0);
   if (i1 < a.id_hi) part[i1 - a.id_lo] = make_float2(ax1, ay1);
@@ -153,6 +180,7 @@ __global__ void __launch_bounds__(kPairThreads) k_nb_merge_part(dsr_nbody_args a
   const float4 p0 = i0 < a.id_hi ? s4(a, i0) : make_float4(0.f, 0.f, 0.f, 0.f);
   const float4 p1 = i1 < a.id_hi ? s4(a, i1) : make_float4(0.f, 0.f, 0.f, 0.f);
   const float R2 = a.R * a.R;
+  const f32x2 PX = pk2(p0.x, p1.x), PY = pk2(p0.y, p1.y);
   const uint32_t jb = blockIdx.y * kChunk, je = min(jb + kChunk, n);
   uint32_t b0 = kNone, b1 = kNone;
   float d0 = R2, d1 = R2;                              // strict d2 < R^2, ties -> smaller j (j ascends)
@@ -165,8 +193,10 @@ __global__ void __launch_bounds__(kPairThreads) k_nb_merge_part(dsr_nbody_args a
 #pragma unroll 4
     for (int k = 0; k < 256; ++k) {
       const float4 p = tile[k];
-      const float dx0 = p.x - p0.x, dy0 = p.y - p0.y, dx1 = p.x - p1.x, dy1 = p.y - p1.y;
-      const float e0 = fmaf(dx0, dx0, dy0 * dy0), e1 = fmaf(dx1, dx1, dy1 * dy1);
+      // per body (packed f32x2): e = dx^2 + dy^2 as fma(dx, dx, dy * dy)
+      const f32x2 DX = sub2(pk2(p.x, p.x), PX), DY = sub2(pk2(p.y, p.y), PY);
+      float e0, e1;
+      upk2(fma2(DX, DX, mul2(DY, DY)), e0, e1);
       if (e0 < d0 || e1 < d1) {                        // rare: a body within R
         const uint32_t j = j0 + k;
         if (e0 < d0 && p.z > 0.f && (p.z > p0.z || (p.z == p0.z && j > i0))) { d0 = e0; b0 = j; }
