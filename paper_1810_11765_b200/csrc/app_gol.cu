@@ -247,8 +247,10 @@ bool gol_method_info(uint32_t id, MethodInfo* mi) {
   switch (id) {
     case DSR_M_GOL_CAND_PREPARE: case DSR_M_GOL_ALIVE_PREPARE: case DSR_M_GOL_DUMP:
       *mi = {0, sizeof(dsr_gol_args)}; return true;
-    case DSR_M_GOL_CAND_UPDATE: case DSR_M_GOL_ALIVE_UPDATE:
+    case DSR_M_GOL_CAND_UPDATE:
       *mi = {1, sizeof(dsr_gol_args)}; return true;
+    case DSR_M_GOL_ALIVE_UPDATE:                        // up to 8 new Candidates per visit: dynamic
+      *mi = {2, sizeof(dsr_gol_args)}; return true;
   }
   return false;
 }

@@ -6,7 +6,8 @@
 
 namespace dsr {
 
-__constant__ uint32_t kMbType[4] = {0, 0, 1, 2};   // [A, A, B, C][t & 3]
+__constant__ uint32_t kMbType[4] = {0, 0, 1, 2};
+constexpr uint32_t kMbChunk = 8;   // warp work unit: 8 x 32 consecutive t   // [A, A, B, C][t & 3]
 
 // ---- phase 1 / 4: user kernel, thread t does new [A,A,B,C][t&3] (device new)
 // (MINB CTAs x 256 threads per SM; latency-bound, so occupancy matters).  The
@@ -14,18 +15,37 @@ __constant__ uint32_t kMbType[4] = {0, 0, 1, 2};   // [A, A, B, C][t & 3]
 // default kernel carries none of its 16 KB of shared memory.
 template <bool CTA, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_mb_new(DevHeap h, uint64_t n, dsr_mb_new_args a) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t kp = rng_prefix(a.seed, 0);
-  // uniform trip count: every thread of the CTA reaches dsr_new_uniform together
-  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
-    const uint64_t i = base + threadIdx.x;
+  auto one = [&](uint64_t i, uint64_t hd) {
+    if (!hd) return;
     const uint64_t t = a.t0 + i;
-    const uint32_t T = kMbType[t & 3];
-    const uint64_t hd = CTA ? dsr_new_uniform(h, T, i < n) : (i < n ? dsr_new(h, T) : 0ull);
-    if (hd) {
-      const uint32_t nf = h.types[T].nfields;
-      for (uint32_t k = 0; k < nf; ++k)
-        *field_ptr<uint32_t>(h, T, k, h_bid(hd), h_slot(hd)) = (uint32_t)rng_key_p(kp, 5, t * 16 + k);
+    const uint32_t T = h_type(hd);
+    const uint32_t nf = h.types[T].nfields;
+    for (uint32_t k = 0; k < nf; ++k)
+      *field_ptr<uint32_t>(h, T, k, h_bid(hd), h_slot(hd)) = (uint32_t)rng_key_p(kp, 5, t * 16 + k);
+  };
+  if (CTA) {
+    // uniform trip count: every thread of the CTA reaches dsr_new_uniform together
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+      const uint64_t i = base + threadIdx.x;
+      one(i, dsr_new_uniform(h, kMbType[(a.t0 + i) & 3], i < n));
+    }
+    return;
+  }
+  // Dynamic work distribution: a warp takes the next kMbChunk x 32 threads'
+  // worth of t from a device counter, so warps slowed by allocation contention
+  // do not leave a tail of idle SMs (static striding left half the warps idle
+  // on average, ncu achieved occupancy 49 %).
+  const uint32_t lane = threadIdx.x & 31;
+  for (;;) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&h.ctrl[CTRL_WORK], 32ull * kMbChunk);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= n) break;
+    for (uint32_t k = 0; k < kMbChunk; ++k) {
+      const uint64_t i = base + 32ull * k + lane;
+      one(i, i < n ? dsr_new(h, kMbType[(a.t0 + i) & 3]) : 0ull);
     }
   }
 }
@@ -329,8 +349,12 @@ bool mb_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* a
       {
         const dsr_mb_new_args& ma = *(const dsr_mb_new_args*)args;
         // (__launch_bounds__ minimum 8 / 6 / 4 CTAs per SM measured equal: 9.2-9.6 ms)
-        if (c.h.flags & DSR_F_CTA_NEW) k_mb_new<true, 8><<<grid_for(c, n, k_mb_new<true, 8>), 256, 0, c.st>>>(c.h, n, ma);
-        else k_mb_new<false, 8><<<grid_for(c, n, k_mb_new<false, 8>), 256, 0, c.st>>>(c.h, n, ma);
+        if (c.h.flags & DSR_F_CTA_NEW) {
+          k_mb_new<true, 8><<<grid_for(c, n, k_mb_new<true, 8>), 256, 0, c.st>>>(c.h, n, ma);
+        } else {
+          if (cudaMemsetAsync(&c.h.ctrl[CTRL_WORK], 0, 8, c.st) != cudaSuccess) { *ok = 0; return true; }
+          k_mb_new<false, 8><<<grid_for(c, n, k_mb_new<false, 8>), 256, 0, c.st>>>(c.h, n, ma);
+        }
       }
       count_launch();
       return true;

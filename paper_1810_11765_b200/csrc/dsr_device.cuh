@@ -42,7 +42,8 @@ struct DevType {
 
 // control page word offsets (u64 units) -- DESIGN.md "HBM layout"
 // CTRL_RBEG + k: begin of the k-th type's range of R in a subtree do-all (k <= DSR_MAX_TYPES)
-enum { CTRL_ERR = 0, CTRL_RCOUNT = 1, CTRL_SCRATCH = 2, CTRL_RBEG = 4, CTRL_STATS = 16, CTRL_AUDIT = 40 };
+// CTRL_WORK: dynamic work counter of persistent user kernels
+enum { CTRL_ERR = 0, CTRL_RCOUNT = 1, CTRL_SCRATCH = 2, CTRL_WORK = 3, CTRL_RBEG = 4, CTRL_STATS = 16, CTRL_AUDIT = 40 };
 enum { ERRB_OOM = 1, ERRB_BUDGET = 2 };
 enum { ST_ALLOCS = 0, ST_FREES, ST_INITS, ST_BFREES, ST_ROLLBACKS, ST_INVFAIL, ST_RESRETRY, ST_OOM,
        ST_REQ, ST_FIND, ST_FINDFAIL, ST_RESZERO, ST_CYC_FIND, ST_CYC_SLOW, ST_CYC_RES, ST_CYC_REQ, ST_HINTZERO,

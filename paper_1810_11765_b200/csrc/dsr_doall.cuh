@@ -19,7 +19,8 @@
 
 namespace dsr {
 
-constexpr int kCompactThreads = 64;   // small CTAs: ~8 per SM at M = 4.6 M blocks (latency-bound)
+constexpr int kCompactThreads = 64;
+constexpr uint32_t kDoallChunk = 4;   // dynamic work unit of allocating passes: 4 x 32 elements per warp   // small CTAs: ~8 per SM at M = 4.6 M blocks (latency-bound)
 
 static __global__ void __launch_bounds__(kCompactThreads) k_compact(DevHeap h, uint32_t T, int snapshot) {
   __shared__ uint64_t s_word[kCompactThreads];
@@ -79,7 +80,7 @@ static __global__ void __launch_bounds__(kCompactThreads) k_compact(DevHeap h, u
 // Persistent-grid element loop shared by all method kernels.  rk < 0: the
 // whole of R; rk = k: the k-th type's range of a subtree do-all
 // (ctrl[CTRL_RBEG + k] .. ctrl[CTRL_RBEG + k + 1]).
-template <class Mth>
+template <class Mth, bool DYN>
 __global__ void __launch_bounds__(256, 8) k_doall(DevHeap h, uint32_t T, int snapshot, int rk, typename Mth::Args a) {
   uint32_t rb = 0, re;
   if (rk < 0) {
@@ -93,6 +94,33 @@ __global__ void __launch_bounds__(256, 8) k_doall(DevHeap h, uint32_t T, int sna
   const uint64_t total = (uint64_t)(re - rb) * N;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   typename Mth::Acc acc;
+  if (DYN) {
+    // Passes with very uneven per-object cost (several allocations per visit):
+    // a warp takes the next 32 x kDoallChunk elements from a device counter
+    // (ctrl[CTRL_WORK], zeroed before the launch) instead of a static stride --
+    // no tail of idle SMs waiting for the slowest warps.  (Measured: GoL
+    // Alive.update 19.5 -> 10-13 ms at 16384^2; light passes get slower.)
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t q32 = 32u / N, r32 = 32u % N;
+    for (;;) {
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(&h.ctrl[CTRL_WORK], 32ull * kDoallChunk);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (base >= total) break;
+      uint64_t e = base + lane;
+      uint64_t bi = e / N;
+      uint32_t s = (uint32_t)(e - bi * N);
+      for (uint32_t k = 0; k < kDoallChunk && e < total; ++k, e += 32) {
+        const uint32_t b = R[bi];
+        if ((h.iter_bm[b] >> s) & 1ull) Mth::run(h, T, b, s, a, acc);
+        bi += q32;
+        s += r32;
+        if (s >= N) { s -= N; ++bi; }
+      }
+    }
+    Mth::flush(acc, a);
+    return;
+  }
   // element e -> (block index bi, slot s) = (e / N, e % N), advanced
   // incrementally by the grid stride (two divisions per thread, not per element)
   uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -20,6 +20,8 @@ struct MethodInfo {
   // iteration-bitmap snapshot.  Without it a visitor could see slots
   // allocated during the pass, or -- when a block empties and is invalidated
   // (all bits set, Alg. 9) -- phantom objects in slots that were already dead.
+  // 2: snapshot + dynamic work distribution (k_doall), for passes whose
+  // per-object cost is very uneven (several allocations per visit).
   int snapshot;
   size_t args_bytes;   // expected sizeof(args)
 };
@@ -65,7 +67,12 @@ inline int grid_for(const LaunchCtx& c, uint64_t n, K kernel, int threads = 256)
 template <class Mth>
 inline void launch_doall(const LaunchCtx& c, uint32_t T, int snapshot, const void* args) {
   typename Mth::Args a = *reinterpret_cast<const typename Mth::Args*>(args);
-  k_doall<Mth><<<persistent_grid(c, k_doall<Mth>), 256, 0, c.st>>>(c.h, T, snapshot, c.rk, a);
+  if (snapshot == 2) {                                                     // dynamic work distribution
+    cudaMemsetAsync(&c.h.ctrl[CTRL_WORK], 0, 8, c.st);
+    k_doall<Mth, true><<<persistent_grid(c, k_doall<Mth, true>), 256, 0, c.st>>>(c.h, T, snapshot, c.rk, a);
+  } else {
+    k_doall<Mth, false><<<persistent_grid(c, k_doall<Mth, false>), 256, 0, c.st>>>(c.h, T, snapshot, c.rk, a);
+  }
   count_launch();
 }
 
