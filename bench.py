@@ -385,11 +385,15 @@ def run_app(args):
             dist.barrier()
         else:
             sim = WaTor(kind, egg, en, FB=6, SB=12, SS=6, seed=42, stream=stream)
+        step_fn = sim.step
+        if world == 1:                     # one step replayed as a CUDA graph (no host launch overhead)
+            sim.capture()
+            step_fn = sim.graph.replay
 
         def per(k):
             for t in range(2):
                 sim.heap.live_count_async(t, live[k, t], stream)
-        ms = time_steps(sim.step, K, W, stream, per)
+        ms = time_steps(step_fn, K, W, stream, per)
         lv = live.cpu().numpy()
         # visits of step k: 4 cell passes + 2 passes over the fish and sharks alive at its start
         starts = np.vstack([lv[:1] * 0 + lv[0], lv[:-1]])       # approx: counts at the previous step end

@@ -346,6 +346,10 @@ typedef struct {
    *   mig  (3 x u32)   migrating agents {kind, egg, energy} (kind 0 = none) */
   uint32_t ghost, y0, Hg;
   uint8_t* halo;
+  /* If non-NULL, the step number is read from this device word instead of
+   * `step` (so one captured CUDA graph of a step can be replayed while the
+   * caller advances the word on the device). */
+  const uint32_t* step_dev;
 } dsr_wator_args;
 #define DSR_WT_HALO_REQ_OUT(W)   0u
 #define DSR_WT_HALO_REQ_IN(W)    (2u * (W))

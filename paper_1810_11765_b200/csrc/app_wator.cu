@@ -43,6 +43,7 @@ __device__ __forceinline__ uint64_t wt_ghost_agent(const DevHeap& h, uint32_t ki
   return kind ? make_handle(kind - 1, h.types[kind - 1].cap, 0, 0) : 0ull;
 }
 struct WtMig { uint32_t kind, egg, energy; };
+__device__ __forceinline__ uint32_t wt_step(const dsr_wator_args& a) { return a.step_dev ? __ldg(a.step_dev) : a.step; }
 __device__ __forceinline__ uint8_t* wt_halo(const dsr_wator_args& a, uint32_t off, uint32_t side) {
   return a.halo + off + side * a.W;
 }
@@ -137,7 +138,7 @@ struct WtCellDecide {
     if (!nd) return;
     const uint32_t id = *field_ptr<uint32_t>(h, T, 0, b, s);
     if (!wt_local(a, id)) return;                                   // ghost cell: its owner decides
-    const uint32_t d = wt_pick(D, nd, rng_key(a.seed, a.step, PHASE, wt_gid(a, id)));
+    const uint32_t d = wt_pick(D, nd, rng_key(a.seed, wt_step(a), PHASE, wt_gid(a, id)));
     const uint32_t nb = wt_nbr(a, id, d);
     if (!wt_local(a, nb)) {                                         // a neighbour shard's agent: grant it
       wt_halo(a, DSR_WT_HALO_GRANT_OUT(a.W), nb == id - a.W ? 0 : 1)[nb % a.W] = 1;
@@ -160,7 +161,7 @@ struct WtFishPrepare {
     for (uint32_t d = 0; d < 4; ++d)
       if (*wt_agent(h, a, wt_nbr(a, c, d)) == 0) fr[nf++] = d;
     if (nf) {
-      const uint32_t d = wt_pick(fr, nf, rng_key(a.seed, a.step, PH_FISH_REQ, wt_gid(a, c)));
+      const uint32_t d = wt_pick(fr, nf, rng_key(a.seed, wt_step(a), PH_FISH_REQ, wt_gid(a, c)));
       *wt_req(h, a, wt_nbr(a, c, d), d ^ 2) = 1;
     } else {
       *wt_req(h, a, c, 4) = 1;
@@ -210,7 +211,7 @@ struct WtSharkPrepare {
       if (ag == 0) fr[nfr++] = d;
       else if (h_is(ag, WT_FISH)) fd[nfd++] = d;
     }
-    const uint64_t key = rng_key(a.seed, a.step, PH_SHARK_REQ, wt_gid(a, c));
+    const uint64_t key = rng_key(a.seed, wt_step(a), PH_SHARK_REQ, wt_gid(a, c));
     if (nfd) {
       const uint32_t d = wt_pick(fd, nfd, key);
       *wt_req(h, a, wt_nbr(a, c, d), d ^ 2) = 1;

@@ -128,7 +128,7 @@ class WatorArgs(C.Structure):
                 ("kind0", C.c_void_p), ("egg0", C.c_void_p), ("energy0", C.c_void_p),
                 ("out_kind", C.c_void_p), ("out_egg", C.c_void_p), ("out_energy", C.c_void_p),
                 ("counters", C.c_void_p), ("ghost", C.c_uint32), ("y0", C.c_uint32), ("Hg", C.c_uint32),
-                ("halo", C.c_void_p)]
+                ("halo", C.c_void_p), ("step_dev", C.c_void_p)]
 
 
 class NbodyArgs(C.Structure):

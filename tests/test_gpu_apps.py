@@ -41,6 +41,22 @@ def test_wator_every_step_bit_exact(P, O, W, H, seed):
     assert sim.heap.check_invariants() == 0
 
 
+def test_wator_cuda_graph_replay(P, O):
+    """One step captured as a CUDA graph (step number in a device word the
+    graph advances) and replayed: every replayed step equals the oracle."""
+    from paper_1810_11765_b200 import inputs as I, wator
+    kind, egg, en = I.wator_init(96, 64, seed=13)
+    sim = wator.WaTor(kind, egg, en, **WT)
+    sim.capture()                                  # runs step 0 eagerly (warm-up)
+    k, e, n, _ = O.wator_run(kind, egg, en, steps=1, **WT)
+    for s in range(1, 25):
+        sim.run_graph(1)
+        k, e, n, _ = O.wator_run(k, e, n, steps=1, step0=s, **WT)
+        gk, ge, gn = sim.state()
+        assert np.array_equal(gk, k) and np.array_equal(ge, e) and np.array_equal(gn, n), f"step {s}"
+    assert sim.heap.check_invariants() == 0
+
+
 def test_wator_2048_prefix_against_oracle(P, O):
     """BASELINE configs[1] grid (2048^2, seed 42) for 10 steps."""
     from paper_1810_11765_b200 import inputs as I, wator
