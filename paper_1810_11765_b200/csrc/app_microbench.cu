@@ -295,7 +295,7 @@ bool mb_method_info(uint32_t id, MethodInfo* mi) {
   switch (id) {
     case DSR_M_MB_REDUCE: *mi = {0, sizeof(dsr_mb_reduce_args)}; return true;
     case DSR_M_MB_FREE_ODD: *mi = {1, 0}; return true;      // self-delete
-    case DSR_M_MB_FREE_ALL: *mi = {1, 0}; return true;
+    case DSR_M_MB_FREE_ALL: *mi = {3, 0}; return true;      // frees whole blocks: blocked distribution
     case DSR_M_COLLECT: *mi = {0, sizeof(dsr_collect_args)}; return true;
     case DSR_M_INH_BUMP: case DSR_M_INH_SUM: *mi = {0, sizeof(dsr_inh_args)}; return true;
     case DSR_M_INH_SPAWN: *mi = {1, sizeof(dsr_inh_args)}; return true;

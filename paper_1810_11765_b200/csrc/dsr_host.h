@@ -22,6 +22,8 @@ struct MethodInfo {
   // (all bits set, Alg. 9) -- phantom objects in slots that were already dead.
   // 2: snapshot + dynamic work distribution (k_doall), for passes whose
   // per-object cost is very uneven (several allocations per visit).
+  // 3: snapshot + blocked distribution (one contiguous range of R per warp),
+  // for passes that free whole blocks.
   int snapshot;
   size_t args_bytes;   // expected sizeof(args)
 };
@@ -69,9 +71,12 @@ inline void launch_doall(const LaunchCtx& c, uint32_t T, int snapshot, const voi
   typename Mth::Args a = *reinterpret_cast<const typename Mth::Args*>(args);
   if (snapshot == 2) {                                                     // dynamic work distribution
     cudaMemsetAsync(&c.h.ctrl[CTRL_WORK], 0, 8, c.st);
-    k_doall<Mth, true><<<persistent_grid(c, k_doall<Mth, true>), 256, 0, c.st>>>(c.h, T, snapshot, c.rk, a);
+    k_doall<Mth, kSchedDynamic><<<persistent_grid(c, k_doall<Mth, kSchedDynamic>), 256, 0, c.st>>>(c.h, T, 1, c.rk, a);
+  } else if (snapshot == 3) {
+    k_doall<Mth, kSchedBlocked><<<persistent_grid(c, k_doall<Mth, kSchedBlocked>), 256, 0, c.st>>>(c.h, T, 1, c.rk, a);
   } else {
-    k_doall<Mth, false><<<persistent_grid(c, k_doall<Mth, false>), 256, 0, c.st>>>(c.h, T, snapshot, c.rk, a);
+    k_doall<Mth, kSchedCyclic><<<persistent_grid(c, k_doall<Mth, kSchedCyclic>), 256, 0, c.st>>>(c.h, T, snapshot, c.rk,
+                                                                                                 a);
   }
   count_launch();
 }
