@@ -161,3 +161,36 @@ def test_nbody_sharded_loopback_equals_one_gpu(P, O):
         assert np.array_equal(a[k], b[k]), k
     for sh in lb.shards:
         assert sh.heap.check_invariants() == 0
+
+
+@pytest.mark.slow
+def test_wator_2048_row_shards_against_oracle(P, O):
+    """BASELINE configs[1] grid split into 8 row bands (loopback on one GPU):
+    10 steps equal the oracle, counters included."""
+    from paper_1810_11765_b200 import inputs as I, wator
+    kind, egg, en = I.wator_init(2048, 2048, seed=42)
+    lb = wator.WaTorLoopback(kind, egg, en, 8, **WT)
+    lb.run(10)
+    gk, ge, gn = lb.state()
+    k, e, n, c = O.wator_run(kind, egg, en, steps=10, **WT)
+    assert np.array_equal(gk, k) and np.array_equal(ge, e) and np.array_equal(gn, n)
+    assert lb.read_counters() == [int(c[:, j].sum()) for j in (2, 3, 4, 5)]
+
+
+@pytest.mark.slow
+def test_wator_2048_100_steps_counters_and_final_state(P, O):
+    """configs[1] for 100 steps: the event counters match every step and the
+    final state matches (oracle: about a minute on one core)."""
+    from paper_1810_11765_b200 import inputs as I, wator
+    kind, egg, en = I.wator_init(2048, 2048, seed=42)
+    sim = wator.WaTor(kind, egg, en, **WT)
+    prev = [0, 0, 0, 0]
+    k, e, n, c = O.wator_run(kind, egg, en, steps=100, **WT)
+    for s in range(100):
+        sim.step()
+        cur = sim.read_counters()
+        assert [a - b for a, b in zip(cur, prev)] == [int(c[s, j]) for j in (2, 3, 4, 5)], f"step {s}"
+        prev = cur
+    gk, ge, gn = sim.state()
+    assert np.array_equal(gk, k) and np.array_equal(ge, e) and np.array_equal(gn, n)
+    assert sim.heap.check_invariants() == 0

@@ -154,3 +154,33 @@ def test_gol_bit_mirror_ragged_and_sharded(G, O, W, H, P):
         sim = G.GameOfLife(a0, bit_mirror=True)
     sim.run(40)
     assert np.array_equal(sim.alive(), O.life_dense(a0, 40))
+
+
+@pytest.mark.slow
+def test_gol_16384_row_shards_equal_single_heap_and_dense(G, O):
+    """BASELINE configs[3] as it is sharded at 8 GPUs: 8 row-band heaps of
+    2048 rows (loopback exchange on one GPU) for 3 generations equal the
+    single-heap GPU run everywhere and the oracle's dense Life on sampled
+    windows, including windows that straddle band boundaries."""
+    from paper_1810_11765_b200 import inputs as I
+    from paper_1810_11765_b200.gol import GameOfLifeLoopback
+    W = H = 16384
+    a0 = I.gol_soup(W, H, 0.25, 42)
+    gens = 3
+    lb = GameOfLifeLoopback(a0, 8)
+    lb.run(gens)
+    got = lb.alive()
+    for s in lb.shards:
+        assert s.heap.check_invariants() == 0
+    del lb
+    torch.cuda.empty_cache()
+    g = G.GameOfLife(a0)
+    g.run(gens)
+    assert np.array_equal(got, g.alive())
+    del g
+    rng = np.random.default_rng(1)
+    for y in [2048 - 131, 4096 - 131, int(rng.integers(0, H - 300)), 14336 - 131]:   # windows stay inside the grid
+        x = int(rng.integers(0, W - 300))
+        win = a0[y:y + 262, x:x + 262]
+        want = O.life_dense(np.ascontiguousarray(win), gens)[3:259, 3:259]
+        assert np.array_equal(got[y + 3:y + 259, x + 3:x + 259], want)
