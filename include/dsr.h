@@ -222,6 +222,25 @@ dsr_status dsr_stats_reset(dsr_heap* h, void* stream);
 dsr_status dsr_copy_state(dsr_heap* h, uint32_t what, uint32_t type, void* host_out, size_t cap, size_t* used,
                           void* stream);
 
+/* Canonical dump of the live objects of `type` (synchronising; SURVEY c.8):
+ * each live object as one packed record -- its fields in declaration order,
+ * field_bytes[f] bytes each (little endian), no padding -- with the records
+ * sorted lexicographically by their bytes, so the dump does not depend on
+ * placement (which block and slot an object got).  host_buf gets the
+ * records if cap is large enough; *used = live x record bytes either way
+ * (DSR_ERR_INVALID when cap < *used).  Rebuilds the do-all block list R. */
+dsr_status dsr_canonical_dump(dsr_heap* h, uint32_t type, void* host_buf, size_t cap, size_t* used, void* stream);
+
+/* The device-side heap descriptor: a POD that kernels take by value.  User
+ * kernels compiled outside this library against the device header
+ * paper_1810_11765_b200/csrc/dsr_device.cuh call dsr::dsr_new,
+ * dsr::dsr_destroy and dsr::field_ptr on it like the library's own kernels
+ * (new / destroy from GPU code), and every host call of this
+ * header keeps working on the same heap.  out (host) receives the view;
+ * out_bytes must equal dsr_device_view_bytes(). */
+size_t dsr_device_view_bytes(void);
+dsr_status dsr_device_view(const dsr_heap* h, void* out, size_t out_bytes);
+
 /* Number of kernels this library launched since load (host counter). */
 uint64_t dsr_kernel_launches(void);
 const char* dsr_status_str(dsr_status s);

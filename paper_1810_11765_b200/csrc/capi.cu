@@ -10,7 +10,9 @@
 #define DSR_BUILD_INFO "sm_100a"
 #endif
 
+#include <algorithm>
 #include <mutex>
+#include <vector>
 #include <unordered_map>
 
 namespace dsr {
@@ -666,6 +668,65 @@ extern "C" dsr_status dsr_copy_state(dsr_heap* h, uint32_t what, uint32_t type, 
   if (what == 5) CUDA_TRY(cudaMemcpyAsync((uint8_t*)host_out + n, &h->dev.ctrl[CTRL_RCOUNT], 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   if (used) *used = n + (what == 5 ? 8 : 0);
+  return DSR_OK;
+}
+
+// ---------------------------------------------------------------- canonical dump, device view
+__global__ void k_dump_records(DevHeap h, uint32_t T, uint32_t rb, uint8_t* out, unsigned long long* cursor) {
+  const uint32_t r = ld_relaxed_u32((const uint32_t*)&h.ctrl[CTRL_RCOUNT]);
+  const uint32_t N = h.types[T].cap;
+  const uint64_t total = (uint64_t)r * N;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = h.R[e / N], s = (uint32_t)(e % N);
+    if (!((h.alloc_bm[b] >> s) & 1ull)) continue;
+    uint8_t* rec = out + atomicAdd(cursor, 1ull) * rb;
+    for (uint32_t f = 0, o = 0; f < h.types[T].nfields; ++f) {
+      const uint32_t sz = h.types[T].fsize[f];
+      const uint8_t* src = h.data + (size_t)b * h.block_bytes + h.types[T].col_off[f] + (size_t)s * sz;
+      for (uint32_t k = 0; k < sz; ++k) rec[o + k] = src[k];
+      o += sz;
+    }
+  }
+}
+
+extern "C" dsr_status dsr_canonical_dump(dsr_heap* h, uint32_t type, void* host_buf, size_t cap, size_t* used,
+                                         void* stream) {
+  if (!h || type >= h->L.ntypes || !used) return DSR_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint64_t live = 0;
+  dsr_status s = dsr_live_count_sync(h, type, &live, stream);
+  if (s != DSR_OK) return s;
+  uint32_t rb = 0;
+  for (uint32_t f = 0; f < h->types[type].num_fields; ++f) rb += h->types[type].field_bytes[f];
+  *used = (size_t)live * rb;
+  if (!host_buf || cap < *used) return DSR_ERR_INVALID;
+  if (live == 0) return DSR_OK;
+  uint8_t* d = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&d, *used + 8, st));
+  unsigned long long* cursor = (unsigned long long*)(d + *used);
+  CUDA_TRY(cudaMemsetAsync(cursor, 0, 8, st));
+  CUDA_TRY(cudaMemsetAsync(&h->dev.ctrl[CTRL_RCOUNT], 0, 8, st));
+  const uint64_t nwords = (h->L.M + 63) / 64;
+  k_compact<<<(int)((nwords + kCompactThreads - 1) / kCompactThreads), kCompactThreads, 0, st>>>(h->dev, type, 0);
+  k_dump_records<<<h->sms * 8, 256, 0, st>>>(h->dev, type, rb, d, cursor);
+  count_launch(2);
+  std::vector<uint8_t> tmp(*used);
+  CUDA_TRY(cudaMemcpyAsync(tmp.data(), d, *used, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaFreeAsync(d, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  std::vector<uint64_t> idx(live);
+  for (uint64_t i = 0; i < live; ++i) idx[i] = i;
+  const uint8_t* base = tmp.data();
+  std::sort(idx.begin(), idx.end(),
+            [&](uint64_t a, uint64_t b) { return memcmp(base + a * rb, base + b * rb, rb) < 0; });
+  for (uint64_t i = 0; i < live; ++i) memcpy((uint8_t*)host_buf + i * rb, base + idx[i] * rb, rb);
+  return DSR_OK;
+}
+
+extern "C" size_t dsr_device_view_bytes(void) { return sizeof(DevHeap); }
+extern "C" dsr_status dsr_device_view(const dsr_heap* h, void* out, size_t out_bytes) {
+  if (!h || !out || out_bytes != sizeof(DevHeap)) return DSR_ERR_INVALID;
+  memcpy(out, &h->dev, sizeof(DevHeap));
   return DSR_OK;
 }
 

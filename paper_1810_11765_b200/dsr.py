@@ -202,6 +202,12 @@ def lib():
         L.dsr_stats_reset.argtypes = [vp, vp]
         L.dsr_copy_state.restype = st
         L.dsr_copy_state.argtypes = [vp, C.c_uint32, C.c_uint32, vp, C.c_size_t, C.POINTER(C.c_size_t), vp]
+        L.dsr_canonical_dump.restype = st
+        L.dsr_canonical_dump.argtypes = [vp, C.c_uint32, vp, C.c_size_t, C.POINTER(C.c_size_t), vp]
+        L.dsr_device_view_bytes.restype = C.c_size_t
+        L.dsr_device_view_bytes.argtypes = []
+        L.dsr_device_view.restype = st
+        L.dsr_device_view.argtypes = [vp, vp, C.c_size_t]
         L.dsr_kernel_launches.restype = C.c_uint64
         L.dsr_kernel_launches.argtypes = []
         L.dsr_status_str.restype = C.c_char_p
@@ -368,6 +374,27 @@ class Heap:
 
     def stats_reset(self, stream=None):
         check("dsr_stats_reset", lib().dsr_stats_reset(self.h, self._s(stream)))
+
+    def canonical_dump(self, type_, stream=None):
+        """Live objects of type_ as packed records (fields in declaration order,
+        no padding), sorted by their bytes: (live, record_bytes) uint8 array."""
+        import numpy as np
+        used = C.c_size_t()
+        rc = lib().dsr_canonical_dump(self.h, type_, None, 0, C.byref(used), self._s(stream))
+        if rc not in (OK, ERR_INVALID):
+            check("dsr_canonical_dump", rc)
+        rb = sum(self.type_fields[type_])
+        out = np.zeros(max(used.value, 1), dtype=np.uint8)
+        check("dsr_canonical_dump", lib().dsr_canonical_dump(self.h, type_, out.ctypes.data, out.nbytes,
+                                                             C.byref(used), self._s(stream)))
+        return out[:used.value].reshape(-1, rb)
+
+    def device_view(self) -> bytes:
+        """The device heap descriptor (POD) for user kernels built against csrc/dsr_device.cuh."""
+        n = lib().dsr_device_view_bytes()
+        buf = (C.c_uint8 * n)()
+        check("dsr_device_view", lib().dsr_device_view(self.h, buf, n))
+        return bytes(buf)
 
     def copy_state(self, what, type_=0, stream=None):
         import numpy as np
