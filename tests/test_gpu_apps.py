@@ -194,3 +194,23 @@ def test_wator_2048_100_steps_counters_and_final_state(P, O):
     gk, ge, gn = sim.state()
     assert np.array_equal(gk, k) and np.array_equal(ge, e) and np.array_equal(gn, n)
     assert sim.heap.check_invariants() == 0
+
+
+def test_independent_heaps_on_concurrent_streams(P, O):
+    """Two heaps, two CUDA streams, interleaved launches (Wa-Tor on one, GoL on
+    the other): each equals its oracle -- heaps share no device state."""
+    from paper_1810_11765_b200 import inputs as I, wator, gol
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    kind, egg, en = I.wator_init(64, 64, seed=21)
+    a0 = I.gol_soup(64, 64, 0.3, 22)
+    w = wator.WaTor(kind, egg, en, stream=s1, **WT)
+    g = gol.GameOfLife(a0, stream=s2)
+    for _ in range(30):
+        w.step()
+        g.generation()
+    torch.cuda.synchronize()
+    k, e, n, _ = O.wator_run(kind, egg, en, steps=30, **WT)
+    gk, ge, gn = w.state()
+    assert np.array_equal(gk, k) and np.array_equal(ge, e) and np.array_equal(gn, n)
+    assert np.array_equal(g.alive(), O.life_dense(a0, 30))
+    assert w.heap.check_invariants() == 0 and g.heap.check_invariants() == 0
