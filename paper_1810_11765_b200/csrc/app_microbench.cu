@@ -21,8 +21,10 @@ __global__ void __launch_bounds__(256, MINB) k_mb_new(DevHeap h, uint64_t n, dsr
     const uint64_t t = a.t0 + i;
     const uint32_t T = h_type(hd);
     const uint32_t nf = h.types[T].nfields;
+    // the object's slot in column 0; column k is col_off[k] bytes further (u32 fields)
+    uint8_t* const obj = h.data + (size_t)h_bid(hd) * h.block_bytes + 4u * h_slot(hd);
     for (uint32_t k = 0; k < nf; ++k)
-      *field_ptr<uint32_t>(h, T, k, h_bid(hd), h_slot(hd)) = (uint32_t)rng_key_p(kp, 5, t * 16 + k);
+      *reinterpret_cast<uint32_t*>(obj + h.types[T].col_off[k]) = (uint32_t)rng_key_p(kp, 5, t * 16 + k);
   };
   if (CTA) {
     // uniform trip count: every thread of the CTA reaches dsr_new_uniform together
@@ -45,7 +47,8 @@ __global__ void __launch_bounds__(256, MINB) k_mb_new(DevHeap h, uint64_t n, dsr
     if (base >= n) break;
     for (uint32_t k = 0; k < kMbChunk; ++k) {
       const uint64_t i = base + 32ull * k + lane;
-      one(i, i < n ? dsr_new(h, kMbType[(a.t0 + i) & 3]) : 0ull);
+      const uint32_t r = (uint32_t)((a.t0 + i) & 3);
+      one(i, i < n ? dsr_new(h, r ? r - 1 : 0) : 0ull);                  // [A, A, B, C][t & 3]
     }
   }
 }
