@@ -9,7 +9,7 @@ timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --
 timeout -s KILL 600 $NCU -k regex:"k_mb_new" -s 2 -c 1 -o gpurun_out/r01_mb_new -f python scripts/prof_targets.py mb > gpurun_out/ncu_a.log 2>&1
 timeout -s KILL 600 $NCU -k regex:"k_mb_reduce" -s 6 -c 3 -o gpurun_out/r01_mb_reduce -f python scripts/prof_targets.py mb > gpurun_out/ncu_b.log 2>&1
 timeout -s KILL 600 $NCU -k regex:"MbFree" -s 6 -c 6 -o gpurun_out/r01_mb_free -f python scripts/prof_targets.py mb > gpurun_out/ncu_c.log 2>&1
-timeout -s KILL 600 $NCU -k regex:"k_compact" -s 24 -c 3 -o gpurun_out/r01_compact -f python scripts/prof_targets.py mb > gpurun_out/ncu_d.log 2>&1
+timeout -s KILL 600 $NCU -k regex:"k_compact" -s 13 -c 3 -o gpurun_out/r01_compact -f python scripts/prof_targets.py mb > gpurun_out/ncu_d.log 2>&1
 timeout -s KILL 600 $NCU -k regex:"k_nb_|NbMove|NbSnapshot" -s 8 -c 6 -o gpurun_out/r01_nbody -f python scripts/prof_targets.py nbody > gpurun_out/ncu_e.log 2>&1
 timeout -s KILL 600 $NCU -k regex:"Wt" -s 8 -c 8 -o gpurun_out/r01_wator -f python scripts/prof_targets.py wator > gpurun_out/ncu_f.log 2>&1
 timeout -s KILL 300 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1
