@@ -403,6 +403,12 @@ def run_app(args):
         cfg = {"workload": "wator (BASELINE configs[1]) 2048^2, FB6 SB12 SS6, seed 42",
                "parallelism": f"{world} row bands, NCCL P2P halo (4 exchanges per half step)" if world > 1
                else "1 GPU"}
+        if world == 1:                     # the paper's static-allocation baseline, same start
+            from paper_1810_11765_b200.wator import WaTorStatic
+            base = WaTorStatic(kind, egg, en, FB=6, SB=12, SS=6, seed=42, stream=stream)
+            bms = time_steps(lambda: base.run(1), K, W, stream)
+            cfg["static_baseline"] = {"ms_per_step": bms, "dynamic_over_static": ms / bms,
+                                      "what": "same rules on cell-indexed SOA arrays, no heap (dsr_wator_static_step)"}
     elif args.workload in ("gol", "gol16k", "gol16k-bits"):
         from paper_1810_11765_b200.gol import GameOfLife, NcclHaloExchange
         Wd = 64 if args.workload == "gol" else 16384

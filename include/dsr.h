@@ -429,6 +429,36 @@ enum {
   DSR_K_NB_CLAIM = 31            /* n = n_total: the claim pass over the (gathered) target array */
 };
 
+/* ---- Static-allocation baseline of Wa-Tor ----
+ * "Baselines (SOA/AOS) are application variants without any dynamic memory
+ * allocation ... In category (3), classes are merged with the underlying
+ * static cell data structure".  The Wa-Tor rules, keys and
+ * request / decide protocol of the object version (reading R-WATOR) on
+ * cell-indexed SOA device arrays, no heap: its results equal the object
+ * version's and the oracle's (or_wator_dense) bit for bit, so its time prices
+ * DynaSOAr's dynamic allocation on the same GPU.
+ *   kind[c]   u8   0 empty, 1 fish, 2 shark        (in/out, W*H)
+ *   egg[c]    u32  breeding counter                (in/out, W*H; 0 on empty cells)
+ *   energy[c] u32  shark energy                    (in/out, W*H; 0 unless shark)
+ *   target[c] u32  scratch, W*H, all 0xFFFFFFFF before the first call (the call leaves it so)
+ *   req       u8   scratch, W*H rounded up to a multiple of 4 bytes, 4-byte aligned,
+ *                  all zero before the first call (the call leaves it so)
+ *   counters  u64[4] or NULL: += fish born, sharks born, fish eaten, sharks starved
+ * All pointers are caller-owned device memory; the call only enqueues work.
+ * Torus W x H, W, H >= 3, W*H < 2^32.  DSR_ERR_INVALID on a bad argument. */
+typedef struct {
+  uint32_t W, H;
+  uint32_t FB, SB, SS;
+  uint32_t step;                  /* step number of the first step (RNG key) */
+  uint64_t seed;
+  uint8_t* kind; uint32_t* egg; uint32_t* energy;
+  uint32_t* target; uint8_t* req;
+  unsigned long long* counters;
+} dsr_wator_static_args;
+/* `steps` consecutive Wa-Tor steps (6 kernels each: prepare / decide / update
+ * for fish, then sharks) on `stream` (cudaStream_t as void*, NULL = default). */
+dsr_status dsr_wator_static_step(const dsr_wator_static_args* args, uint32_t steps, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

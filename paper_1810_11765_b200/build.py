@@ -16,7 +16,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT = PKG / "libdsr.so"
 BUILD = PKG / "_build"
-SOURCES = ["capi.cu", "app_microbench.cu", "app_gol.cu", "app_wator.cu", "app_nbody.cu"]
+SOURCES = ["capi.cu", "app_microbench.cu", "app_gol.cu", "app_wator.cu", "app_wator_static.cu", "app_nbody.cu"]
 HEADERS = ["dsr_device.cuh", "dsr_doall.cuh", "dsr_host.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -131,6 +131,12 @@ class WatorArgs(C.Structure):
                 ("halo", C.c_void_p), ("step_dev", C.c_void_p)]
 
 
+class WatorStaticArgs(C.Structure):
+    _fields_ = [("W", C.c_uint32), ("H", C.c_uint32), ("FB", C.c_uint32), ("SB", C.c_uint32), ("SS", C.c_uint32),
+                ("step", C.c_uint32), ("seed", C.c_uint64), ("kind", C.c_void_p), ("egg", C.c_void_p),
+                ("energy", C.c_void_p), ("target", C.c_void_p), ("req", C.c_void_p), ("counters", C.c_void_p)]
+
+
 class NbodyArgs(C.Structure):
     _fields_ = [("S", C.c_void_p), ("V", C.c_void_p), ("target", C.c_void_p), ("incoming", C.c_void_p),
                 ("shandle", C.c_void_p),
@@ -172,6 +178,8 @@ def lib():
         L.dsr_heap_layout.argtypes = [vp, C.POINTER(Layout)]
         L.dsr_heap_configure.restype = st
         L.dsr_heap_configure.argtypes = [vp, C.POINTER(Config)]
+        L.dsr_wator_static_step.restype = st
+        L.dsr_wator_static_step.argtypes = [C.POINTER(WatorStaticArgs), C.c_uint32, vp]
         L.dsr_parallel_new.restype = st
         L.dsr_parallel_new.argtypes = [vp, C.c_uint32, C.c_uint64, C.c_uint32, vp, C.c_size_t, vp]
         L.dsr_parallel_do.restype = st

@@ -238,3 +238,52 @@ class WaTorLoopback:
 
     def read_counters(self):
         return [sum(v) for v in zip(*(s.read_counters() for s in self.shards))]
+
+
+class WaTorStatic:
+    """The paper's static-allocation baseline: the same Wa-Tor rules
+    on cell-indexed SOA device arrays, no heap, no objects (dsr_wator_static_step).
+    Its state after any number of steps equals WaTor's bit for bit; its time
+    prices the dynamic allocation."""
+
+    def __init__(self, kind, egg, energy, FB=6, SB=12, SS=6, seed=42, device=None, stream=None, step0=0):
+        import ctypes as C
+        import numpy as np
+        import torch
+        H, W = kind.shape
+        self.H, self.W, self.N = H, W, H * W
+        self.device = torch.device(device if device is not None else "cuda")
+        self.stream = stream
+        dev = self.device
+        self.kind = torch.from_numpy(np.ascontiguousarray(kind, dtype=np.uint8).ravel()).to(dev)
+        self.egg = torch.from_numpy(np.ascontiguousarray(egg, dtype=np.uint32).ravel().view(np.int32)).to(dev)
+        self.energy = torch.from_numpy(np.ascontiguousarray(energy, dtype=np.uint32).ravel().view(np.int32)).to(dev)
+        self.target = torch.full((self.N,), -1, dtype=torch.int32, device=dev)
+        self.req = torch.zeros(((self.N + 3) // 4) * 4, dtype=torch.uint8, device=dev)
+        self.counters = torch.zeros(4, dtype=torch.int64, device=dev)
+        self.args = dsr.WatorStaticArgs(W, H, FB, SB, SS, step0, seed, self.kind.data_ptr(), self.egg.data_ptr(),
+                                        self.energy.data_ptr(), self.target.data_ptr(), self.req.data_ptr(),
+                                        self.counters.data_ptr())
+        self.step_no = step0
+        self._C = C
+
+    def run(self, steps, stream=None):
+        s = stream if stream is not None else self.stream
+        self.args.step = self.step_no
+        dsr.check("dsr_wator_static_step",
+                  dsr.lib().dsr_wator_static_step(self._C.byref(self.args), steps, dsr._stream_ptr(s)))
+        self.step_no += steps
+
+    def state(self):
+        """(kind, egg, energy) per cell as (H, W) numpy arrays."""
+        import numpy as np
+        import torch
+        torch.cuda.synchronize()
+        k = self.kind.cpu().numpy().reshape(self.H, self.W).copy()
+        e = self.egg.cpu().numpy().view(np.uint32).reshape(self.H, self.W).copy()
+        n = self.energy.cpu().numpy().view(np.uint32).reshape(self.H, self.W).copy()
+        return k, e, n
+
+    def read_counters(self):
+        """Cumulative (fish born, sharks born, eaten, starved)."""
+        return [int(v) for v in self.counters.cpu().tolist()]
