@@ -71,6 +71,9 @@ def ncu_traffic():
             v = [r["dram_bytes"] for r in rows if key in r.get("kernel", "") and "dram_bytes" in r]
             if v:
                 out[key] = sum(v) / len(v)
+            v = [r["inst_executed"] for r in rows if key in r.get("kernel", "") and "inst_executed" in r]
+            if v:
+                out[key + ":inst"] = sum(v) / len(v)
     return out
 
 
@@ -327,6 +330,16 @@ def run_ours(args):
                          "traffic": traffic.get("k_mb_new"), "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": new_bytes / 2,
                          "note": "latency/contention-bound on the shared active-block bitmaps, not HBM"},
+            # the allocation kernel is instruction-issue bound (ncu: issue slots ~80 % busy): warp
+            # instructions per new1 launch (committed ncu --set full summary) / live new1 time, against
+            # 148 SMs x 4 schedulers x 1 warp-instruction/clk at the sampled SM clock
+            "roofline_issue": None if "k_mb_new:inst" not in traffic or not clk.get("sm_mhz") else {
+                "bound": "issue", "kernel": "k_mb_new (phase new1 launch)",
+                "achieved": traffic["k_mb_new:inst"] / (phase_ms[1] * 1e-3) / 1e9,
+                "peak": 148 * 4 * clk["sm_mhz"] * 1e6 / 1e9, "unit": "G warp-inst/s",
+                "frac": traffic["k_mb_new:inst"] / (phase_ms[1] * 1e-3) / (148 * 4 * clk["sm_mhz"] * 1e6),
+                "inst_per_launch": traffic["k_mb_new:inst"],
+                "note": "instruction count from the committed ncu summary of the same build (profiles/)"},
             "roofline_scan": {"bound": "hbm", "kernel": "k_mb_reduce<NF> (do-all field scan body, 6 launches/step; "
                                                         "the BASELINE >= 60% target)",
                               "achieved": scan_gbs, "peak": peak, "unit": "GB/s", "frac": scan_gbs / peak,

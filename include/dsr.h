@@ -109,7 +109,8 @@ typedef struct {
   uint64_t invalidate_fail;  /* failed / rolled-back invalidations (Alg. 9 l.8) */
   uint64_t reserve_retries;  /* reservations that lost every selected bit (Alg. 6 loop) */
   uint64_t oom;              /* OOM events */
-  /* profiling (DSR_F_STATS): leader requests, active lookups, failed lookups,
+  /* profiling (DSR_F_STATS in a library built with -DDSR_PROFILE, else 0):
+   * leader requests, active lookups, failed lookups,
    * zero-slot reservations, and SM cycles summed over leaders spent in the
    * lookup, the slow path, the reservation (+ FULL handling), whole requests */
   uint64_t requests, finds, find_fails, reserve_zero, cyc_find, cyc_slow, cyc_reserve, cyc_request;

@@ -43,15 +43,20 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, profile: bool = False) -> Path:
+    """profile=True: a second library, _build/libdsr_prof.so, compiled with
+    -DDSR_PROFILE (request-level allocator counters; load it with
+    DSR_LIBPATH=... for scripts/prof_mb.py).  The product library has none."""
+    out = BUILD / "libdsr_prof.so" if profile else OUT
+    if not force and not profile and not _stale():
         return OUT
     BUILD.mkdir(exist_ok=True)
     info = f'-DDSR_BUILD_INFO="sm_100a {_git_rev()} {time.strftime("%Y-%m-%d")}"'
+    extra = ["-DDSR_PROFILE"] if profile else []
 
     def compile_one(src: str) -> Path:
-        obj = BUILD / (Path(src).stem + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, *PER_FILE.get(src, []), info, "-I", str(ROOT / "include"), "-c",
+        obj = BUILD / (Path(src).stem + ("_prof" if profile else "") + ".o")
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, *PER_FILE.get(src, []), info, "-I", str(ROOT / "include"), "-c",
                str(CSRC / src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
@@ -62,16 +67,16 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    tmp = OUT.with_suffix(".so.tmp")
+    tmp = out.with_suffix(".so.tmp")
     cmd = [NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcuda"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
     t0 = time.time()
-    p = build(force="--force" in sys.argv, verbose=True)
+    p = build(force="--force" in sys.argv, verbose=True, profile="--profile" in sys.argv)
     print(f"built {p} in {time.time() - t0:.1f}s")

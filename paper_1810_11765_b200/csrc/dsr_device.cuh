@@ -414,8 +414,15 @@ __device__ __forceinline__ void block_free(const DevHeap& h, uint32_t T, uint32_
 // try_find_set FAILs or when the block it returned yields no slot (full or
 // invalidated meanwhile); after r failed attempts the leader takes the slow
 // path (reading R-RETRY).  Sequentially this is exactly Alg. 1.
+// The request-level profile (lookups, zero-slot reservations, cycle stamps)
+// exists only in a -DDSR_PROFILE build (scripts/gpu_stats.sh): its live
+// registers cost the default path spills and ~4 % of its instructions.
 static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint32_t T, uint32_t need, uint32_t* bid_out) {
+#ifdef DSR_PROFILE
   const bool prof = h.flags & DSR_F_STATS;
+#else
+  constexpr bool prof = false;
+#endif
   uint32_t oom_tries = 0, fails = 0;
   long long c0 = prof ? clock64() : 0;
   if (prof) stat_add(h, ST_REQ, 1);
@@ -442,14 +449,16 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
     int64_t bid = -1;
     bool fresh = false, hinted = false;
     long long c1 = prof ? clock64() : 0;
+    // one hash per attempt: bits 0-35 rotate the levels of the search, bits
+    // 58-63 the slot selection inside the block
+    const uint64_t rh = rot_hash(h, who, iter);
     if (hint < h.M) {
       bid = hint;
       hint = 0xFFFFFFFFu;
       hinted = true;
     } else if (fails < h.r_attempts) {
       uint64_t leaf = 0;
-      bid = home ? bm_find_home(h.activebm[T], hlo, hlen, rot_hash(h, who, iter), &leaf)
-                 : bm_try_find_set(h.activebm[T], rot_hash(h, who, iter), &leaf);
+      bid = home ? bm_find_home(h.activebm[T], hlo, hlen, rh, &leaf) : bm_try_find_set(h.activebm[T], rh, &leaf);
       if (prof) { stat_add(h, ST_FIND, 1); stat_add(h, ST_CYC_FIND, clock64() - c1); }
       if (bid < 0) { if (prof) stat_add(h, ST_FINDFAIL, 1); ++fails; continue; }
     } else {                                                                  // slow path
@@ -483,7 +492,7 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
     }
     uint64_t before = 0;
     long long c2 = prof ? clock64() : 0;
-    const uint32_t rot = (uint32_t)(rot_hash(h, who, iter + 0x1000) >> 58);
+    const uint32_t rot = (uint32_t)(rh >> 58);
     // A fresh block's word is known (no read).  (A "blind" first atomicOr on
     // found blocks, assuming them empty, was measured 1.5x slower: partial
     // fills doubled the number of requests.)

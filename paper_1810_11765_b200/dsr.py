@@ -11,7 +11,9 @@ import ctypes as C
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIBPATH = PKG / "libdsr.so"
+import os as _os
+# DSR_LIBPATH: an alternative build of the same library (A/B experiments only)
+LIBPATH = Path(_os.environ["DSR_LIBPATH"]) if _os.environ.get("DSR_LIBPATH") else PKG / "libdsr.so"
 
 MAX_TYPES, MAX_FIELDS, MAX_LEVELS = 8, 16, 6
 

@@ -16,6 +16,8 @@ KEYS = {
     "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum": "ld_sectors",
     "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum": "ld_requests",
     "lts__t_requests_srcunit_tex_op_atom.sum": "l2_atom_requests",
+    "smsp__inst_executed.sum": "inst_executed",
+    "sm__issue_active.avg.pct_of_peak_sustained_elapsed": "issue_active_pct",
 }
 UNIT = {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "s": 1.0, "nsecond": 1e-9,
         "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
