@@ -256,10 +256,15 @@ const char* dsr_build_info(void);
 
 /* ---- allocator microbenchmark (BASELINE configs[4], SURVEY c.4) ----
  * types: 0 = A{3 x u32}, 1 = B{4 x u32}, 2 = C{6 x u32} */
-typedef struct { uint64_t seed; uint64_t t0; } dsr_mb_new_args;   /* thread t -> new [A,A,B,C][(t0+t)&3] */
+/* thread t -> new [A,A,B,C][(t0+t)&3].  in == NULL: field k of thread t's
+ * object = low32(key(seed, 0, MB_FIELD, 16t + k)) computed on the device.
+ * in != NULL (device pointer, t0 % 4 == 0): the field values come from the
+ * caller, packed per 4 threads as 16 u32 = {A: 3, A: 3, B: 4, C: 6 fields},
+ * i.e. thread t0 + i reads in[16 (i / 4) + {0, 3, 6, 10}[i % 4] + k]. */
+typedef struct { uint64_t seed; uint64_t t0; const uint32_t* in; } dsr_mb_new_args;
 typedef struct { uint64_t* out3; } dsr_mb_reduce_args;           /* out3[0..2] += (count, sum, xor) */
 enum {
-  DSR_K_MB_NEW = 1,          /* args dsr_mb_new_args; fields k = low32(key(seed,0,MB_FIELD,16t+k)) */
+  DSR_K_MB_NEW = 1,          /* args dsr_mb_new_args; fields k = low32(key(seed,0,MB_FIELD,16t+k)) or from `in` */
   DSR_M_MB_REDUCE = 1,       /* args dsr_mb_reduce_args (no allocation: reads the allocation bitmap) */
   DSR_M_MB_FREE_ODD = 2,     /* args none: destroy(this) if field0 & 1 */
   DSR_M_MB_FREE_ALL = 3      /* args none: destroy(this) */

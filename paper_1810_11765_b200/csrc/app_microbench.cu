@@ -13,7 +13,9 @@ constexpr uint32_t kMbChunk = 8;   // warp work unit: 8 x 32 consecutive t   // 
 // (MINB CTAs x 256 threads per SM; latency-bound, so occupancy matters).  The
 // CTA-coalescing ablation (DSR_F_CTA_NEW) is a separate instantiation so the
 // default kernel carries none of its 16 KB of shared memory.
-template <bool CTA, int MINB>
+// IN: the field values come from the caller's array a.in (end-to-end runs with
+// host-resident inputs) instead of being computed from the key.
+template <bool CTA, int MINB, bool IN = false>
 __global__ void __launch_bounds__(256, MINB) k_mb_new(DevHeap h, uint64_t n, dsr_mb_new_args a) {
   const uint64_t kp = rng_prefix(a.seed, 0);
   auto one = [&](uint64_t i, uint64_t hd) {
@@ -23,8 +25,9 @@ __global__ void __launch_bounds__(256, MINB) k_mb_new(DevHeap h, uint64_t n, dsr
     const uint32_t nf = h.types[T].nfields;
     // the object's slot in column 0; column k is col_off[k] bytes further (u32 fields)
     uint8_t* const obj = h.data + (size_t)h_bid(hd) * h.block_bytes + 4u * h_slot(hd);
+    const uint32_t* src = IN ? a.in + 16 * (i >> 2) + ((0xA630u >> (4 * (i & 3))) & 0xFu) : nullptr;
     for (uint32_t k = 0; k < nf; ++k)
-      *reinterpret_cast<uint32_t*>(obj + h.types[T].col_off[k]) = (uint32_t)rng_key_p(kp, 5, t * 16 + k);
+      *reinterpret_cast<uint32_t*>(obj + h.types[T].col_off[k]) = IN ? __ldg(src + k) : (uint32_t)rng_key_p(kp, 5, t * 16 + k);
   };
   if (CTA) {
     // uniform trip count: every thread of the CTA reaches dsr_new_uniform together
@@ -352,11 +355,14 @@ bool mb_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* a
       {
         const dsr_mb_new_args& ma = *(const dsr_mb_new_args*)args;
         // (__launch_bounds__ minimum 8 / 6 / 4 CTAs per SM measured equal: 9.2-9.6 ms)
+        if (ma.in && (ma.t0 & 3)) { *ok = 0; return true; }
         if (c.h.flags & DSR_F_CTA_NEW) {
+          if (ma.in) { *ok = 0; return true; }
           k_mb_new<true, 8><<<grid_for(c, n, k_mb_new<true, 8>), 256, 0, c.st>>>(c.h, n, ma);
         } else {
           if (cudaMemsetAsync(&c.h.ctrl[CTRL_WORK], 0, 8, c.st) != cudaSuccess) { *ok = 0; return true; }
-          k_mb_new<false, 8><<<grid_for(c, n, k_mb_new<false, 8>), 256, 0, c.st>>>(c.h, n, ma);
+          if (ma.in) k_mb_new<false, 8, true><<<grid_for(c, n, k_mb_new<false, 8, true>), 256, 0, c.st>>>(c.h, n, ma);
+          else k_mb_new<false, 8><<<grid_for(c, n, k_mb_new<false, 8>), 256, 0, c.st>>>(c.h, n, ma);
         }
       }
       count_launch();

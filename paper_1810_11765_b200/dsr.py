@@ -90,7 +90,7 @@ class Counters(C.Structure):
 
 # ---- argument structs (mirror include/dsr.h)
 class MbNewArgs(C.Structure):
-    _fields_ = [("seed", C.c_uint64), ("t0", C.c_uint64)]
+    _fields_ = [("seed", C.c_uint64), ("t0", C.c_uint64), ("in_", C.c_void_p)]
 
 
 class MbReduceArgs(C.Structure):

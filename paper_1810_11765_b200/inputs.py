@@ -29,6 +29,32 @@ def key(seed, step, phase, idx):
     return sm(sm(s) ^ ((np.uint64(phase) << np.uint64(40)) | np.asarray(idx, dtype=np.uint64)))
 
 
+# ------------------------------------------------------------------ microbench
+MB_NF = (3, 3, 4, 6)       # fields of thread t's object, [A, A, B, C][t & 3]
+
+
+def mb_fields(seed: int, t0: int, n: int, chunk: int = 1 << 20) -> np.ndarray:
+    """Field values of threads t0 .. t0+n-1 of the microbench (t0 % 4 == 0,
+    n % 4 == 0), packed per 4 threads as 16 u32 {A: 3, A: 3, B: 4, C: 6}:
+    field k of thread t = low32(key(seed, 0, MB_FIELD, 16 t + k)) (DESIGN.md
+    "Input recipe").  Host-resident inputs for the end-to-end bench."""
+    assert t0 % 4 == 0 and n % 4 == 0
+    out = np.empty(4 * n, dtype=np.uint32)
+    # (thread offset within the group of 4, field k) for the 16 packed slots
+    toff = np.array([0] * 3 + [1] * 3 + [2] * 4 + [3] * 6, dtype=np.uint64)
+    kk = np.array([0, 1, 2, 0, 1, 2, 0, 1, 2, 3, 0, 1, 2, 3, 4, 5], dtype=np.uint64)
+    def fill(g0):
+        g = np.arange(g0, min(n // 4, g0 + chunk), dtype=np.uint64)
+        t = np.uint64(t0) + np.uint64(4) * g[:, None] + toff[None, :]
+        out[16 * g0:16 * (g0 + len(g))] = (key(seed, 0, PH_MB_FIELD, np.uint64(16) * t + kk[None, :])
+                                           & np.uint64(0xFFFFFFFF)).astype(np.uint32).ravel()
+    import concurrent.futures as cf
+    import os
+    with cf.ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:   # numpy releases the GIL
+        list(ex.map(fill, range(0, n // 4, chunk)))
+    return out
+
+
 # ------------------------------------------------------------------ Game of Life
 def gol_soup(W: int, H: int, p: float, seed: int) -> np.ndarray:
     """Bernoulli(p) alive bitmap, (H, W) uint8 (BASELINE configs[0]/[3])."""

@@ -228,3 +228,27 @@ def test_microbench_variants_match_oracle(D, O, reserve, flags):
     mb.step()
     assert np.array_equal(mb.results(), O.microbench(5, 200_000, 100_000)[0])
     assert mb.heap.check_invariants() == 0
+
+
+@pytest.mark.parametrize("n1,n2", [(1 << 16, 1 << 15), (400_000, 123_456)])
+def test_microbench_host_inputs_match_oracle(D, O, n1, n2):
+    """The end-to-end form of the step (bench.py e2e): field values copied from
+    host-resident arrays (inputs.mb_fields) instead of computed on the device;
+    same results as the oracle.  n2 not a multiple of 4 is padded by the caller."""
+    from paper_1810_11765_b200 import inputs as I
+    from paper_1810_11765_b200.microbench import Microbench
+    f1 = torch.from_numpy(I.mb_fields(1, 0, n1).view(np.int32)).cuda()
+    f2 = torch.from_numpy(I.mb_fields(1, n1, -(-n2 // 4) * 4).view(np.int32)).cuda()
+    mb = Microbench(n1=n1, n2=n2, seed=1)
+    mb.step(inputs=(f1.data_ptr(), f2.data_ptr()))
+    torch.cuda.synchronize()
+    assert np.array_equal(mb.results(), O.microbench(1, n1, n2)[0])
+    assert mb.heap.check_invariants() == 0
+
+
+def test_microbench_host_inputs_reject_unaligned_t0(D):
+    from paper_1810_11765_b200.microbench import Microbench
+    mb = Microbench(n1=4096, n2=4096, seed=1)
+    buf = torch.zeros(4 * 4096, dtype=torch.int32, device="cuda")
+    with pytest.raises(D.DsrError):
+        mb.heap.launch(D.K_MB_NEW, 1024, D.MbNewArgs(1, 2, buf.data_ptr()))
