@@ -12,6 +12,7 @@ timeout -s KILL 600 $NCU -k regex:"MbFree" -s 6 -c 6 -o gpurun_out/r01_mb_free -
 timeout -s KILL 600 $NCU -k regex:"k_compact" -s 13 -c 3 -o gpurun_out/r01_compact -f python scripts/prof_targets.py mb > gpurun_out/ncu_d.log 2>&1
 timeout -s KILL 600 $NCU -k regex:"k_nb_|NbMove|NbSnapshot" -s 8 -c 6 -o gpurun_out/r01_nbody -f python scripts/prof_targets.py nbody > gpurun_out/ncu_e.log 2>&1
 timeout -s KILL 600 $NCU -k regex:"Wt" -s 8 -c 8 -o gpurun_out/r01_wator -f python scripts/prof_targets.py wator > gpurun_out/ncu_f.log 2>&1
+timeout -s KILL 1200 $NCU -k regex:"Gol(CandPrepare|AliveUpdate|CandUpdate|AlivePrepare)" -s 4 -c 4 -o gpurun_out/r01_gol16k -f python scripts/prof_targets.py gol16k > gpurun_out/ncu_g.log 2>&1
 timeout -s KILL 300 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1
 rm -f gpurun_out/bench_apps.log
 for w in wator gol gol16k gol16k-bits nbody; do

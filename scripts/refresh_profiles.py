@@ -25,6 +25,12 @@ if reps:
                          capture_output=True, text=True).stdout
     (P / "ncu_summary.txt").write_text(txt)
 
+gr = G / f"{rnd}_gol16k.ncu-rep"
+if gr.exists():
+    txt = subprocess.run([sys.executable, str(ROOT / "scripts" / "ncu_summarize.py"), str(P / "ncu_gol16k.json"), str(gr)],
+                         capture_output=True, text=True).stdout
+    (P / "ncu_gol16k.txt").write_text(txt)
+
 lc = G / f"{rnd}_launches.csv"
 if lc.exists():
     shutil.copy(lc, P / "launches_bench_step.csv")
