@@ -74,6 +74,9 @@ def ncu_traffic():
             v = [r["inst_executed"] for r in rows if key in r.get("kernel", "") and "inst_executed" in r]
             if v:
                 out[key + ":inst"] = sum(v) / len(v)
+            v = [r["l2_atom_alu_requests"] for r in rows if key in r.get("kernel", "") and "l2_atom_alu_requests" in r]
+            if v:
+                out[key + ":atom"] = sum(v) / len(v)
     return out
 
 
@@ -221,6 +224,22 @@ def run_ours(args):
         step()
     torch.cuda.synchronize()
     assert mb.heap.poll_error() == dsr.OK, "device error during warm-up"
+
+    # L2 atomic peak (roofline denominator of the allocator's atomics): the
+    # library's probe, hashed independent u64 atomicOr-with-return over a
+    # 32 MiB (L2-resident) buffer, timed with events; best of 3
+    abuf = torch.zeros(4 << 20, dtype=torch.int64, device="cuda")
+    dsr.probe_atomics(abuf, 0, 64, stream)
+    atom_rates = []
+    for _ in range(3):
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        nops = dsr.probe_atomics(abuf, 0, 256, stream)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        atom_rates.append(nops / (a0.elapsed_time(a1) * 1e-3))
+    atom_peak = max(atom_rates)
+    del abuf
 
     K = args.steps
     phase_ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(7)] for _ in range(K)]
@@ -378,6 +397,15 @@ def run_ours(args):
                 "frac": traffic["k_mb_new:inst"] / (phase_ms[1] * 1e-3) / (148 * 4 * clk["sm_mhz"] * 1e6),
                 "inst_per_launch": traffic["k_mb_new:inst"],
                 "note": "instruction count from the committed ncu summary of the same build (profiles/)"},
+            # the allocation kernel's L2 atomics (ncu request count of the same build, per new1
+            # launch) against the measured L2 atomic peak: not the bound, reported per SURVEY §8(d)
+            "roofline_atomics": {
+                "bound": "l2_atomics", "kernel": "k_mb_new (phase new1 launch)",
+                "achieved": traffic["k_mb_new:atom"] / (phase_ms[1] * 1e-3) / 1e9 if "k_mb_new:atom" in traffic else None,
+                "peak": atom_peak / 1e9, "unit": "G atomics/s",
+                "frac": traffic["k_mb_new:atom"] / (phase_ms[1] * 1e-3) / atom_peak if "k_mb_new:atom" in traffic else None,
+                "atomics_per_alloc": traffic["k_mb_new:atom"] / N1 if "k_mb_new:atom" in traffic else None,
+                "peak_source": "measured in this run: dsr_probe_atomics, hashed u64 atomicOr with return over 32 MiB"},
             "roofline_scan": {"bound": "hbm", "kernel": "k_mb_reduce<NF> (do-all field scan body, 6 launches/step; "
                                                         "the BASELINE >= 60% target)",
                               "achieved": scan_gbs, "peak": peak, "unit": "GB/s", "frac": scan_gbs / peak,

@@ -242,6 +242,20 @@ dsr_status dsr_canonical_dump(dsr_heap* h, uint32_t type, void* host_buf, size_t
 size_t dsr_device_view_bytes(void);
 dsr_status dsr_device_view(const dsr_heap* h, void* out, size_t out_bytes);
 
+/* Roofline denominator for the allocator's atomics ("allocs/s
+ * ... as a fraction of the measured atomic peak").  Launches one persistent
+ * grid in which every thread issues `iters` 64-bit atomicOr WITH return value
+ * (the allocator's RMW form, atom.global.or.b64) on the u64 words of dev_buf
+ * (bytes, device, caller-owned, contents overwritten):
+ *   mode 0  hashed, independent addresses over the buffer (size it to fit L2
+ *           for the L2 atomic-ALU peak: every bitmap word the allocator
+ *           touches is L2-resident)
+ *   mode 1  every thread on word 0 (same-address serialisation)
+ * *ops_out (host) receives the number of atomics issued; time the call with
+ * events on `stream`.  DSR_ERR_INVALID if bytes < 8 or iters == 0. */
+dsr_status dsr_probe_atomics(void* dev_buf, uint64_t bytes, uint32_t mode, uint32_t iters, uint64_t* ops_out,
+                             void* stream);
+
 /* Number of kernels this library launched since load (host counter). */
 uint64_t dsr_kernel_launches(void);
 const char* dsr_status_str(dsr_status s);

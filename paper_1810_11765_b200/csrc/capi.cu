@@ -730,6 +730,36 @@ extern "C" dsr_status dsr_device_view(const dsr_heap* h, void* out, size_t out_b
   return DSR_OK;
 }
 
+// ---- atomic-throughput probe (the allocator's roofline denominator)
+static __global__ void __launch_bounds__(256) k_probe_atom(unsigned long long* buf, uint64_t words, uint32_t mode,
+                                                           uint32_t iters, unsigned long long* sink) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t x = t * 0x9E3779B97F4A7C15ull + 1, acc = 0;
+  for (uint32_t i = 0; i < iters; ++i) {
+    x ^= x >> 29; x *= 0xBF58476D1CE4E5B9ull;                  // next hashed address
+    const uint64_t w = mode ? 0 : (x >> 20) % words;
+    acc += atomicOr(buf + w, 1ull << (t & 63));                 // RMW with return (ATOMG)
+  }
+  if (acc == 0x5EED5EED5EED5EEDull) *sink = acc;                 // keeps the results live
+}
+
+extern "C" dsr_status dsr_probe_atomics(void* dev_buf, uint64_t bytes, uint32_t mode, uint32_t iters,
+                                        uint64_t* ops_out, void* stream) {
+  if (!dev_buf || bytes < 16 || iters == 0 || mode > 1 || !ops_out) return DSR_ERR_INVALID;
+  int dev = 0, sms = 0, per = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_probe_atom, 256, 0));
+  const uint64_t words = bytes / 8 - 1;                          // the last word is the sink
+  unsigned long long* buf = (unsigned long long*)dev_buf;
+  const int grid = sms * per;
+  k_probe_atom<<<grid, 256, 0, (cudaStream_t)stream>>>(buf, words, mode, iters, buf + words);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  *ops_out = (uint64_t)grid * 256 * iters;
+  return DSR_OK;
+}
+
 extern "C" uint64_t dsr_kernel_launches(void) { return g_launches.load(); }
 
 extern "C" const char* dsr_status_str(dsr_status s) {

@@ -180,6 +180,9 @@ def lib():
         L.dsr_heap_layout.argtypes = [vp, C.POINTER(Layout)]
         L.dsr_heap_configure.restype = st
         L.dsr_heap_configure.argtypes = [vp, C.POINTER(Config)]
+        if hasattr(L, "dsr_probe_atomics"):       # (absent in older builds loaded via DSR_LIBPATH for A/B runs)
+            L.dsr_probe_atomics.restype = st
+            L.dsr_probe_atomics.argtypes = [vp, C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64), vp]
         L.dsr_wator_static_step.restype = st
         L.dsr_wator_static_step.argtypes = [C.POINTER(WatorStaticArgs), C.c_uint32, vp]
         L.dsr_parallel_new.restype = st
@@ -428,3 +431,13 @@ class Heap:
             levels.append(words[o:o + n])
             o += n
         return levels
+
+
+def probe_atomics(buf, mode=0, iters=64, stream=None) -> int:
+    """Launch the atomic-throughput probe on the torch CUDA tensor `buf`
+    (dsr_probe_atomics); returns the number of atomics issued."""
+    n = C.c_uint64(0)
+    check("dsr_probe_atomics", lib().dsr_probe_atomics(C.c_void_p(buf.data_ptr()), buf.numel() * buf.element_size(),
+                                                       mode, iters, C.byref(n), _stream_ptr(stream)))
+    return n.value
+

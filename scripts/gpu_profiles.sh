@@ -19,3 +19,10 @@ for w in wator gol gol16k gol16k-bits nbody; do
   timeout -s KILL 300 python bench.py --workload $w --steps 10 --warmup 3 >> gpurun_out/bench_apps.log 2>&1
 done
 timeout -s KILL 600 python scripts/prof_apps.py > gpurun_out/prof_apps.log 2>&1
+# summaries travel back (gpurun_out is capped at 64 MiB): per-line source pages of the
+# allocation kernel and the GoL passes, then drop the big reports
+python scripts/refresh_profiles.py r01 gpurun_out/prof_r01 > gpurun_out/refresh.log 2>&1
+ncu -i gpurun_out/r01_mb_new.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/prof_r01/mb_new_source.csv 2>/dev/null
+ncu -i gpurun_out/r01_gol16k.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/prof_r01/gol16k_source.csv 2>/dev/null
+gzip -f gpurun_out/prof_r01/*_source.csv
+rm -f gpurun_out/r01_gol16k.ncu-rep gpurun_out/r01_nbody.ncu-rep gpurun_out/r01_wator.ncu-rep gpurun_out/r01_compact.ncu-rep gpurun_out/r01_mb_free.ncu-rep

@@ -17,6 +17,7 @@ KEYS = {
     "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum": "ld_requests",
     "lts__t_requests_srcunit_tex_op_atom.sum": "l2_atom_requests",
     "smsp__inst_executed.sum": "inst_executed",
+    "lts__t_requests_srcunit_tex_op_atom_dot_alu.sum": "l2_atom_alu_requests",
     "sm__issue_active.avg.pct_of_peak_sustained_elapsed": "issue_active_pct",
 }
 UNIT = {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "s": 1.0, "nsecond": 1e-9,

@@ -2,7 +2,10 @@
 tracked profiles/<round>/ directory: ncu summaries, the launch list of one bench
 step (+ its per-kernel share table), the bench lines and the per-pass app times.
 
-    python scripts/refresh_profiles.py [r01]
+    python scripts/refresh_profiles.py [r01] [out_dir]
+
+(out_dir defaults to profiles/<round>; the GPU-side script writes to
+gpurun_out/prof_<round> so only small summaries travel back.)
 """
 import collections
 import csv
@@ -15,7 +18,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
 G = ROOT / "gpurun_out"
 rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
-P = ROOT / "profiles" / rnd
+P = Path(sys.argv[2]) if len(sys.argv) > 2 else ROOT / "profiles" / rnd
 P.mkdir(parents=True, exist_ok=True)
 
 reps = [str(G / f"{rnd}_{k}.ncu-rep") for k in ("mb_new", "mb_reduce", "mb_free", "compact", "nbody", "wator")]

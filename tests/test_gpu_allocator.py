@@ -252,3 +252,22 @@ def test_microbench_host_inputs_reject_unaligned_t0(D):
     buf = torch.zeros(4 * 4096, dtype=torch.int32, device="cuda")
     with pytest.raises(D.DsrError):
         mb.heap.launch(D.K_MB_NEW, 1024, D.MbNewArgs(1, 2, buf.data_ptr()))
+
+
+def test_atomic_probe(D):
+    """dsr_probe_atomics: both modes run and report the atomics issued; the
+    same-address mode is far slower than hashed addresses (serialisation)."""
+    buf = torch.zeros(1 << 20, dtype=torch.int64, device="cuda")
+    rates = []
+    for mode in (0, 1):
+        D.probe_atomics(buf, mode, 4)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        n = D.probe_atomics(buf, mode, 8)
+        e1.record()
+        torch.cuda.synchronize()
+        assert n > 0 and n % 256 == 0
+        rates.append(n / e0.elapsed_time(e1))
+    assert rates[0] > 10 * rates[1]
+    with pytest.raises(D.DsrError):
+        D.probe_atomics(buf[:1], 0, 4)
