@@ -443,8 +443,24 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
   // same for every request would keep landing on the frontier of blocks its
   // neighbours in rotation space are filling (measured: 16 % fewer lookups,
   // new4 2.43 -> 2.06 ms).
+  // A warp whose last block is full (top bit) first tries a random other
+  // active block of that block's leaf container (one load of the leaf word
+  // instead of a top-down search; counts as a lookup attempt like the hint):
+  // finds per step 7.8 M -> 5.7 M, new4 1.96 -> 1.83 ms, GoL 16384^2
+  // 49.6 -> 44.4 ms/gen.
   const uint64_t who = warp_gid() ^ ((uint64_t)hint << 24);
-  hint = (hint & 0x80000000u) ? 0xFFFFFFFFu : hint;
+  uint32_t sib = 0xFFFFFFFFu;
+  if ((hint & 0x80000000u) && hint != 0xFFFFFFFFu) {
+    const uint32_t last = hint & 0x7FFFFFFFu;
+    if (last < h.M) {
+      const uint64_t lw = ld_relaxed(h.activebm[T].lvl[0] + (last >> 6)) & ~(1ull << (last & 63));
+      if (lw) {
+        const uint32_t r6 = (uint32_t)(rot_hash(h, who, 0x777) >> 40) & 63u;
+        sib = (last & ~63u) | nth_bit(lw, (r6 * (uint32_t)__popcll(lw)) >> 6);
+      }
+    }
+  }
+  hint = (hint & 0x80000000u) ? sib : hint;
   // SM-affine home ranges are an ablation (DSR_F_HOME_ROT): measured slower than
   // the hashed global rotation (all 64 warps of an SM pile onto the few active
   // blocks of its range) and it strands active blocks of other ranges near OOM.
