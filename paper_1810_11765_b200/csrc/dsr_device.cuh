@@ -414,6 +414,21 @@ __device__ __forceinline__ void block_free(const DevHeap& h, uint32_t T, uint32_
   }
 }
 
+// A random active block of T near `last` (same leaf word, else a random
+// non-empty leaf under the same level-1 word); 0xFFFFFFFF if none.  One or two
+// relaxed loads of active[T] instead of a top-down search.
+__device__ __forceinline__ uint32_t near_block(const DevHeap& h, uint32_t T, uint32_t last, uint64_t rr) {
+  if (last >= h.M) return 0xFFFFFFFFu;
+  const uint64_t lw = ld_relaxed(h.activebm[T].lvl[0] + (last >> 6)) & ~(1ull << (last & 63));
+  if (lw) return (last & ~63u) | nth_bit(lw, ((((uint32_t)(rr >> 40)) & 63u) * (uint32_t)__popcll(lw)) >> 6);
+  if (h.activebm[T].nlevels < 2) return 0xFFFFFFFFu;
+  const uint64_t l1 = ld_relaxed(h.activebm[T].lvl[1] + (last >> 12));
+  if (!l1) return 0xFFFFFFFFu;
+  const uint32_t li = ((last >> 12) << 6) | nth_bit(l1, ((((uint32_t)(rr >> 46)) & 63u) * (uint32_t)__popcll(l1)) >> 6);
+  const uint64_t w = ld_relaxed(h.activebm[T].lvl[0] + li);
+  return w ? (li << 6) | nth_bit(w, ((((uint32_t)(rr >> 52)) & 63u) * (uint32_t)__popcll(w)) >> 6) : 0xFFFFFFFFu;
+}
+
 // Alg. 1 for one coalesced request of `need` slots (leader lane only).
 // Returns the reserved slot mask (0 = OOM) and the block in *bid_out.
 // An "active block lookup attempt" (Fig. 11) fails when
@@ -451,24 +466,7 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
   // new4 1.96 -> 1.64 ms, GoL 16384^2 49.6 -> 44.4 ms/gen.
   const uint64_t who = warp_gid() ^ ((uint64_t)hint << 24);
   uint32_t sib = 0xFFFFFFFFu;
-  if ((hint & 0x80000000u) && hint != 0xFFFFFFFFu) {
-    const uint32_t last = hint & 0x7FFFFFFFu;
-    if (last < h.M) {
-      const uint64_t lw = ld_relaxed(h.activebm[T].lvl[0] + (last >> 6)) & ~(1ull << (last & 63));
-      const uint64_t rr = rot_hash(h, who, 0x777);
-      if (lw) {
-        const uint32_t r6 = (uint32_t)(rr >> 40) & 63u;
-        sib = (last & ~63u) | nth_bit(lw, (r6 * (uint32_t)__popcll(lw)) >> 6);
-      } else if (h.activebm[T].nlevels > 1) {                                  // none: a random leaf of its level-1 word
-        const uint64_t l1 = ld_relaxed(h.activebm[T].lvl[1] + (last >> 12));
-        if (l1) {
-          const uint32_t li = ((last >> 12) << 6) | nth_bit(l1, (((uint32_t)(rr >> 46) & 63u) * (uint32_t)__popcll(l1)) >> 6);
-          const uint64_t w = ld_relaxed(h.activebm[T].lvl[0] + li);
-          if (w) sib = (li << 6) | nth_bit(w, (((uint32_t)(rr >> 52) & 63u) * (uint32_t)__popcll(w)) >> 6);
-        }
-      }
-    }
-  }
+  if ((hint & 0x80000000u) && hint != 0xFFFFFFFFu) sib = near_block(h, T, hint & 0x7FFFFFFFu, rot_hash(h, who, 0x777));
   hint = (hint & 0x80000000u) ? sib : hint;
   // SM-affine home ranges are an ablation (DSR_F_HOME_ROT): measured slower than
   // the hashed global rotation (all 64 warps of an SM pile onto the few active
