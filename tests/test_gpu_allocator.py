@@ -271,3 +271,17 @@ def test_atomic_probe(D):
     assert rates[0] > 10 * rates[1]
     with pytest.raises(D.DsrError):
         D.probe_atomics(buf[:1], 0, 4)
+
+
+@pytest.mark.parametrize("n1,n2", [(0, 0), (1, 0), (3, 1), (5, 7), (33, 31)])
+def test_microbench_degenerate_sizes(D, O, n1, n2):
+    """Empty and tiny workloads (no object, one object, partial warps and
+    partial type groups) give the oracle's results and leave the heap empty."""
+    from paper_1810_11765_b200.microbench import Microbench
+    mb = Microbench(n1=n1, n2=n2, seed=9)
+    mb.step()
+    torch.cuda.synchronize()
+    assert np.array_equal(mb.results(), O.microbench(9, n1, n2)[0])
+    assert mb.heap.poll_error() == D.OK
+    assert [mb.heap.live_count(t) for t in range(3)] == [0, 0, 0]
+    assert mb.heap.check_invariants() == 0

@@ -214,3 +214,29 @@ def test_independent_heaps_on_concurrent_streams(P, O):
     assert np.array_equal(gk, k) and np.array_equal(ge, e) and np.array_equal(gn, n)
     assert np.array_equal(g.alive(), O.life_dense(a0, 30))
     assert w.heap.check_invariants() == 0 and g.heap.check_invariants() == 0
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 257])
+def test_nbody_tiny_and_ragged(P, O, n):
+    """Degenerate body counts: a single body (no force, no merge), a pair that
+    merges (placed within R), three bodies, and a count that leaves a ragged
+    tile (257 = 256 + 1): alive sets equal, positions at the BJ tolerance."""
+    from paper_1810_11765_b200 import inputs as I, nbody
+    st = I.nbody_init(n, seed=11)
+    if n == 2:                                     # inside R of each other: one absorbs the other
+        st["x"][1] = st["x"][0] + np.float32(0.004)
+        st["y"][1] = st["y"][0]
+    prm = dict(G=2e-9, dt=0.5, eps=0.01, R=0.02)
+    sim = nbody.NBody(st, merges=True, **prm)
+    sim.run(5)
+    got = sim.state()
+    want = O.nbody_run(st, merges=True, steps=5, **prm)
+    assert np.array_equal(got["alive"], want["alive"])
+    al = want["alive"] == 1
+    for k in ("x", "y"):
+        assert rel_pos_err(got[k][al], want[k][al]) <= 1e-4, k
+    if n == 2:
+        assert int(al.sum()) == 1
+    assert abs(float(got["m"][al].astype(np.float64).sum()) - float(st["m"].astype(np.float64).sum())) <= \
+        1e-5 * float(st["m"].astype(np.float64).sum())
+    assert sim.heap.check_invariants() == 0
