@@ -43,19 +43,23 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, profile: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, profile: bool = False, variant: str = "",
+          defines=()) -> Path:
     """profile=True: a second library, _build/libdsr_prof.so, compiled with
     -DDSR_PROFILE (request-level allocator counters; load it with
-    DSR_LIBPATH=... for scripts/prof_mb.py).  The product library has none."""
-    out = BUILD / "libdsr_prof.so" if profile else OUT
-    if not force and not profile and not _stale():
+    DSR_LIBPATH=... for scripts/prof_mb.py).  The product library has none.
+    variant/defines: an experiment build _build/libdsr_<variant>.so with extra
+    -D definitions (tuning sweeps through DSR_LIBPATH)."""
+    tag = "prof" if profile else variant
+    out = BUILD / f"libdsr_{tag}.so" if tag else OUT
+    if not force and not tag and not _stale():
         return OUT
     BUILD.mkdir(exist_ok=True)
     info = f'-DDSR_BUILD_INFO="sm_100a {_git_rev()} {time.strftime("%Y-%m-%d")}"'
-    extra = ["-DDSR_PROFILE"] if profile else []
+    extra = (["-DDSR_PROFILE"] if profile else []) + [f"-D{d}" for d in defines]
 
     def compile_one(src: str) -> Path:
-        obj = BUILD / (Path(src).stem + ("_prof" if profile else "") + ".o")
+        obj = BUILD / (Path(src).stem + (f"_{tag}" if tag else "") + ".o")
         cmd = [NVCC, *ARCH, *FLAGS, *extra, *PER_FILE.get(src, []), info, "-I", str(ROOT / "include"), "-c",
                str(CSRC / src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)

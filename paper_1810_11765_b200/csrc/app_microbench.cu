@@ -7,7 +7,13 @@
 namespace dsr {
 
 __constant__ uint32_t kMbType[4] = {0, 0, 1, 2};
-constexpr uint32_t kMbChunk = 8;   // warp work unit: 8 x 32 consecutive t   // [A, A, B, C][t & 3]
+#ifndef DSR_MB_CHUNK
+#define DSR_MB_CHUNK 8
+#endif
+#ifndef DSR_MB_MINB
+#define DSR_MB_MINB 8
+#endif
+constexpr uint32_t kMbChunk = DSR_MB_CHUNK;   // warp work unit: 8 x 32 consecutive t
 
 // ---- phase 1 / 4: user kernel, thread t does new [A,A,B,C][t&3] (device new)
 // (MINB CTAs x 256 threads per SM; latency-bound, so occupancy matters).  The
@@ -361,8 +367,8 @@ bool mb_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* a
           k_mb_new<true, 8><<<grid_for(c, n, k_mb_new<true, 8>), 256, 0, c.st>>>(c.h, n, ma);
         } else {
           if (cudaMemsetAsync(&c.h.ctrl[CTRL_WORK], 0, 8, c.st) != cudaSuccess) { *ok = 0; return true; }
-          if (ma.in) k_mb_new<false, 8, true><<<grid_for(c, n, k_mb_new<false, 8, true>), 256, 0, c.st>>>(c.h, n, ma);
-          else k_mb_new<false, 8><<<grid_for(c, n, k_mb_new<false, 8>), 256, 0, c.st>>>(c.h, n, ma);
+          if (ma.in) k_mb_new<false, DSR_MB_MINB, true><<<grid_for(c, n, k_mb_new<false, DSR_MB_MINB, true>), 256, 0, c.st>>>(c.h, n, ma);
+          else k_mb_new<false, DSR_MB_MINB><<<grid_for(c, n, k_mb_new<false, DSR_MB_MINB>), 256, 0, c.st>>>(c.h, n, ma);
         }
       }
       count_launch();

@@ -20,7 +20,10 @@
 namespace dsr {
 
 constexpr int kCompactThreads = 64;
-constexpr uint32_t kDoallChunk = 4;   // dynamic work unit of allocating passes: 4 x 32 elements per warp   // small CTAs: ~8 per SM at M = 4.6 M blocks (latency-bound)
+#ifndef DSR_DOALL_CHUNK
+#define DSR_DOALL_CHUNK 4
+#endif
+constexpr uint32_t kDoallChunk = DSR_DOALL_CHUNK;   // dynamic work unit of allocating passes: 4 x 32 elements per warp
 
 static __global__ void __launch_bounds__(kCompactThreads) k_compact(DevHeap h, uint32_t T, int snapshot) {
   __shared__ uint64_t s_word[kCompactThreads];
