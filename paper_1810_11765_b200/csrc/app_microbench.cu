@@ -8,12 +8,15 @@ namespace dsr {
 
 __constant__ uint32_t kMbType[4] = {0, 0, 1, 2};
 #ifndef DSR_MB_CHUNK
-#define DSR_MB_CHUNK 8
+#define DSR_MB_CHUNK 4
+#endif
+#ifndef DSR_MB_FREEODD_SNAP
+#define DSR_MB_FREEODD_SNAP 1
 #endif
 #ifndef DSR_MB_MINB
 #define DSR_MB_MINB 8
 #endif
-constexpr uint32_t kMbChunk = DSR_MB_CHUNK;   // warp work unit: 8 x 32 consecutive t
+constexpr uint32_t kMbChunk = DSR_MB_CHUNK;   // warp work unit: 4 x 32 consecutive t (sweep: 2/4/8/16 -> 4)
 
 // ---- phase 1 / 4: user kernel, thread t does new [A,A,B,C][t&3] (device new)
 // (MINB CTAs x 256 threads per SM; latency-bound, so occupancy matters).  The
@@ -306,7 +309,7 @@ struct InhSpawn {  // visits the pre-pass objects only, although it creates obje
 bool mb_method_info(uint32_t id, MethodInfo* mi) {
   switch (id) {
     case DSR_M_MB_REDUCE: *mi = {0, sizeof(dsr_mb_reduce_args)}; return true;
-    case DSR_M_MB_FREE_ODD: *mi = {1, 0}; return true;      // self-delete
+    case DSR_M_MB_FREE_ODD: *mi = {DSR_MB_FREEODD_SNAP, 0}; return true;      // self-delete
     case DSR_M_MB_FREE_ALL: *mi = {3, 0}; return true;      // frees whole blocks: blocked distribution
     case DSR_M_COLLECT: *mi = {0, sizeof(dsr_collect_args)}; return true;
     case DSR_M_INH_BUMP: case DSR_M_INH_SUM: *mi = {0, sizeof(dsr_inh_args)}; return true;

@@ -21,9 +21,9 @@ namespace dsr {
 
 constexpr int kCompactThreads = 64;
 #ifndef DSR_DOALL_CHUNK
-#define DSR_DOALL_CHUNK 4
+#define DSR_DOALL_CHUNK 2
 #endif
-constexpr uint32_t kDoallChunk = DSR_DOALL_CHUNK;   // dynamic work unit of allocating passes: 4 x 32 elements per warp
+constexpr uint32_t kDoallChunk = DSR_DOALL_CHUNK;   // dynamic work unit of allocating passes: 2 x 32 elements per warp (sweep 1/2/4/8 -> 2)
 
 static __global__ void __launch_bounds__(kCompactThreads) k_compact(DevHeap h, uint32_t T, int snapshot) {
   __shared__ uint64_t s_word[kCompactThreads];
