@@ -424,7 +424,8 @@ __global__ void __launch_bounds__(256) k_trim(DevHeap h, uint32_t T) {
       const uint32_t b = (uint32_t)(i * 64 + __ffsll((long long)w) - 1);
       w &= w - 1;
       if (h.alloc_bm[b] != pad) continue;                  // holds objects
-      if (block_invalidate(h, b)) {                        // quiescent: succeeds for an empty block
+      uint32_t t;
+      if (block_invalidate(h, b, &t)) {                    // quiescent: succeeds for an empty block (t == T)
         bm_clear(h.activebm[T], b);
         bm_clear(h.allocbm[T], b);
         bm_set(h.freebm, b);

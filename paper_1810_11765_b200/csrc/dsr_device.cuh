@@ -261,6 +261,27 @@ __device__ __forceinline__ void bm_clear_from(const DevBitmap& b, uint32_t l, ui
     pos >>= 6;
   }
 }
+// the rest of a level-0 bm_clear / bm_set whose blind first atomic returned `prev`
+__device__ __forceinline__ void bm_clear_finish(const DevBitmap& b, uint64_t pos, uint64_t prev) {
+  uint64_t* w = b.lvl[0] + (pos >> 6);
+  const uint64_t m = 1ull << (pos & 63);
+  uint32_t ns = 32;
+  while (!(prev & m)) {
+    backoff(ns);
+    if (ld_relaxed(w) & m) prev = atom_and(w, ~m);
+  }
+  if (prev == m && b.nlevels > 1) bm_clear_from(b, 1, pos >> 6);
+}
+__device__ __forceinline__ void bm_set_finish(const DevBitmap& b, uint64_t pos, uint64_t prev) {
+  uint64_t* w = b.lvl[0] + (pos >> 6);
+  const uint64_t m = 1ull << (pos & 63);
+  uint32_t ns = 32;
+  while (prev & m) {
+    backoff(ns);
+    if (!(ld_relaxed(w) & m)) prev = atom_or(w, m);
+  }
+  if (prev == 0 && b.nlevels > 1) bm_set_from(b, 1, pos >> 6);
+}
 __device__ __forceinline__ void bm_set(const DevBitmap& b, uint64_t pos) { bm_set_from(b, 0, pos); }
 __device__ __forceinline__ void bm_clear(const DevBitmap& b, uint64_t pos) { bm_clear_from(b, 0, pos); }
 
@@ -380,14 +401,15 @@ __device__ __forceinline__ uint64_t block_reserve(const DevHeap& h, uint32_t bid
 
 // Alg. 9 (iterative, footnote P:1077) with padding: succeeds iff every
 // non-padding bit was 0, i.e. before == pad(t).
-__device__ __forceinline__ bool block_invalidate(const DevHeap& h, uint32_t bid) {
+// *t_out: the block's type, read while we hold its invalidated bits.
+__device__ __forceinline__ bool block_invalidate(const DevHeap& h, uint32_t bid, uint32_t* t_out) {
   uint64_t* w = h.alloc_bm + bid;
   for (;;) {
     const uint64_t before = atom_or_acquire(w, ~0ull);
     if (before == ~0ull) return false;
     const uint32_t t = ld_relaxed_u8(h.type + bid) - 1u;   // fixed while we hold invalidated bits
     const uint64_t pad = h.types[t].pad;
-    if (before == pad) return true;
+    if (before == pad) { *t_out = t; return true; }
     stat_add(h, ST_INVFAIL, 1);
     const uint64_t before_rb = atom_and(w, before);         // rollback exactly our bits
     if (before_rb != ~0ull) bm_clear(h.activebm[t], bid);   // deferred deactivation
@@ -403,14 +425,21 @@ __device__ __forceinline__ void block_free(const DevHeap& h, uint32_t T, uint32_
   const bool first = before == ~0ull;
   const bool empty = (before & ~mask) == h.types[T].pad;
   if (first) bm_set(h.activebm[T], bid);
-  if (empty) {
-    if (block_invalidate(h, bid)) {
-      const uint32_t t = ld_relaxed_u8(h.type + bid) - 1u;
-      bm_clear(h.activebm[t], bid);
-      bm_clear(h.allocbm[t], bid);
-      bm_set(h.freebm, bid);
-      stat_add(h, ST_BFREES, 1);
-    }
+  uint32_t t;
+  if (empty && block_invalidate(h, bid, &t)) {
+    // Alg. 2 l.7-11: active[t].clear, allocated[t].clear, free.set -- three
+    // independent leaf words, so the three blind first atomics are in flight
+    // together; each then finishes (wrong-state retry, upward cascade) as in
+    // bm_clear / bm_set.  (One L2 round trip instead of three, plus the type
+    // read that block_invalidate already did.)
+    const uint64_t m = 1ull << (bid & 63);
+    const uint64_t pa = atom_and(h.activebm[t].lvl[0] + (bid >> 6), ~m);
+    const uint64_t pl = atom_and(h.allocbm[t].lvl[0] + (bid >> 6), ~m);
+    const uint64_t pf = atom_or(h.freebm.lvl[0] + (bid >> 6), m);
+    bm_clear_finish(h.activebm[t], bid, pa);
+    bm_clear_finish(h.allocbm[t], bid, pl);
+    bm_set_finish(h.freebm, bid, pf);
+    stat_add(h, ST_BFREES, 1);
   }
 }
 
@@ -513,8 +542,13 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
         continue;
       }
       init_block(h, T, (uint32_t)bid);
-      bm_set(h.allocbm[T], (uint64_t)bid);
-      bm_set(h.activebm[T], (uint64_t)bid);
+      {                                                                       // allocated[T].set, active[T].set:
+        const uint64_t m = 1ull << (bid & 63);                                // both blind atomics in flight together
+        const uint64_t pl = atom_or(h.allocbm[T].lvl[0] + (bid >> 6), m);
+        const uint64_t pa = atom_or(h.activebm[T].lvl[0] + (bid >> 6), m);
+        bm_set_finish(h.allocbm[T], (uint64_t)bid, pl);
+        bm_set_finish(h.activebm[T], (uint64_t)bid, pa);
+      }
       stat_add(h, ST_INITS, 1);
       if (prof) stat_add(h, ST_CYC_SLOW, clock64() - c1);
       fresh = true;
