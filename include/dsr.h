@@ -272,10 +272,18 @@ const char* dsr_build_info(void);
  * types: 0 = A{3 x u32}, 1 = B{4 x u32}, 2 = C{6 x u32} */
 /* thread t -> new [A,A,B,C][(t0+t)&3].  in == NULL: field k of thread t's
  * object = low32(key(seed, 0, MB_FIELD, 16t + k)) computed on the device.
- * in != NULL (device pointer, t0 % 4 == 0): the field values come from the
- * caller, packed per 4 threads as 16 u32 = {A: 3, A: 3, B: 4, C: 6 fields},
- * i.e. thread t0 + i reads in[16 (i / 4) + {0, 3, 6, 10}[i % 4] + k]. */
-typedef struct { uint64_t seed; uint64_t t0; const uint32_t* in; } dsr_mb_new_args;
+ * in != NULL (t0 % 4 == 0): the field values come from the caller, packed per
+ * 4 threads as 16 u32 = {A: 3, A: 3, B: 4, C: 6 fields}, i.e. thread t0 + i
+ * reads in[16 (i / 4) + {0, 3, 6, 10}[i % 4] + k]; ceil(n / 4) groups.
+ *   in_host == 0: `in` is a device pointer.
+ *   in_host != 0: `in` is a HOST pointer (pinned for asynchronous copies).
+ *     dsr_launch copies it into one of two heap-owned device staging buffers
+ *     on the heap's own copy stream (waiting until the kernel that last read
+ *     that buffer has finished) and makes `stream` wait for the copy, so the
+ *     copy of one launch overlaps the work already queued on `stream`.  The
+ *     host buffer must stay valid until the copy completes (stream-ordered:
+ *     synchronise `stream` before reusing it). */
+typedef struct { uint64_t seed; uint64_t t0; const uint32_t* in; uint32_t in_host; uint32_t pad_; } dsr_mb_new_args;
 typedef struct { uint64_t* out3; } dsr_mb_reduce_args;           /* out3[0..2] += (count, sum, xor) */
 enum {
   DSR_K_MB_NEW = 1,          /* args dsr_mb_new_args; fields k = low32(key(seed,0,MB_FIELD,16t+k)) or from `in` */

@@ -364,7 +364,7 @@ bool mb_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* a
       {
         const dsr_mb_new_args& ma = *(const dsr_mb_new_args*)args;
         // (__launch_bounds__ minimum 8 / 6 / 4 CTAs per SM measured equal: 9.2-9.6 ms)
-        if (ma.in && (ma.t0 & 3)) { *ok = 0; return true; }
+        if (ma.in && ((ma.t0 & 3) || ma.in_host)) { *ok = 0; return true; }   // host inputs are staged by dsr_launch
         if (c.h.flags & DSR_F_CTA_NEW) {
           if (ma.in) { *ok = 0; return true; }
           k_mb_new<true, 8><<<grid_for(c, n, k_mb_new<true, 8>), 256, 0, c.st>>>(c.h, n, ma);

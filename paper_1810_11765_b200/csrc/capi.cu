@@ -39,6 +39,21 @@ struct dsr_heap {
   DevHeap dev;
   int device;
   int sms;
+  // host-input staging (dsr_mb_new_args.in_host): two device buffers used
+  // alternately, filled on a copy stream; `used` = the last kernel reading it
+  void* stage[2] = {nullptr, nullptr};
+  size_t stage_cap[2] = {0, 0};
+  cudaEvent_t ready[2] = {nullptr, nullptr}, used[2] = {nullptr, nullptr};
+  cudaStream_t cstream = nullptr;
+  int stage_next = 0;
+  ~dsr_heap() {
+    for (int k = 0; k < 2; ++k) {
+      if (stage[k]) cudaFree(stage[k]);
+      if (ready[k]) cudaEventDestroy(ready[k]);
+      if (used[k]) cudaEventDestroy(used[k]);
+    }
+    if (cstream) cudaStreamDestroy(cstream);
+  }
 };
 
 #define CUDA_TRY(x)                                         \
@@ -384,12 +399,53 @@ extern "C" dsr_status dsr_parallel_new(dsr_heap* h, uint32_t type, uint64_t n, u
   return DSR_OK;
 }
 
+// dsr_mb_new_args.in_host: stage the caller's host array into a device buffer
+// on the heap's copy stream; `launch_stream` waits for it (see dsr.h)
+static dsr_status stage_host_input(dsr_heap* h, uint64_t n, dsr_mb_new_args* a, cudaStream_t st) {
+  const size_t bytes = (size_t)64 * ((n + 3) / 4);
+  const int k = h->stage_next;
+  h->stage_next ^= 1;
+  if (!h->cstream) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
+    for (int j = 0; j < 2; ++j) {
+      CUDA_TRY(cudaEventCreateWithFlags(&h->ready[j], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&h->used[j], cudaEventDisableTiming));
+    }
+  }
+  if (h->stage_cap[k] < bytes) {                      // grow (first use): wait for the buffer's last reader
+    CUDA_TRY(cudaEventSynchronize(h->used[k]));
+    if (h->stage[k]) CUDA_TRY(cudaFree(h->stage[k]));
+    h->stage[k] = nullptr;
+    h->stage_cap[k] = 0;
+    CUDA_TRY(cudaMalloc(&h->stage[k], bytes));
+    h->stage_cap[k] = bytes;
+  }
+  CUDA_TRY(cudaStreamWaitEvent(h->cstream, h->used[k], 0));
+  CUDA_TRY(cudaMemcpyAsync(h->stage[k], a->in, bytes, cudaMemcpyHostToDevice, h->cstream));
+  CUDA_TRY(cudaEventRecord(h->ready[k], h->cstream));
+  CUDA_TRY(cudaStreamWaitEvent(st, h->ready[k], 0));
+  a->in = (const uint32_t*)h->stage[k];
+  a->in_host = 0;
+  return DSR_OK;
+}
+
 extern "C" dsr_status dsr_launch(dsr_heap* h, uint32_t kernel_id, uint64_t n, const void* args, size_t args_bytes,
                                  void* stream) {
   if (!h || !args) return DSR_ERR_INVALID;
   if (n == 0) return DSR_OK;
   LaunchCtx c = ctx(h, stream);
   int ok = 1;
+  dsr_mb_new_args staged;
+  int stage_slot = -1;
+  if (kernel_id == DSR_K_MB_NEW && args_bytes == sizeof(dsr_mb_new_args) &&
+      ((const dsr_mb_new_args*)args)->in && ((const dsr_mb_new_args*)args)->in_host) {
+    staged = *(const dsr_mb_new_args*)args;
+    if (staged.t0 & 3) return DSR_ERR_INVALID;
+    stage_slot = h->stage_next;
+    dsr_status s = stage_host_input(h, n, &staged, c.st);
+    if (s != DSR_OK) return s;
+    args = &staged;
+  }
   bool known = mb_kernel_launch(kernel_id, c, n, args, args_bytes, &ok) ||
                gol_kernel_launch(kernel_id, c, n, args, args_bytes, &ok) ||
                wt_kernel_launch(kernel_id, c, n, args, args_bytes, &ok) ||
@@ -397,6 +453,7 @@ extern "C" dsr_status dsr_launch(dsr_heap* h, uint32_t kernel_id, uint64_t n, co
   if (!known) return DSR_ERR_UNSUPPORTED;
   if (!ok) return DSR_ERR_INVALID;
   CUDA_TRY(cudaGetLastError());
+  if (stage_slot >= 0) CUDA_TRY(cudaEventRecord(h->used[stage_slot], c.st));   // the staging buffer's reader
   return DSR_OK;
 }
 

@@ -90,7 +90,8 @@ class Counters(C.Structure):
 
 # ---- argument structs (mirror include/dsr.h)
 class MbNewArgs(C.Structure):
-    _fields_ = [("seed", C.c_uint64), ("t0", C.c_uint64), ("in_", C.c_void_p)]
+    _fields_ = [("seed", C.c_uint64), ("t0", C.c_uint64), ("in_", C.c_void_p), ("in_host", C.c_uint32),
+                ("pad_", C.c_uint32)]
 
 
 class MbReduceArgs(C.Structure):

@@ -36,13 +36,14 @@ class Microbench:
     def _reduce_args(self, k):
         return dsr.MbReduceArgs(self.out.data_ptr() + 8 * k)
 
-    def step(self, stream=None, events=None, body_events=None, inputs=None, before_new4=None):
+    def step(self, stream=None, events=None, body_events=None, inputs=None, before_new4=None, host_inputs=False):
         """One pass of the whole hot path: heap init, new 2^26, reduce, free odd,
         new 2^25, reduce, drain.  `events`: optional list of 7 torch.cuda.Event
         pairs recorded around the phases; `body_events`: 6 pairs around the
         reduce bodies (k_mb_reduce) of phases 2 and 5 (timing only).  `inputs`:
         optional (in1, in2) device pointers to the field values of the phase-1 /
-        phase-4 objects (inputs.mb_fields layout) instead of device-computed keys;
+        phase-4 objects (inputs.mb_fields layout) instead of device-computed keys
+        (host pointers with host_inputs=True: the library stages them, dsr.h);
         `before_new4`: called (host side) just before phase 4 is enqueued."""
         h = self.heap
         s = stream if stream is not None else self.stream
@@ -71,7 +72,7 @@ class Microbench:
             for t, cnt in enumerate(self._counts(0, self.n1)):
                 h.reserve_blocks(t, int(-(-cnt // self.heap.cap[t]) * (1.0 + self.reserve_slack)), s)
         in1, in2 = inputs if inputs is not None else (None, None)
-        h.launch(dsr.K_MB_NEW, self.n1, dsr.MbNewArgs(self.seed, 0, in1), s)
+        h.launch(dsr.K_MB_NEW, self.n1, dsr.MbNewArgs(self.seed, 0, in1, int(bool(host_inputs))), s)
         if self.reserve:
             for t in range(3):
                 h.trim(t, s)
@@ -86,7 +87,7 @@ class Microbench:
         ev(3, 1)
         if before_new4 is not None:
             before_new4()
-        ev(4, 0); h.launch(dsr.K_MB_NEW, self.n2, dsr.MbNewArgs(self.seed, self.n1, in2), s); ev(4, 1)
+        ev(4, 0); h.launch(dsr.K_MB_NEW, self.n2, dsr.MbNewArgs(self.seed, self.n1, in2, int(bool(host_inputs))), s); ev(4, 1)
         ev(5, 0)
         for t in range(3):
             reduce(t, 9 + 3 * t, 3 + t)

@@ -230,19 +230,25 @@ def test_microbench_variants_match_oracle(D, O, reserve, flags):
     assert mb.heap.check_invariants() == 0
 
 
-@pytest.mark.parametrize("n1,n2", [(1 << 16, 1 << 15), (400_000, 123_456)])
-def test_microbench_host_inputs_match_oracle(D, O, n1, n2):
-    """The end-to-end form of the step (bench.py e2e): field values copied from
-    host-resident arrays (inputs.mb_fields) instead of computed on the device;
-    same results as the oracle.  n2 not a multiple of 4 is padded by the caller."""
+@pytest.mark.parametrize("host", [False, True])
+@pytest.mark.parametrize("n1,n2", [(1 << 16, 1 << 15), (400_000, 123_458)])
+def test_microbench_host_inputs_match_oracle(D, O, n1, n2, host):
+    """The end-to-end form of the step (bench.py e2e): field values from
+    caller arrays (inputs.mb_fields) instead of device-computed keys -- device
+    arrays, or HOST arrays that dsr_launch stages through its copy stream and
+    two alternating device buffers (three steps reuse them); same results as
+    the oracle.  n2 not a multiple of 4: the caller passes ceil(n/4) groups."""
     from paper_1810_11765_b200 import inputs as I
     from paper_1810_11765_b200.microbench import Microbench
-    f1 = torch.from_numpy(I.mb_fields(1, 0, n1).view(np.int32)).cuda()
-    f2 = torch.from_numpy(I.mb_fields(1, n1, -(-n2 // 4) * 4).view(np.int32)).cuda()
+    f1 = torch.from_numpy(I.mb_fields(1, 0, n1).view(np.int32))
+    f2 = torch.from_numpy(I.mb_fields(1, n1, -(-n2 // 4) * 4).view(np.int32))
+    f1, f2 = (f1.pin_memory(), f2.pin_memory()) if host else (f1.cuda(), f2.cuda())
     mb = Microbench(n1=n1, n2=n2, seed=1)
-    mb.step(inputs=(f1.data_ptr(), f2.data_ptr()))
-    torch.cuda.synchronize()
-    assert np.array_equal(mb.results(), O.microbench(1, n1, n2)[0])
+    want = O.microbench(1, n1, n2)[0]
+    for _ in range(3 if host else 1):
+        mb.step(inputs=(f1.data_ptr(), f2.data_ptr()), host_inputs=host)
+        torch.cuda.synchronize()
+        assert np.array_equal(mb.results(), want)
     assert mb.heap.check_invariants() == 0
 
 
