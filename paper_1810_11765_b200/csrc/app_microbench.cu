@@ -132,14 +132,15 @@ struct MbFreeOdd {
   struct Args { uint64_t unused; };
   DSR_NO_ACC
   static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args&, Acc&) {
-    if (*field_ptr<uint32_t>(h, T, 0, b, s) & 1u) dsr_destroy(h, make_handle(T, h.types[T].cap, b, s));
+    // read-only, and the destroy is control-dependent on the read: no release needed
+    if (*field_ptr<uint32_t>(h, T, 0, b, s) & 1u) dsr_destroy_ro(h, make_handle(T, h.types[T].cap, b, s));
   }
 };
 struct MbFreeAll {
   struct Args { uint64_t unused; };
   DSR_NO_ACC
   static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args&, Acc&) {
-    dsr_destroy(h, make_handle(T, h.types[T].cap, b, s));
+    dsr_destroy_ro(h, make_handle(T, h.types[T].cap, b, s));   // never reads or writes the object
   }
 };
 // handle collection (tests): out[atomic++] = this

@@ -102,6 +102,12 @@ __device__ __forceinline__ uint64_t atom_or_acquire(uint64_t* p, uint64_t m) {
   asm volatile("atom.acquire.gpu.global.or.b64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(m) : "memory");
   return old;
 }
+// relaxed RMW that is also a compiler barrier (dsr_destroy_ro)
+__device__ __forceinline__ uint64_t atom_and_relaxed(uint64_t* p, uint64_t m) {
+  uint64_t old;
+  asm volatile("atom.relaxed.gpu.global.and.b64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(m) : "memory");
+  return old;
+}
 // release: earlier reads / writes of the freed objects are ordered before the RMW
 __device__ __forceinline__ uint64_t atom_and_release(uint64_t* p, uint64_t m) {
   uint64_t old;
@@ -420,8 +426,10 @@ __device__ __forceinline__ bool block_invalidate(const DevHeap& h, uint32_t bid,
 // Alg. 7 + Alg. 2 for a mask of slots of one block of type T (coalesced free).
 // FIRST iff before == ~0; EMPTY iff the remaining bits are padding only;
 // both at once: activate, then invalidate (reading R-FIRSTEMPTY / C17).
+// RELEASE = false: the relaxed form for dsr_destroy_ro (no fence).
+template <bool RELEASE = true>
 __device__ __forceinline__ void block_free(const DevHeap& h, uint32_t T, uint32_t bid, uint64_t mask) {
-  const uint64_t before = atom_and_release(h.alloc_bm + bid, ~mask);
+  const uint64_t before = RELEASE ? atom_and_release(h.alloc_bm + bid, ~mask) : atom_and_relaxed(h.alloc_bm + bid, ~mask);
   const bool first = before == ~0ull;
   const bool empty = (before & ~mask) == h.types[T].pad;
   if (first) bm_set(h.activebm[T], bid);
@@ -678,7 +686,9 @@ __device__ __forceinline__ uint64_t dsr_new_bulk(const DevHeap& h, uint32_t T, b
 
 // Device destroy: lanes freeing slots of the same block combine their
 // bits into one atomicAnd (coalesced version of Alg. 7).
-__device__ __forceinline__ void dsr_destroy(const DevHeap& h, uint64_t x) {
+// RELEASE = false is dsr_destroy_ro below.
+template <bool RELEASE = true>
+__device__ __forceinline__ void dsr_destroy_t(const DevHeap& h, uint64_t x) {
   if (x == 0) return;
   const uint32_t lane = lane_id();
   const uint32_t act = __activemask();
@@ -691,9 +701,17 @@ __device__ __forceinline__ void dsr_destroy(const DevHeap& h, uint64_t x) {
   __syncwarp(peers);   // memory ordering among the lanes: their object accesses precede the leader's release
   if (lane == leader) {
     const uint64_t mask = ((uint64_t)hi << 32) | lo;
-    block_free(h, h_type(x), h_bid(x), mask);
+    block_free<RELEASE>(h, h_type(x), h_bid(x), mask);
     stat_add(h, ST_FREES, __popcll(mask));
   }
 }
+__device__ __forceinline__ void dsr_destroy(const DevHeap& h, uint64_t x) { dsr_destroy_t<true>(h, x); }
+// Destroy without the release fence (atom.release compiles to MEMBAR.ALL.GPU +
+// ATOMG; ncu showed the fence as the free passes' second stall reason).  Only
+// for callers whose lanes have NOT written the object since they last
+// synchronised with other threads, and whose reads of it are all consumed
+// (the call is data- or control-dependent on them, or there are none): then
+// nothing of theirs can be reordered past the slot's reuse.
+__device__ __forceinline__ void dsr_destroy_ro(const DevHeap& h, uint64_t x) { dsr_destroy_t<false>(h, x); }
 
 }  // namespace dsr
