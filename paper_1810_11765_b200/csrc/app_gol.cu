@@ -148,7 +148,8 @@ struct GolCandUpdate {    // pass 3 (allocates Alive)
     const uint8_t act = *field_ptr<uint8_t>(h, T, 1, b, s);
     if (act == ACT_NONE) return;
     const uint32_t c = *field_ptr<uint32_t>(h, T, 0, b, s);
-    dsr_destroy(h, make_handle(T, h.types[T].cap, b, s));
+    // never written; act is consumed by the branch, c by the handle (after_load)
+    dsr_destroy_ro(h, after_load(make_handle(T, h.types[T].cap, b, s), c));
     if (act == ACT_SPAWN) a.cell[c] = new_alive(h, c, 1);
     else a.cell[c] = 0;
     if (act == ACT_SPAWN && a.bits) gol_bit_set(a, c, true);
@@ -168,7 +169,7 @@ struct GolAliveUpdate {   // pass 4 (allocates Candidate)
         if (ld_relaxed((const uint64_t*)pe) == 0 && atomicCAS(pe, 0ull, kReserved) == 0ull) todo |= 1u << d;
       }
     } else if (*field_ptr<uint8_t>(h, T, 2, b, s) == ACT_DIE) {
-      dsr_destroy(h, make_handle(T, h.types[T].cap, b, s));
+      dsr_destroy_ro(h, after_load(make_handle(T, h.types[T].cap, b, s), c));   // read-only, c consumed
       if (a.bits) gol_bit_set(a, c, false);
       todo = 1u << 8;
     }

@@ -713,5 +713,9 @@ __device__ __forceinline__ void dsr_destroy(const DevHeap& h, uint64_t x) { dsr_
 // (the call is data- or control-dependent on them, or there are none): then
 // nothing of theirs can be reordered past the slot's reuse.
 __device__ __forceinline__ void dsr_destroy_ro(const DevHeap& h, uint64_t x) { dsr_destroy_t<false>(h, x); }
+// x, made data-dependent on v (a value loaded from the object that is used
+// after a dsr_destroy_ro): v never equals 0xFFFFFFFF at the call sites (a cell
+// id), so the result is x, but the destroy cannot issue before v has arrived.
+__device__ __forceinline__ uint64_t after_load(uint64_t x, uint32_t v) { return x | (v == 0xFFFFFFFFu ? 1ull : 0ull); }
 
 }  // namespace dsr
