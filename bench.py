@@ -510,13 +510,67 @@ def run_app(args):
         cfg = {"workload": "nbody with merging (BASELINE configs[2]) 65536 bodies", "pairs_per_step": 2 * 65536 ** 2,
                "pair_interactions_per_s": 2 * 65536 ** 2 / (ms * 1e-3),
                "parallelism": f"{world} id-range shards, NCCL all-gather of snapshot chunks" if world > 1 else "1 GPU"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = app_cpu_baseline(args.workload)
+        except Exception as e:   # the line must still print
+            cpu = {"value": None, "unit": "object-updates/s", "cores": 1, "kind": "oracle", "sample": f"failed: {e}"}
     if rank == 0:
+        if cpu is not None:
+            cfg["cpu_baseline"] = cpu
         print(json.dumps({"metric": METRIC, "value": visits / K / (ms * 1e-3), "unit": "object-updates/s",
                           "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms, "higher_is_better": True,
                           "scaling": "strong", "dtype": "u32" if args.workload != "nbody" else "f32",
                           "data": "synthetic", "config": cfg}), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def app_cpu_baseline(workload):
+    """The oracle (plain C, one core) on a bounded prefix of the same app
+    workload, in object-updates/s counted the way the GPU line counts them
+    (the runs are identical, so the object counts are the same)."""
+    import numpy as np
+    from oracle import oracle as O
+    from paper_1810_11765_b200 import inputs as I
+    O.build()
+    if workload == "wator":
+        kind, egg, en = I.wator_init(2048, 2048, seed=42)
+        S = 10
+        t0 = time.perf_counter()
+        _, _, _, c = O.wator_run(kind, egg, en, FB=6, SB=12, SS=6, seed=42, steps=S)
+        t = time.perf_counter() - t0
+        agents = [int((kind != 0).sum())] + [int(c[i, 0] + c[i, 1]) for i in range(S - 1)]
+        visits = 4 * 2048 * 2048 * S + 2 * sum(agents)
+        sample = f"first {S} steps of the 2048^2 run (object oracle), {t:.1f} s"
+    elif workload in ("gol", "gol16k", "gol16k-bits"):
+        Wd = 64 if workload == "gol" else 16384
+        a0 = I.gol_soup(Wd, Wd, 0.3 if Wd == 64 else 0.25, 1 if Wd == 64 else 42)
+        if Wd > 64:                  # bounded sample: one quadrant of the same soup, as its own torus
+            a0 = np.ascontiguousarray(a0[:Wd // 2, :Wd // 2])
+        G = 100 if Wd == 64 else 1
+        t0 = time.perf_counter()
+        O.gol_run(a0, G)
+        t = time.perf_counter() - t0
+        visits = 0
+        a = a0
+        for g in range(G):      # objects at each generation's start: alive + dead cells next to an alive one
+            n = sum(np.roll(np.roll(a, dy, 0), dx, 1) for dy in (-1, 0, 1) for dx in (-1, 0, 1)) - a
+            visits += 2 * (int(a.sum()) + int(((a == 0) & (n > 0)).sum()))
+            if g + 1 < G:
+                a = O.life_dense(a, 1)
+        sample = (f"first {G} generation(s) of the {a0.shape[0]}^2 " + ("run" if Wd == 64 else "quadrant of the same soup")
+                  + f" (object oracle), {t:.1f} s")
+    else:
+        n = 32768                    # bounded sample: half the bodies (a quarter of the pairs)
+        st = I.nbody_init(n, seed=7)
+        t0 = time.perf_counter()
+        O.nbody_run(st, merges=True, steps=1, **I.NBODY_PARAMS)
+        t = time.perf_counter() - t0
+        visits = 8 * n
+        sample = f"one step of {n} bodies (oracle: fp32 state, fp64 arithmetic; {n * n / t:.3g} pairs/s), {t:.1f} s"
+    return {"value": visits / t, "unit": "object-updates/s", "cores": 1, "kind": "oracle", "sample": sample}
 
 
 def main():
