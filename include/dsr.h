@@ -93,6 +93,7 @@ typedef struct {
 #define DSR_F_NO_HINT     0x10u /* no per-warp block hint: every request searches active[T] (paper-exact, replay) */
 #define DSR_F_CTA_NEW     0x20u /* bulk constructors use CTA-level instead of warp-level request coalescing (microbench new kernel only) */
 #define DSR_F_HOME_ROT    0x40u /* ablation: SM-affine rotation (searches start in the SM's range of level-1 containers) */
+#define DSR_F_SLOT_ROTATE 0x80u /* paper: also rotate a block's object bitmap before choosing its free slots; off by default */
 
 typedef struct {
   uint32_t active_retries;   /* r: try_find_set attempts before the slow path (Fig. 11); 0 -> 5 */

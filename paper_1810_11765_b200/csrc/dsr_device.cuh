@@ -563,7 +563,11 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
     }
     uint64_t before = 0;
     long long c2 = prof ? clock64() : 0;
-    const uint32_t rot = (uint32_t)(rh >> 58);
+    // Slots inside the block: the lowest free ones by default; the paper also
+    // rotates here (DSR_F_SLOT_ROTATE).  With per-warp hints a block
+    // has mostly one filler, and unrotated reservations are contiguous runs
+    // (cheap n-th-bit, coalesced constructor stores): new1 4.75 -> 3.87 ms.
+    const uint32_t rot = (h.flags & DSR_F_SLOT_ROTATE) ? (uint32_t)(rh >> 58) : 0u;
     // A fresh block's word is known (no read).  (A "blind" first atomicOr on
     // found blocks, assuming them empty, was measured 1.5x slower: partial
     // fills doubled the number of requests.)

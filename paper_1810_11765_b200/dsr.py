@@ -20,8 +20,8 @@ MAX_TYPES, MAX_FIELDS, MAX_LEVELS = 8, 16, 6
 # status codes
 OK, ERR_INVALID, ERR_OOM, ERR_CUDA, ERR_RETRY_BUDGET, ERR_INVARIANT, ERR_UNSUPPORTED = range(7)
 # flags
-F_NO_ROTATE, F_NO_COALESCE, F_STATS, F_SPIN_ON_OOM, F_NO_HINT, F_CTA_NEW, F_HOME_ROT = (0x1, 0x2, 0x4, 0x8, 0x10, 0x20,
-                                                                                   0x40)
+F_NO_ROTATE, F_NO_COALESCE, F_STATS, F_SPIN_ON_OOM, F_NO_HINT, F_CTA_NEW, F_HOME_ROT, F_SLOT_ROTATE = (
+    0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40, 0x80)
 
 # ids (mirror include/dsr.h)
 K_MB_NEW, M_MB_REDUCE, M_MB_FREE_ODD, M_MB_FREE_ALL = 1, 1, 2, 3

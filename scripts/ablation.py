@@ -16,7 +16,7 @@ import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-FLAGS = {"default": 0, "NoShift": 0x1, "NoCoal": 0x2, "NoCoal-NoShift": 0x3, "NoHint": 0x10}
+FLAGS = {"default": 0, "NoShift": 0x1, "NoCoal": 0x2, "NoCoal-NoShift": 0x3, "NoHint": 0x10, "SlotRotate": 0x80}
 
 
 def agent_frag(heap, types):
@@ -118,13 +118,13 @@ def runs():
         return [("wator", {"name": n, "flags": FLAGS[n], "r": 5, **hb}) for n in ("NoShift", "NoCoal-NoShift")
                 for hb in ({}, {"heap_bytes": 4 << 30})]
     out = []
-    for name in ["default", "NoShift", "NoCoal", "NoCoal-NoShift", "NoHint"]:
+    for name in ["default", "NoShift", "NoCoal", "NoCoal-NoShift", "NoHint", "SlotRotate"]:
         out.append(("mb", {"name": name, "flags": FLAGS[name], "r": 5, "reserve": True}))
-    out.append(("mb", {"name": "paper-exact (NoHint, no reserve)", "flags": 0x10, "r": 5, "reserve": False}))
+    out.append(("mb", {"name": "paper-exact (NoHint, SlotRotate, no reserve)", "flags": 0x90, "r": 5, "reserve": False}))
     out.append(("mb", {"name": "default, no reserve", "flags": 0, "r": 5, "reserve": False}))
     for r in [1, 2, 3, 8]:
         out.append(("mb", {"name": f"r={r}", "flags": 0, "r": r, "reserve": True}))
-    for name in ["default", "NoShift", "NoCoal", "NoCoal-NoShift", "NoHint"]:
+    for name in ["default", "NoShift", "NoCoal", "NoCoal-NoShift", "NoHint", "SlotRotate"]:
         out.append(("wator", {"name": name, "flags": FLAGS[name], "r": 5}))
     for r in [1, 2, 3, 8]:
         out.append(("wator", {"name": f"r={r}", "flags": 0, "r": r}))
