@@ -8,7 +8,7 @@ namespace dsr {
 
 __constant__ uint32_t kMbType[4] = {0, 0, 1, 2};
 #ifndef DSR_MB_CHUNK
-#define DSR_MB_CHUNK 4
+#define DSR_MB_CHUNK 2
 #endif
 #ifndef DSR_MB_FREEODD_SNAP
 #define DSR_MB_FREEODD_SNAP 1
@@ -16,7 +16,7 @@ __constant__ uint32_t kMbType[4] = {0, 0, 1, 2};
 #ifndef DSR_MB_MINB
 #define DSR_MB_MINB 8
 #endif
-constexpr uint32_t kMbChunk = DSR_MB_CHUNK;   // warp work unit: 4 x 32 consecutive t (sweep: 2/4/8/16 -> 4)
+constexpr uint32_t kMbChunk = DSR_MB_CHUNK;   // warp work unit: 2 x 32 consecutive t (sweeps: 2/4/8/16)
 
 // ---- phase 1 / 4: user kernel, thread t does new [A,A,B,C][t&3] (device new)
 // (MINB CTAs x 256 threads per SM; latency-bound, so occupancy matters).  The
