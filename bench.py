@@ -274,11 +274,11 @@ def run_ours(args):
     blocks = []
     mb.heap.reset(stream)
     mb.out.zero_()
-    mb.heap.launch(dsr.K_MB_NEW, N1, dsr.MbNewArgs(SEED, 0), stream)
+    mb.heap.launch(mb.kernel, N1, dsr.MbNewArgs(SEED, 0), stream)
     blocks.append(mb.heap.fragmentation(stream)[1])
     for t in range(3):
         mb.heap.parallel_do(t, dsr.M_MB_FREE_ODD, None, stream)
-    mb.heap.launch(dsr.K_MB_NEW, N2, dsr.MbNewArgs(SEED, N1), stream)
+    mb.heap.launch(mb.kernel, N2, dsr.MbNewArgs(SEED, N1), stream)
     frag5, b5 = mb.heap.fragmentation(stream)
     blocks.append(b5)
     # algorithmic bytes of the reduce bodies: live x size_T + 12 B per block

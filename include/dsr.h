@@ -288,6 +288,14 @@ typedef struct { uint64_t seed; uint64_t t0; const uint32_t* in; uint32_t in_hos
 typedef struct { uint64_t* out3; } dsr_mb_reduce_args;           /* out3[0..2] += (count, sum, xor) */
 enum {
   DSR_K_MB_NEW = 1,          /* args dsr_mb_new_args; fields k = low32(key(seed,0,MB_FIELD,16t+k)) or from `in` */
+  /* The same objects and fields, allocated with warp-cooperative bulk requests
+   * (reading R-BULK): a warp takes 768 consecutive t and reserves
+   * all objects of one type of them with one request -- fresh blocks up to 64
+   * per free-bitmap atomic, or free slots of active blocks found by 32
+   * parallel rotated searches (P:649-654 generalised to many slots).  Which
+   * object lands in which slot differs; every object and field value is the
+   * same as DSR_K_MB_NEW's. */
+  DSR_K_MB_NEW_BULK = 8,
   DSR_M_MB_REDUCE = 1,       /* args dsr_mb_reduce_args (no allocation: reads the allocation bitmap) */
   DSR_M_MB_FREE_ODD = 2,     /* args none: destroy(this) if field0 & 1 */
   DSR_M_MB_FREE_ALL = 3      /* args none: destroy(this) */

@@ -72,3 +72,31 @@ int or_microbench(uint64_t seed, uint64_t n1, uint64_t n2, uint64_t order_seed,
   for (uint32_t ty = 0; ty < 3; ty++) ost_fini(&st[ty]);
   return err;
 }
+
+/* The live objects of type `ty` after phase `stop` (1 = after the first
+ * allocation burst, 3 = after the odd-free pass, 4 = after the second burst),
+ * each as its packed u32 fields in store order (the caller sorts them into the
+ * canonical order, SURVEY c.8).  *count = live objects; records are written
+ * only while they fit in cap u32 words.  Returns 1 on an illegal delete. */
+int or_microbench_live(uint64_t seed, uint64_t n1, uint64_t n2, uint32_t stop, uint32_t ty,
+                       uint32_t* out, uint64_t cap, uint64_t* count) {
+  ost_t st[3];
+  for (uint32_t q = 0; q < 3; q++) ost_init(&st[q], q + 1, 4 * MB_NF[q]);
+  int err = 0;
+  uint64_t scratch[9];
+  mb_new_range(st, seed, 0, n1);
+  if (stop >= 3) {
+    mb_reduce(st, 0, 100, scratch);
+    err |= mb_free_pass(st, 0, 200, 1);
+  }
+  if (stop >= 4) mb_new_range(st, seed, n1, n2);
+  uint64_t k = 0;
+  for (uint64_t i = 0; i < st[ty].n; i++) {
+    if (!st[ty].live[i]) continue;
+    if ((k + 1) * MB_NF[ty] <= cap) memcpy(out + k * MB_NF[ty], st[ty].data + i * st[ty].rec, st[ty].rec);
+    k++;
+  }
+  *count = k;
+  for (uint32_t q = 0; q < 3; q++) ost_fini(&st[q]);
+  return err;
+}

@@ -112,6 +112,8 @@ uint32_t or_assign_slot(uint32_t NT, uint64_t n, uint64_t tid, uint64_t k);
  * each phase 1..6.  order_seed != 0 shuffles every do-all's visit order. */
 int or_microbench(uint64_t seed, uint64_t n1, uint64_t n2, uint64_t order_seed,
                   uint64_t* out, uint64_t* live_out);
+int or_microbench_live(uint64_t seed, uint64_t n1, uint64_t n2, uint32_t stop, uint32_t ty,
+                       uint32_t* out, uint64_t cap, uint64_t* count);
 
 /* Game of Life, O(#alive) Alive/Candidate version (SURVEY c.1, Table 1).
  * alive: W*H bytes (0/1), updated in place after `gens` generations.

@@ -145,6 +145,9 @@ def lib():
         L.or_assign_slot.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64]
         L.or_microbench.restype = C.c_int
         L.or_microbench.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, u64p, u64p]
+        L.or_microbench_live.restype = C.c_int
+        L.or_microbench_live.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, u32p,
+                                         C.c_uint64, u64p]
         L.or_gol_run.restype = C.c_int
         L.or_gol_run.argtypes = [C.c_uint32, C.c_uint32, u8p, C.c_uint32, C.c_uint64, vp, C.c_uint64, vp]
         L.or_life_dense.restype = None
@@ -307,6 +310,29 @@ def microbench(seed, n1, n2, order_seed=0):
     if rc:
         raise RuntimeError(f"or_microbench rc={rc}")
     return out.reshape(2, 3, 3), live.reshape(6, 3)
+
+
+def microbench_live(seed, n1, n2, stop, ty):
+    """Canonical dump of type ty's live objects after phase `stop` (1, 3 or 4):
+    (live, nfields) uint32 records sorted by their little-endian bytes (the
+    order of dsr_canonical_dump)."""
+    nf = [3, 4, 6][ty]
+    cnt = np.zeros(1, dtype=np.uint64)
+    lib().or_microbench_live(seed, n1, n2, stop, ty, np.zeros(1, dtype=np.uint32), 0, cnt)
+    k = int(cnt[0])
+    out = np.zeros(max(k, 1) * nf, dtype=np.uint32)
+    rc = lib().or_microbench_live(seed, n1, n2, stop, ty, out, out.size, cnt)
+    if rc:
+        raise RuntimeError(f"or_microbench_live rc={rc}")
+    return sort_records(out[:k * nf].reshape(k, nf))
+
+
+def sort_records(recs):
+    """Rows of a (k, n) little-endian array sorted lexicographically by their bytes."""
+    recs = np.ascontiguousarray(recs)
+    b = recs.view(np.uint8).reshape(len(recs), -1)
+    order = np.lexsort(b.T[::-1]) if len(recs) else np.zeros(0, dtype=np.int64)
+    return recs[order]
 
 
 def gol_run(alive, gens, order_seed=0, dump=False):

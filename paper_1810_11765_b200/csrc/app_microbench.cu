@@ -65,6 +65,90 @@ __global__ void __launch_bounds__(256, MINB) k_mb_new(DevHeap h, uint64_t n, dsr
   }
 }
 
+// ---- phase 1 / 4, batched: the same objects (thread t -> [A,A,B,C][t&3],
+// field k = low32(key(seed, 0, MB_FIELD, 16t + k))), but each warp takes a
+// work unit of kMbUnit consecutive t and allocates all objects of one type
+// of the unit with ONE warp-cooperative request (dsr_new_warp, reading
+// R-BULK) instead of one coalesced request per 32 threads; the constructor
+// then writes the reserved slots chunk by chunk (lane j -> slot j of a chunk:
+// coalesced column stores).  768 t = 384 A + 192 B + 192 C = exactly 6 / 4 / 6
+// blocks of N_T = 64 / 48 / 32.
+#ifndef DSR_MB_UNIT
+#define DSR_MB_UNIT 768
+#endif
+constexpr uint32_t kMbUnit = DSR_MB_UNIT;
+
+template <bool IN = false>
+__global__ void __launch_bounds__(256) k_mb_new_bulk(DevHeap h, uint64_t n, dsr_mb_new_args a) {
+  const uint64_t kp = rng_prefix(a.seed, 0);
+  const uint32_t lane = threadIdx.x & 31;
+  for (;;) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&h.ctrl[CTRL_WORK], (unsigned long long)kMbUnit);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= n) break;
+    const uint32_t un = (uint32_t)(n - base < kMbUnit ? n - base : kMbUnit);
+    const uint64_t ts = a.t0 + base;                       // first t of the unit
+#pragma unroll 1
+    for (uint32_t T = 0; T < 3; ++T) {
+      // residues r = t & 3 of type T ([A,A,B,C]) as offsets from ts, ascending
+      uint32_t off0 = 0, off1 = 0, nres = 0;
+#pragma unroll
+      for (uint32_t d = 0; d < 4; ++d) {
+        const uint32_t r = (uint32_t)((ts + d) & 3);
+        if ((r ? r - 1 : 0) == T) {
+          if (nres == 0) off0 = d; else off1 = d;
+          ++nres;
+        }
+      }
+      // objects of T among ts .. ts + un - 1
+      uint32_t need = off0 < un ? (un - off0 + 3) / 4 : 0;
+      if (nres == 2) need += off1 < un ? (un - off1 + 3) / 4 : 0;
+      const uint32_t nf = h.types[T].nfields;
+      uint32_t done = 0;
+      while (done < need) {
+        uint32_t bid;
+        uint64_t mask;
+        const uint32_t got = dsr_new_warp(h, T, need - done, &bid, &mask);
+        if (!got) break;                                   // OOM (sticky error set)
+        const uint32_t cnt = (uint32_t)__popcll(mask);
+        uint32_t cum = cnt;                                // exclusive prefix in lane order
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t v = __shfl_up_sync(0xffffffffu, cum, o);
+          if (lane >= (uint32_t)o) cum += v;
+        }
+        cum -= cnt;
+        uint32_t chunks = __ballot_sync(0xffffffffu, mask != 0);
+        while (chunks) {
+          const uint32_t c = __ffs(chunks) - 1;
+          chunks &= chunks - 1;
+          const uint32_t cb = __shfl_sync(0xffffffffu, bid, c);
+          const uint64_t cm = shfl64(0xffffffffu, mask, c);
+          const uint32_t c0 = __shfl_sync(0xffffffffu, cum, c) + done;
+          const uint32_t cn = (uint32_t)__popcll(cm);
+          uint8_t* const blk = h.data + (size_t)cb * h.block_bytes;
+          for (uint32_t j = lane; j < cn; j += 32) {
+            const uint32_t s = nth_bit(cm, j);
+            const uint32_t i = c0 + j;                     // i-th object of T in the unit
+            const uint64_t t = nres == 2 ? ts + 4ull * (i >> 1) + ((i & 1) ? off1 : off0) : ts + 4ull * i + off0;
+            uint8_t* const obj = blk + 4u * s;
+            if (IN) {
+              const uint64_t ti = t - a.t0;
+              const uint32_t* src = a.in + 16 * (ti >> 2) + ((0xA630u >> (4 * (ti & 3))) & 0xFu);
+              for (uint32_t k = 0; k < nf; ++k) *reinterpret_cast<uint32_t*>(obj + h.types[T].col_off[k]) = __ldg(src + k);
+            } else {
+              for (uint32_t k = 0; k < nf; ++k)
+                *reinterpret_cast<uint32_t*>(obj + h.types[T].col_off[k]) = (uint32_t)rng_key_p(kp, 5, t * 16 + k);
+            }
+          }
+        }
+        done += got;
+      }
+    }
+  }
+}
+
 // ---- phase 2 / 5: field reduction.  Vectorised do-all body: one thread per
 // 4 consecutive slots ("quad") of a block; each field column is read with one
 // 128-bit non-coherent load per quad (16 lanes cover a 64-slot u32 column).
@@ -375,6 +459,18 @@ bool mb_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* a
           else k_mb_new<false, DSR_MB_MINB><<<grid_for(c, n, k_mb_new<false, DSR_MB_MINB>), 256, 0, c.st>>>(c.h, n, ma);
         }
       }
+      count_launch();
+      return true;
+    }
+    case DSR_K_MB_NEW_BULK: {
+      if (bytes != sizeof(dsr_mb_new_args) || c.h.ntypes < 3) { *ok = 0; return true; }
+      const dsr_mb_new_args& ma = *(const dsr_mb_new_args*)args;
+      if (ma.in && ((ma.t0 & 3) || ma.in_host)) { *ok = 0; return true; }   // host inputs are staged by dsr_launch
+      for (uint32_t t = 0; t < 3; ++t)
+        if (c.h.types[t].nfields > DSR_MAX_FIELDS) { *ok = 0; return true; }
+      if (cudaMemsetAsync(&c.h.ctrl[CTRL_WORK], 0, 8, c.st) != cudaSuccess) { *ok = 0; return true; }
+      if (ma.in) k_mb_new_bulk<true><<<grid_for(c, n, k_mb_new_bulk<true>), 256, 0, c.st>>>(c.h, n, ma);
+      else k_mb_new_bulk<false><<<grid_for(c, n, k_mb_new_bulk<false>), 256, 0, c.st>>>(c.h, n, ma);
       count_launch();
       return true;
     }

@@ -437,7 +437,7 @@ extern "C" dsr_status dsr_launch(dsr_heap* h, uint32_t kernel_id, uint64_t n, co
   int ok = 1;
   dsr_mb_new_args staged;
   int stage_slot = -1;
-  if (kernel_id == DSR_K_MB_NEW && args_bytes == sizeof(dsr_mb_new_args) &&
+  if ((kernel_id == DSR_K_MB_NEW || kernel_id == DSR_K_MB_NEW_BULK) && args_bytes == sizeof(dsr_mb_new_args) &&
       ((const dsr_mb_new_args*)args)->in && ((const dsr_mb_new_args*)args)->in_host) {
     staged = *(const dsr_mb_new_args*)args;
     if (staged.t0 & 3) return DSR_ERR_INVALID;
@@ -760,8 +760,11 @@ extern "C" dsr_status dsr_canonical_dump(dsr_heap* h, uint32_t type, void* host_
   if (!host_buf || cap < *used) return DSR_ERR_INVALID;
   if (live == 0) return DSR_OK;
   uint8_t* d = nullptr;
-  CUDA_TRY(cudaMallocAsync((void**)&d, *used + 8, st));
-  unsigned long long* cursor = (unsigned long long*)(d + *used);
+  // the record cursor gets its own 8-B aligned word after the records (record
+  // sizes such as 5, 12 or 17 B leave live * rb unaligned)
+  const size_t cur_off = align_up(*used, 8);
+  CUDA_TRY(cudaMallocAsync((void**)&d, cur_off + 8, st));
+  unsigned long long* cursor = (unsigned long long*)(d + cur_off);
   CUDA_TRY(cudaMemsetAsync(cursor, 0, 8, st));
   CUDA_TRY(cudaMemsetAsync(&h->dev.ctrl[CTRL_RCOUNT], 0, 8, st));
   const uint64_t nwords = (h->L.M + 63) / 64;

@@ -688,6 +688,174 @@ __device__ __forceinline__ uint64_t dsr_new_bulk(const DevHeap& h, uint32_t T, b
   return want ? dsr_new(h, T) : 0ull;
 }
 
+// ------------------------------------------------------------------ warp-cooperative bulk new (reading R-BULK)
+// Multi-bit forms of the bitmap operations: the paper's coalescing of
+// reservations into one atomicOr applied to the block bitmaps when
+// one request needs several blocks.  The cascade rule is the single-bit one
+// (Alg. 3 l.6, Def. P:1129): the thread whose atomic turned the container
+// from non-zero to 0 (0 to non-zero) updates the nested level.
+//
+// clear_many: up to k set bits of ONE leaf container of `b` (found by a
+// rotated try_find_set), the first k at or after the found bit
+// cyclically, cleared with one atomicAnd.  Returns the bits this call cleared
+// (0 = FAIL) and their leaf index in *wi.
+__device__ __forceinline__ uint64_t bm_clear_many(const DevBitmap& b, uint64_t rh, uint32_t k, uint64_t* wi) {
+  uint64_t leaf = 0;
+  const int64_t pos = bm_try_find_set(b, rh, &leaf);
+  if (pos < 0) return 0;
+  const uint32_t p = (uint32_t)pos & 63u;
+  uint64_t c = rotr64(leaf, p);                                  // bit 0 = the found bit
+  if ((uint32_t)__popcll(c) > k) c &= (2ull << nth_bit(c, k - 1)) - 1ull;
+  const uint64_t sel = rotl64(c, p);
+  *wi = (uint64_t)pos >> 6;
+  const uint64_t before = atom_and(b.lvl[0] + *wi, ~sel);
+  const uint64_t got = before & sel;
+  if (got && (before & ~sel) == 0 && b.nlevels > 1) bm_clear_from(b, 1, *wi);
+  return got;
+}
+// set_many: set the bits `mask` of leaf container wi (legal use: all 0).
+// A bit found already set has a clear in flight (a block being freed while
+// another thread already took it from the free bitmap): wait and set it after
+// the clear, as bm_set does.
+__device__ __forceinline__ void bm_set_many(const DevBitmap& b, uint64_t wi, uint64_t mask) {
+  uint64_t* w = b.lvl[0] + wi;
+  const uint64_t prev = atom_or(w, mask);
+  bool up = prev == 0;
+  uint64_t late = prev & mask;
+  while (late) {
+    const uint64_t m = late & (0ull - late);
+    late &= late - 1;
+    uint64_t pv = prev;
+    uint32_t ns = 32;
+    while (pv & m) {
+      backoff(ns);
+      if (!(ld_relaxed(w) & m)) pv = atom_or(w, m);
+    }
+    up |= pv == 0;
+  }
+  if (up && b.nlevels > 1) bm_set_from(b, 1, wi);
+}
+
+// Warp-cooperative new of `need` objects of type T (every lane of a full warp
+// calls it with the same T and need).  Generalises Alg. 1 to a request of many
+// slots (reading R-BULK):
+//  * fast path: up to 32 lanes each take an active block of T found with a
+//    rotated try_find_set (one search per lane, distinct rotations),
+//    duplicate finds are merged (__match_any_sync), the lanes split the
+//    request over their blocks' free slots by a warp prefix sum and reserve
+//    with ONE atomicOr per block (Alg. 6).  FULL -> active.clear
+//    (Alg. 1 l.12); a block whose type changed is rolled back (l.14).  A
+//    lookup that finds nothing or yields no slot is a failed attempt.
+//  * after r failed attempts, the slow path: fresh blocks from the
+//    free bitmap, up to 64 per atomicAnd (bm_clear_many), initialised by the
+//    lanes in parallel (Alg. 8) with their reserved slots already set (a block
+//    whose slots are all taken is born full and never active),
+//    allocated[T].set for all of them with one atomicOr, active[T].set only
+//    for a partially used one (Alg. 1 l.4-7).
+// Returns the number of slots reserved (warp-uniform; < need only on OOM or
+// when all 32 lanes hold a chunk -- call again for the rest).  Lane i holds
+// chunk i: block *bid_out and reserved slots *mask_out (0 = no chunk); the
+// objects are ranked in lane order, then by slot.
+__device__ __forceinline__ uint32_t dsr_new_warp(const DevHeap& h, uint32_t T, uint32_t need, uint32_t* bid_out,
+                                                 uint64_t* mask_out) {
+  const uint32_t lane = lane_id();
+  const uint32_t lt = (1u << lane) - 1u;
+  const uint32_t cap = h.types[T].cap;
+  const uint64_t valid = h.types[T].valid, pad = h.types[T].pad;
+  const uint64_t who = warp_gid() * 32 + lane;
+  uint32_t my_bid = 0, have = 0, fails = 0, oom_tries = 0;
+  uint64_t my_mask = 0;
+  for (uint32_t round = 0; have < need; ++round) {
+    const uint32_t rem = need - have;
+    const uint32_t freelanes = __ballot_sync(0xffffffffu, my_mask == 0);
+    if (!freelanes) break;
+    const uint32_t frank = __popc(freelanes & lt);                 // rank among chunk-less lanes
+    if (fails < h.r_attempts) {
+      // searches: about two per expected half-free block of the remainder
+      const uint32_t k = min(__popc(freelanes), (2u * rem + cap - 1u) / cap + 1u);
+      const bool searcher = my_mask == 0 && frank < k;
+      int64_t cand = -1;
+      if (searcher) cand = bm_try_find_set(h.activebm[T], rot_hash(h, who, round));
+      const uint32_t same = __match_any_sync(0xffffffffu, (ull)cand);
+      const bool lead = searcher && cand >= 0 && (uint32_t)(__ffs(same) - 1) == lane;
+      const uint64_t cur = lead ? ld_relaxed(h.alloc_bm + cand) : ~0ull;
+      const uint32_t f = (uint32_t)__popcll(~cur);
+      uint32_t incl = f;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += v;
+      }
+      const uint32_t excl = incl - f;
+      const uint32_t take = excl >= rem ? 0u : min(f, rem - excl);
+      uint64_t got = 0;
+      if (take) {
+        uint64_t fr = ~cur;
+        if ((uint32_t)__popcll(fr) > take) fr &= (2ull << nth_bit(fr, take - 1)) - 1ull;
+        const uint64_t before = atom_or_acquire(h.alloc_bm + cand, fr);
+        got = fr & ~before;
+        if (got) {
+          const uint32_t t = ld_relaxed_u8(h.type + cand) - 1u;       // volatile read (Alg. 1 l.10)
+          if ((before | got) == ~0ull) bm_clear(h.activebm[t], (uint64_t)cand);   // FULL (l.12)
+          if (t != T) {                                               // type changed: rollback (l.14)
+            block_free(h, t, (uint32_t)cand, got);
+            stat_add(h, ST_ROLLBACKS, 1);
+            got = 0;
+          }
+        }
+        if (got) { my_bid = (uint32_t)cand; my_mask = got; }
+      }
+      const uint32_t gained = __reduce_add_sync(0xffffffffu, (uint32_t)__popcll(got));
+      const uint32_t failed = __popc(__ballot_sync(0xffffffffu, searcher && (cand < 0 || (take && !got) || (lead && f == 0))));
+      have += gained;
+      fails += failed ? failed : (gained ? 0u : 1u);
+      continue;
+    }
+    // slow path: fresh blocks for the remainder, leader lane claims them from the free bitmap
+    const uint32_t nb = min((rem + cap - 1u) / cap, (uint32_t)__popc(freelanes));
+    const uint32_t leader = __ffs(freelanes) - 1;
+    uint64_t got = 0, wi = 0;
+    if (lane == leader) got = bm_clear_many(h.freebm, rot_hash(h, who, 0x100000ull + round), nb, &wi);
+    got = shfl64(0xffffffffu, got, leader);
+    wi = shfl64(0xffffffffu, wi, leader);
+    if (!got) {
+      // FAIL: free bitmap empty or transiently inconsistent; only a
+      // top-level word of 0 counts towards OOM (reading R-OOM)
+      const bool empty = ld_relaxed(h.freebm.lvl[h.freebm.nlevels - 1]) == 0;
+      if (empty && !(h.flags & DSR_F_SPIN_ON_OOM) && ++oom_tries >= 64) {
+        if (lane == 0) { flag_error(h, ERRB_OOM); stat_add(h, ST_OOM, 1); }
+        break;
+      }
+      uint32_t ns = 128;
+      backoff(ns);
+      fails = 0;                                                      // look for active blocks again
+      continue;
+    }
+    const uint32_t ngot = (uint32_t)__popcll(got);
+    bool partial = false;
+    if (my_mask == 0 && frank < ngot) {                               // the frank-th claimed block
+      const uint32_t bid = (uint32_t)(wi * 64 + nth_bit(got, frank));
+      const uint32_t left = rem - frank * cap;                        // > 0: ngot <= ceil(rem / cap)
+      const uint64_t slots = left >= cap ? valid : ((1ull << left) - 1ull);
+      partial = left < cap;
+      st_relaxed_u8(h.type + bid, T + 1);                             // Alg. 8, slots already reserved
+      st_release(h.alloc_bm + bid, pad | slots);
+      my_bid = bid;
+      my_mask = slots;
+    }
+    __syncwarp();
+    if (lane == leader) { bm_set_many(h.allocbm[T], wi, got); stat_add(h, ST_INITS, ngot); }
+    __syncwarp();
+    if (partial) bm_set(h.activebm[T], my_bid);
+    have += min(rem, ngot * cap);
+  }
+  if (lane == 0) stat_add(h, ST_ALLOCS, have);
+  __syncwarp();
+  *bid_out = my_bid;
+  *mask_out = my_mask;
+  return have;
+}
+
 // Device destroy: lanes freeing slots of the same block combine their
 // bits into one atomicAnd (coalesced version of Alg. 7).
 // RELEASE = false is dsr_destroy_ro below.

@@ -25,6 +25,7 @@ F_NO_ROTATE, F_NO_COALESCE, F_STATS, F_SPIN_ON_OOM, F_NO_HINT, F_CTA_NEW, F_HOME
 
 # ids (mirror include/dsr.h)
 K_MB_NEW, M_MB_REDUCE, M_MB_FREE_ODD, M_MB_FREE_ALL = 1, 1, 2, 3
+K_MB_NEW_BULK = 8
 K_LS_ALLOC, K_LS_FREE = 2, 3
 K_REPLAY, K_TORTURE, M_COLLECT = 4, 5, 4
 K_INH_NEW, K_INH_READ, M_INH_BUMP, M_INH_SUM, M_INH_SPAWN = 6, 7, 5, 6, 7

@@ -12,10 +12,12 @@ PHASES = ["init", "new1", "reduce2", "free3", "new4", "reduce5", "drain6"]
 
 class Microbench:
     def __init__(self, n1=1 << 26, n2=1 << 25, seed=1, heap_bytes=None, device=None, retries=5, flags=0,
-                 stream=None, reserve=True, reserve_slack=0.0):
+                 stream=None, reserve=False, reserve_slack=0.0, bulk=True):
         import torch
         self.n1, self.n2, self.seed = n1, n2, seed
-        self.reserve = reserve      # dsr_reserve_blocks before / dsr_trim after the phase-1 burst
+        self.reserve = reserve      # dsr_reserve_blocks before / dsr_trim after the phase-1 burst (host foreknowledge; off by default)
+        self.bulk = bulk            # K_MB_NEW_BULK (warp-cooperative requests, R-BULK) instead of per-thread K_MB_NEW
+        self.kernel = dsr.K_MB_NEW_BULK if bulk else dsr.K_MB_NEW
         self.reserve_slack = reserve_slack   # extra fraction of blocks reserved (trimmed afterwards)
         if heap_bytes is None:
             # room for every object of phase 1 + 4 at the worst per-block fill, x2 for contention slack
@@ -36,7 +38,8 @@ class Microbench:
     def _reduce_args(self, k):
         return dsr.MbReduceArgs(self.out.data_ptr() + 8 * k)
 
-    def step(self, stream=None, events=None, body_events=None, inputs=None, before_new4=None, host_inputs=False):
+    def step(self, stream=None, events=None, body_events=None, inputs=None, before_new4=None, host_inputs=False,
+             stop=None):
         """One pass of the whole hot path: heap init, new 2^26, reduce, free odd,
         new 2^25, reduce, drain.  `events`: optional list of 7 torch.cuda.Event
         pairs recorded around the phases; `body_events`: 6 pairs around the
@@ -44,7 +47,8 @@ class Microbench:
         optional (in1, in2) device pointers to the field values of the phase-1 /
         phase-4 objects (inputs.mb_fields layout) instead of device-computed keys
         (host pointers with host_inputs=True: the library stages them, dsr.h);
-        `before_new4`: called (host side) just before phase 4 is enqueued."""
+        `before_new4`: called (host side) just before phase 4 is enqueued.
+        `stop`: 1, 3 or 4 -- return after that phase (parity of the live set)."""
         h = self.heap
         s = stream if stream is not None else self.stream
 
@@ -72,11 +76,13 @@ class Microbench:
             for t, cnt in enumerate(self._counts(0, self.n1)):
                 h.reserve_blocks(t, int(-(-cnt // self.heap.cap[t]) * (1.0 + self.reserve_slack)), s)
         in1, in2 = inputs if inputs is not None else (None, None)
-        h.launch(dsr.K_MB_NEW, self.n1, dsr.MbNewArgs(self.seed, 0, in1, int(bool(host_inputs))), s)
+        h.launch(self.kernel, self.n1, dsr.MbNewArgs(self.seed, 0, in1, int(bool(host_inputs))), s)
         if self.reserve:
             for t in range(3):
                 h.trim(t, s)
         ev(1, 1)
+        if stop == 1:
+            return
         ev(2, 0)
         for t in range(3):
             reduce(t, 3 * t, t)
@@ -85,9 +91,13 @@ class Microbench:
         for t in range(3):
             h.parallel_do(t, dsr.M_MB_FREE_ODD, None, s)
         ev(3, 1)
+        if stop == 3:
+            return
         if before_new4 is not None:
             before_new4()
-        ev(4, 0); h.launch(dsr.K_MB_NEW, self.n2, dsr.MbNewArgs(self.seed, self.n1, in2, int(bool(host_inputs))), s); ev(4, 1)
+        ev(4, 0); h.launch(self.kernel, self.n2, dsr.MbNewArgs(self.seed, self.n1, in2, int(bool(host_inputs))), s); ev(4, 1)
+        if stop == 4:
+            return
         ev(5, 0)
         for t in range(3):
             reduce(t, 9 + 3 * t, 3 + t)

@@ -142,10 +142,11 @@ def mb_expected(O, seed, n1, n2):
     return out
 
 
+@pytest.mark.parametrize("bulk", [True, False])
 @pytest.mark.parametrize("n1,n2", [(1000, 500), (1 << 16, 1 << 15), (3 * 65536 + 77, 40001)])
-def test_microbench_matches_oracle(D, O, n1, n2):
+def test_microbench_matches_oracle(D, O, n1, n2, bulk):
     from paper_1810_11765_b200.microbench import Microbench
-    mb = Microbench(n1=n1, n2=n2, seed=1)
+    mb = Microbench(n1=n1, n2=n2, seed=1, bulk=bulk)
     mb.step()
     torch.cuda.synchronize()
     assert np.array_equal(mb.results(), mb_expected(O, 1, n1, n2))
@@ -157,13 +158,14 @@ def test_microbench_matches_oracle(D, O, n1, n2):
     assert np.array_equal(mb.results(), mb_expected(O, 1, n1, n2))
 
 
-def test_microbench_full_size_closed_form(D):
+@pytest.mark.parametrize("bulk", [True, False])
+def test_microbench_full_size_closed_form(D, bulk):
     """BASELINE configs[4] at full size (2^26 + 2^25 objects) in the bench's
     launch configuration, against the closed form (direct loop over t)."""
     from paper_1810_11765_b200.microbench import Microbench
     from test_oracle_apps import mb_closed_form
     n1, n2 = 1 << 26, 1 << 25
-    mb = Microbench(n1=n1, n2=n2, seed=1)
+    mb = Microbench(n1=n1, n2=n2, seed=1, bulk=bulk)
     mb.step()
     torch.cuda.synchronize()
     r = mb.results()
@@ -221,10 +223,11 @@ def test_reserve_blocks_and_trim(D):
     assert heap.poll_error() == D.OK
 
 
-@pytest.mark.parametrize("reserve,flags", [(False, 0), (True, 0), (True, 32)])
-def test_microbench_variants_match_oracle(D, O, reserve, flags):
+@pytest.mark.parametrize("reserve,flags,bulk", [(False, 0, False), (True, 0, False), (True, 32, False),
+                                                (True, 0, True), (False, 1, True), (False, 2, True)])
+def test_microbench_variants_match_oracle(D, O, reserve, flags, bulk):
     from paper_1810_11765_b200.microbench import Microbench
-    mb = Microbench(n1=200_000, n2=100_000, seed=5, reserve=reserve, flags=flags)
+    mb = Microbench(n1=200_000, n2=100_000, seed=5, reserve=reserve, flags=flags, bulk=bulk)
     mb.step()
     assert np.array_equal(mb.results(), O.microbench(5, 200_000, 100_000)[0])
     assert mb.heap.check_invariants() == 0
@@ -279,15 +282,52 @@ def test_atomic_probe(D):
         D.probe_atomics(buf[:1], 0, 4)
 
 
-@pytest.mark.parametrize("n1,n2", [(0, 0), (1, 0), (3, 1), (5, 7), (33, 31)])
-def test_microbench_degenerate_sizes(D, O, n1, n2):
+@pytest.mark.parametrize("bulk", [True, False])
+@pytest.mark.parametrize("n1,n2", [(0, 0), (1, 0), (3, 1), (5, 7), (33, 31), (767, 769), (1536, 1)])
+def test_microbench_degenerate_sizes(D, O, n1, n2, bulk):
     """Empty and tiny workloads (no object, one object, partial warps and
-    partial type groups) give the oracle's results and leave the heap empty."""
+    partial type groups, ragged bulk units) give the oracle's results and
+    leave the heap empty."""
     from paper_1810_11765_b200.microbench import Microbench
-    mb = Microbench(n1=n1, n2=n2, seed=9)
+    mb = Microbench(n1=n1, n2=n2, seed=9, bulk=bulk)
     mb.step()
     torch.cuda.synchronize()
     assert np.array_equal(mb.results(), O.microbench(9, n1, n2)[0])
     assert mb.heap.poll_error() == D.OK
     assert [mb.heap.live_count(t) for t in range(3)] == [0, 0, 0]
     assert mb.heap.check_invariants() == 0
+
+
+@pytest.mark.parametrize("bulk", [True, False])
+def test_microbench_live_set_elementwise(D, O, bulk):
+    """Element-wise parity of the microbench (SURVEY c.8): after phases 1, 3
+    and 4 the canonical dump of every type (each live object's packed fields,
+    sorted by bytes) equals the oracle object store's live set, at n1 = 2^20
+    (ragged n2), with the bench's kernels."""
+    from paper_1810_11765_b200.microbench import Microbench
+    n1, n2 = 1 << 20, (1 << 19) + 13
+    mb = Microbench(n1=n1, n2=n2, seed=1, bulk=bulk)
+    for stop in (1, 3, 4):
+        mb.step(stop=stop)
+        torch.cuda.synchronize()
+        for t in range(3):
+            got = mb.heap.canonical_dump(t)
+            want = O.microbench_live(1, n1, n2, stop, t)
+            assert got.shape[0] == want.shape[0], (stop, t)
+            assert np.array_equal(got.reshape(-1).view(np.uint32).reshape(want.shape), want), (stop, t)
+        assert mb.heap.check_invariants() == 0
+        assert mb.heap.poll_error() == D.OK
+
+
+@pytest.mark.parametrize("rec,n", [([4, 1], 4097), ([4, 4, 4], 3), ([4, 8, 4, 1], 5)])
+def test_canonical_dump_odd_record_sizes(D, rec, n):
+    """Record sizes that are not multiples of 8 (5, 12, 17 B) with odd live
+    counts: the dump's cursor stays aligned and the records equal
+    what the user kernel wrote."""
+    heap = D.Heap([rec], 1 << 24)
+    out = torch.zeros(n, dtype=torch.int64, device="cuda")
+    heap.launch(D.K_LS_ALLOC, n, D.LsArgs(out.data_ptr(), 1, 0))
+    torch.cuda.synchronize()
+    recs = heap.canonical_dump(0)
+    assert recs.shape == (n, sum(rec))
+    assert heap.poll_error() == D.OK
