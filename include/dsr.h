@@ -40,7 +40,9 @@ typedef enum {
   DSR_ERR_INVALID = 1,       /* bad argument, detected on the host before launch */
   DSR_ERR_OOM = 2,           /* device-side: free block bitmap exhausted (reading R-OOM) */
   DSR_ERR_CUDA = 3,          /* a CUDA runtime call failed */
-  DSR_ERR_RETRY_BUDGET = 4,  /* debug builds: a spin exceeded its bound (P:1146 illegal use) */
+  DSR_ERR_RETRY_BUDGET = 4,  /* debug builds (-DDSR_DEBUG): illegal use detected -- a bitmap spin exceeded its
+                                bound or a destroy named a slot that is not allocated (Alg. 7
+                                precondition); release builds deadlock there, as the paper does */
   DSR_ERR_INVARIANT = 5,     /* dsr_check_invariants found violations */
   DSR_ERR_UNSUPPORTED = 6    /* id not compiled into this library */
 } dsr_status;
@@ -94,11 +96,14 @@ typedef struct {
 #define DSR_F_CTA_NEW     0x20u /* bulk constructors use CTA-level instead of warp-level request coalescing (microbench new kernel only) */
 #define DSR_F_HOME_ROT    0x40u /* ablation: SM-affine rotation (searches start in the SM's range of level-1 containers) */
 #define DSR_F_SLOT_ROTATE 0x80u /* paper: also rotate a block's object bitmap before choosing its free slots; off by default */
+#define DSR_F_SCALAR_DOALL 0x100u /* ablation: one thread per object in methods that also have a quad-mapped (vectorised) body */
 
 typedef struct {
   uint32_t active_retries;   /* r: try_find_set attempts before the slow path (Fig. 11); 0 -> 5 */
   uint32_t flags;            /* DSR_F_* */
   uint64_t seed;             /* rotation seed */
+  uint64_t max_blocks;       /* dsr_heap_create only: 0 = as many blocks as fit in the buffer, else
+                                M = min(that, max_blocks) ("M is determined at compile time") */
 } dsr_config;
 
 typedef struct {
@@ -289,7 +294,7 @@ typedef struct { uint64_t* out3; } dsr_mb_reduce_args;           /* out3[0..2] +
 enum {
   DSR_K_MB_NEW = 1,          /* args dsr_mb_new_args; fields k = low32(key(seed,0,MB_FIELD,16t+k)) or from `in` */
   /* The same objects and fields, allocated with warp-cooperative bulk requests
-   * (reading R-BULK): a warp takes 768 consecutive t and reserves
+   * (reading R-BULK): a warp takes 3072 consecutive t and reserves
    * all objects of one type of them with one request -- fresh blocks up to 64
    * per free-bitmap atomic, or free slots of active blocks found by 32
    * parallel rotated searches (P:649-654 generalised to many slots).  Which

@@ -12,8 +12,10 @@
  *   clear()         : P:529, reading R-CLEARANY (retry while try_clear fails)
  *   indices         : Alg. 5, P:592-621 (uses the nested level to skip)
  *   consistency     : Definition
- * Sequential execution: an op that the paper would spin on forever (illegal
- * use) sets b->error instead.
+ * Sequential execution: a set / clear that finds its bit already in the
+ * target state waits (pending) for the opposite op, as the paper's spinning
+ * thread would; one never released is the paper's deadlock (illegal use,
+ * P:1146) and makes or_bm_error report it.
  */
 #include "oracle.h"
 #include <stdlib.h>
@@ -61,6 +63,27 @@ static void trace(or_bitmap_t* b, uint32_t level, uint64_t pos, uint32_t is_set)
   }
 }
 
+/* the op waiting on (level, pos) for the opposite state, if any, completes now */
+static void resolve_pending(or_bitmap_t* b, uint32_t level, uint64_t pos, uint32_t want_set) {
+  for (uint32_t i = 0; i < b->npend; i++) {
+    if (b->pend_lvl[i] == level && b->pend_pos[i] == pos && b->pend_set[i] == want_set) {
+      b->npend--;
+      b->pend_lvl[i] = b->pend_lvl[b->npend];
+      b->pend_pos[i] = b->pend_pos[b->npend];
+      b->pend_set[i] = b->pend_set[b->npend];
+      if (want_set) or_bm_try_set(b, level, pos); else or_bm_try_clear(b, level, pos);
+      return;
+    }
+  }
+}
+static void add_pending(or_bitmap_t* b, uint32_t level, uint64_t pos, uint32_t is_set) {
+  if (b->npend == 16) { b->error = 1; return; }
+  b->pend_lvl[b->npend] = level;
+  b->pend_pos[b->npend] = pos;
+  b->pend_set[b->npend] = is_set;
+  b->npend++;
+}
+
 /* Alg. 3: prev <- atomicAnd(&container[cid], ~mask); success <- prev & mask;
  * if success and has_nested and popc(prev) = 1: nested.clear(cid). */
 int or_bm_try_clear(or_bitmap_t* b, uint32_t level, uint64_t pos) {
@@ -71,6 +94,7 @@ int or_bm_try_clear(or_bitmap_t* b, uint32_t level, uint64_t pos) {
   if (success) trace(b, level, pos, 0);
   if (success && level + 1 < b->nlevels && __builtin_popcountll(prev) == 1)
     or_bm_clear(b, level + 1, cid);
+  if (success) resolve_pending(b, level, pos, 1);
   return success;
 }
 
@@ -83,16 +107,19 @@ int or_bm_try_set(or_bitmap_t* b, uint32_t level, uint64_t pos) {
   if (success) trace(b, level, pos, 1);
   if (success && level + 1 < b->nlevels && prev == 0)
     or_bm_set(b, level + 1, cid);
+  if (success) resolve_pending(b, level, pos, 0);
   return success;
 }
 
-/* clear(pos) == while (!try_clear(pos)) {}.  Sequentially a failing
- * try_clear can never succeed later, so that is the paper's deadlock. */
+/* clear(pos) == while (!try_clear(pos)) {}: an op that finds the bit
+ * already cleared waits (pending) until a set of the same bit lets it
+ * through; one still waiting at quiescence is the paper's deadlock (illegal
+ * use), reported by or_bm_error. */
 void or_bm_clear(or_bitmap_t* b, uint32_t level, uint64_t pos) {
-  if (!or_bm_try_clear(b, level, pos)) b->error = 1;
+  if (!or_bm_try_clear(b, level, pos)) add_pending(b, level, pos, 0);
 }
 void or_bm_set(or_bitmap_t* b, uint32_t level, uint64_t pos) {
-  if (!or_bm_try_set(b, level, pos)) b->error = 1;
+  if (!or_bm_try_set(b, level, pos)) add_pending(b, level, pos, 1);
 }
 
 /* Alg. 4 (NoShift): cid from the nested bitmap, then ffs in container[cid]. */
@@ -185,4 +212,4 @@ uint32_t or_bm_ntrace(const or_bitmap_t* b) { return b->ntrace; }
 void or_bm_trace_get(const or_bitmap_t* b, uint32_t i, uint32_t* lvl, uint32_t* pos, uint32_t* is_set) {
   *lvl = b->trace[i][0]; *pos = b->trace[i][1]; *is_set = b->trace[i][2];
 }
-int or_bm_error(const or_bitmap_t* b) { return b->error; }
+int or_bm_error(const or_bitmap_t* b) { return b->error || b->npend > 0; }

@@ -24,7 +24,24 @@ struct or_heap {
   or_bitmap_t* allocated[OR_MAXT];
   or_bitmap_t* active[OR_MAXT];
   int error;
+  or_hook_fn hook;         /* scripted interleavings (tests) */
+  void* hook_ctx;
+  uint32_t hook_armed;     /* bit p: call the hook at point p once */
+  uint64_t counters[4];
 };
+
+void or_heap_set_hook(or_heap_t* h, or_hook_fn fn, void* ctx, uint32_t point) {
+  h->hook = fn;
+  h->hook_ctx = ctx;
+  h->hook_armed |= 1u << point;
+}
+uint64_t or_heap_counter(const or_heap_t* h, uint32_t k) { return k < 4 ? h->counters[k] : 0; }
+static void fire(or_heap_t* h, uint32_t point, uint64_t bid) {
+  if (h->hook && (h->hook_armed & (1u << point))) {
+    h->hook_armed &= ~(1u << point);
+    h->hook(h->hook_ctx, point, bid);
+  }
+}
 
 /* type ids are 1-based in handles and type[] (reading R-TYPEID / C18) */
 static uint64_t pad_mask(uint32_t cap) { return cap == 64 ? 0ULL : ~((1ULL << cap) - 1); }
@@ -43,11 +60,11 @@ void or_handle_decode(uint64_t h, uint32_t* type, uint32_t* cap, uint64_t* bid, 
   *type = (uint32_t)(h >> 56);
 }
 
-or_heap_t* or_heap_new(uint32_t ntypes, const uint32_t* nfields, const uint32_t* fsizes_flat,
-                       uint64_t heap_bytes) {
+or_heap_t* or_heap_new(uint32_t ntypes, const uint32_t* nfields, const uint32_t* fsizes_flat, uint64_t M) {
   or_heap_t* h = (or_heap_t*)calloc(1, sizeof(or_heap_t));
-  if (or_layout(ntypes, nfields, fsizes_flat, heap_bytes, &h->L) != 0) { free(h); return NULL; }
-  uint64_t M = h->L.M;
+  /* capacities from the layout; the block count is the caller's */
+  if (M == 0 || or_layout(ntypes, nfields, fsizes_flat, 1ULL << 40, &h->L) != 0) { free(h); return NULL; }
+  h->L.M = M;
   h->alloc_bm = (uint64_t*)malloc(M * sizeof(uint64_t));
   /* uninitialised blocks behave like invalidated ones: all bits 1 */
   for (uint64_t b = 0; b < M; b++) h->alloc_bm[b] = ~0ULL;
@@ -97,10 +114,15 @@ static int invalidate(or_heap_t* h, uint64_t bid) {
     if (before == ~0ULL) return 0;
     uint32_t t = h->type[bid] - 1u;
     if (before == pad_mask(h->L.cap[t])) return 1;
+    h->counters[1]++;
+    fire(h, OR_HOOK_INVALIDATED, bid);
     uint64_t before_rb = h->alloc_bm[bid];
     h->alloc_bm[bid] = before_rb & before;                /* rollback */
-    if (before_rb != ~0ULL) or_bm_clear(h->active[t], 0, bid);
-    if ((before_rb & before) == pad_mask(h->L.cap[t])) continue;   /* empty again */
+    if (before_rb != ~0ULL) {                             /* deferred deactivation (l.10) */
+      or_bm_clear(h->active[t], 0, bid);
+      h->counters[3]++;
+    }
+    if ((before_rb & before) == pad_mask(h->L.cap[t])) { h->counters[2]++; continue; }   /* empty again */
     return 0;
   }
 }
@@ -115,6 +137,7 @@ static void dealloc_block(or_heap_t* h, uint32_t T, uint64_t bid, uint64_t mask)
   int empty = ((before & ~mask) == pad_mask(h->L.cap[T]));   /* popc(before) = 1 */
   if (first) or_bm_set(h->active[T], 0, bid);
   if (empty) {
+    fire(h, OR_HOOK_EMPTIED, bid);
     if (invalidate(h, bid)) {
       uint32_t t = h->type[bid] - 1u;
       or_bm_clear(h->active[t], 0, bid);
@@ -137,13 +160,15 @@ uint64_t or_heap_alloc(or_heap_t* h, uint32_t T) {
       or_bm_set(h->allocated[T], 0, (uint64_t)bid);
       or_bm_set(h->active[T], 0, (uint64_t)bid);
     }
+    fire(h, OR_HOOK_FOUND, (uint64_t)bid);
     uint32_t slot;
     int full;
     if (reserve(h, (uint64_t)bid, &slot, &full)) {
       uint32_t t = h->type[bid] - 1u;                      /* volatile read */
       if (full) or_bm_clear(h->active[t], 0, (uint64_t)bid);
       if (t == T) return or_handle_encode(T + 1, h->L.cap[T], (uint64_t)bid, slot);
-      dealloc_block(h, t, (uint64_t)bid, 1ULL << slot);    /* rollback */
+      h->counters[0]++;
+      dealloc_block(h, t, (uint64_t)bid, 1ULL << slot);    /* rollback (l.14) */
     }
   }
 }

@@ -26,7 +26,7 @@ uint64_t or_key(uint64_t seed, uint64_t step, uint64_t phase, uint64_t idx);
 enum { OR_PH_INIT = 0, OR_PH_FISH_REQ = 1, OR_PH_FISH_DEC = 2,
        OR_PH_SHARK_REQ = 3, OR_PH_SHARK_DEC = 4, OR_PH_MB_FIELD = 5 };
 
-/* ---------------- heap layout (C20) ---------------------- */
+/* ---------------- heap layout (reading R-LAYOUT) -- */
 #define OR_MAXT 8
 #define OR_MAXF 16
 #define OR_MAXL 8
@@ -35,14 +35,11 @@ typedef struct {
   uint32_t nfields[OR_MAXT];
   uint32_t fsize[OR_MAXT][OR_MAXF];
   uint32_t cap[OR_MAXT];                 /* N_T, eq. P:308 */
-  uint32_t col_off[OR_MAXT][OR_MAXF];    /* byte offset of field column */
+  uint32_t col_off[OR_MAXT][OR_MAXF];    /* byte offset of field column (R-LAYOUT) */
   uint32_t block_bytes;                  /* data-segment bytes per block */
-  uint64_t M;                            /* number of blocks */
-  uint32_t nlevels;                      /* levels of one M-bit bitmap */
+  uint64_t M;                            /* upper bound on the block count (see or_layout) */
+  uint32_t nlevels;                      /* levels of one M-bit bitmap (P:501) */
   uint64_t level_words[OR_MAXL];         /* u64 containers per level */
-  uint64_t off_data, off_alloc_bm, off_iter_bm, off_type, off_R, off_bitmaps;
-  uint64_t bitmap_words;                 /* words of one hierarchical bitmap */
-  uint64_t total_bytes;                  /* bytes used of heap_bytes */
 } or_layout_t;
 
 /* returns 0 on success, nonzero on invalid input (type > 64x smallest, ...) */
@@ -60,6 +57,13 @@ typedef struct {
   uint32_t trace_on, ntrace;
   uint32_t trace[64][3];
   int error;             /* set on illegal use (spin-forever in the paper) */
+  /* set / clear ops that found their bit already in the target state: the
+   * paper's op "spins until it actually changed the bit";
+   * sequentially it waits here and completes right after the opposite op on
+   * the same bit.  Still pending at quiescence = the paper's deadlock. */
+  uint32_t npend;
+  uint32_t pend_lvl[16], pend_set[16];
+  uint64_t pend_pos[16];
 } or_bitmap_t;
 
 or_bitmap_t* or_bm_new(uint64_t n, uint32_t W, int all_set);
@@ -83,8 +87,8 @@ int or_bm_error(const or_bitmap_t* b);
 
 /* ---------------- sequential model of the paper's heap (Algs. 1-9) --------- */
 typedef struct or_heap or_heap_t;
-or_heap_t* or_heap_new(uint32_t ntypes, const uint32_t* nfields, const uint32_t* fsizes_flat,
-                       uint64_t heap_bytes);
+/* a heap of exactly M blocks ("M is determined at compile time") */
+or_heap_t* or_heap_new(uint32_t ntypes, const uint32_t* nfields, const uint32_t* fsizes_flat, uint64_t M);
 void or_heap_free(or_heap_t* h);
 uint64_t or_heap_alloc(or_heap_t* h, uint32_t type);      /* 0 == OOM */
 int or_heap_dealloc(or_heap_t* h, uint64_t handle);       /* 0 ok */
@@ -96,6 +100,19 @@ or_bitmap_t* or_heap_bitmap(or_heap_t* h, uint32_t which, uint32_t type);
 uint64_t or_heap_live(const or_heap_t* h, uint32_t type);
 double or_heap_fragmentation(const or_heap_t* h);
 int or_heap_error(const or_heap_t* h);
+/* Scripted interleavings (pins of the concurrent branches of Algs. 1, 2, 9):
+ * a one-shot hook called at a linearisation point, from which the test runs
+ * "another thread's" operations on the same heap.
+ *   OR_HOOK_FOUND        or_heap_alloc: block bid chosen (active or fresh), before the reservation (Alg. 1 l.9)
+ *   OR_HOOK_EMPTIED      dealloc: the last slot of bid freed (EMPTY), before invalidate (Alg. 2 l.7)
+ *   OR_HOOK_INVALIDATED  invalidate: atomicOr(~0) returned before != pad, before the rollback (Alg. 9 l.8) */
+enum { OR_HOOK_FOUND = 0, OR_HOOK_EMPTIED = 1, OR_HOOK_INVALIDATED = 2 };
+typedef void (*or_hook_fn)(void* ctx, uint32_t point, uint64_t bid);
+void or_heap_set_hook(or_heap_t* h, or_hook_fn fn, void* ctx, uint32_t point);
+/* counters: 0 type-change rollbacks (Alg. 1 l.14), 1 failed invalidations
+ * (Alg. 9 l.8), 2 invalidation retries after an empty-again rollback (l.12),
+ * 3 deferred deactivations (l.10) */
+uint64_t or_heap_counter(const or_heap_t* h, uint32_t k);
 
 /* handle codec, Fig. 5 / Listing 2, readings C6/C7 */
 uint64_t or_handle_encode(uint32_t type, uint32_t cap, uint64_t bid, uint32_t slot);

@@ -46,14 +46,6 @@ class Layout(C.Structure):
         ("M", C.c_uint64),
         ("nlevels", C.c_uint32),
         ("level_words", C.c_uint64 * 8),
-        ("off_data", C.c_uint64),
-        ("off_alloc_bm", C.c_uint64),
-        ("off_iter_bm", C.c_uint64),
-        ("off_type", C.c_uint64),
-        ("off_R", C.c_uint64),
-        ("off_bitmaps", C.c_uint64),
-        ("bitmap_words", C.c_uint64),
-        ("total_bytes", C.c_uint64),
     ]
 
 
@@ -67,6 +59,8 @@ class NbodyParams(C.Structure):
 
 
 _lib = None
+HOOK = C.CFUNCTYPE(None, C.c_void_p, C.c_uint32, C.c_uint64)
+HOOK_FOUND, HOOK_EMPTIED, HOOK_INVALIDATED = 0, 1, 2
 
 
 def lib():
@@ -133,6 +127,9 @@ def lib():
         L.or_heap_fragmentation.argtypes = [vp]
         L.or_heap_error.restype = C.c_int
         L.or_heap_error.argtypes = [vp]
+        L.or_heap_set_hook.argtypes = [vp, HOOK, vp, C.c_uint32]
+        L.or_heap_counter.restype = C.c_uint64
+        L.or_heap_counter.argtypes = [vp, C.c_uint32]
         L.or_handle_encode.restype = C.c_uint64
         L.or_handle_encode.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32]
         L.or_handle_decode.argtypes = [C.c_uint64, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
@@ -181,7 +178,9 @@ def _flat(type_fields):
 
 
 def layout(type_fields, heap_bytes):
-    """type_fields: list of lists of field byte sizes.  Returns a dict."""
+    """type_fields: list of lists of field byte sizes.  Returns a dict: cap,
+    col_off, block_bytes, M (the paper-derived bound on the block count of a
+    heap of heap_bytes, see or_layout), nlevels, level_words (of M bits)."""
     nf, fs = _flat(type_fields)
     L = Layout()
     rc = lib().or_layout(len(type_fields), nf, fs, heap_bytes, C.byref(L))
@@ -195,9 +194,6 @@ def layout(type_fields, heap_bytes):
         "M": L.M,
         "nlevels": L.nlevels,
         "level_words": [L.level_words[i] for i in range(L.nlevels)],
-        "off_data": L.off_data, "off_alloc_bm": L.off_alloc_bm, "off_iter_bm": L.off_iter_bm,
-        "off_type": L.off_type, "off_R": L.off_R, "off_bitmaps": L.off_bitmaps,
-        "bitmap_words": L.bitmap_words, "total_bytes": L.total_bytes,
     }
 
 
@@ -257,9 +253,10 @@ class _BorrowedBitmap(Bitmap):
 class PaperHeap:
     """O2 sequential model of the paper's allocator (Algs. 1-9)."""
 
-    def __init__(self, type_fields, heap_bytes):
+    def __init__(self, type_fields, M):
+        """A heap of exactly M blocks for the given types."""
         nf, fs = _flat(type_fields)
-        self.p = lib().or_heap_new(len(type_fields), nf, fs, heap_bytes)
+        self.p = lib().or_heap_new(len(type_fields), nf, fs, M)
         if not self.p:
             raise ValueError("bad heap")
         self.ntypes = len(type_fields)
@@ -269,6 +266,19 @@ class PaperHeap:
         if getattr(self, "p", None):
             lib().or_heap_free(self.p)
             self.p = None
+
+    def on(self, point, fn):
+        """Arm a one-shot hook at `point` (HOOK_*): fn(bid) runs "another
+        thread's" operations on this heap at that linearisation point."""
+        if not hasattr(self, "_fns"):
+            self._fns = {}
+            self._cb = HOOK(lambda ctx, pt, bid: self._fns[pt](bid))   # kept alive with the heap
+        self._fns[point] = fn
+        lib().or_heap_set_hook(self.p, self._cb, None, point)
+
+    def counters(self):
+        return {k: lib().or_heap_counter(self.p, i)
+                for i, k in enumerate(["rollbacks", "invalidate_fail", "invalidate_retry", "deferred_deactivation"])}
 
     def alloc(self, t): return lib().or_heap_alloc(self.p, t)
     def dealloc(self, h): return lib().or_heap_dealloc(self.p, h)

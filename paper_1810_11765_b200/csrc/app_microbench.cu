@@ -71,12 +71,59 @@ __global__ void __launch_bounds__(256, MINB) k_mb_new(DevHeap h, uint64_t n, dsr
 // of the unit with ONE warp-cooperative request (dsr_new_warp, reading
 // R-BULK) instead of one coalesced request per 32 threads; the constructor
 // then writes the reserved slots chunk by chunk (lane j -> slot j of a chunk:
-// coalesced column stores).  768 t = 384 A + 192 B + 192 C = exactly 6 / 4 / 6
+// coalesced column stores).  3072 t = 1536 A + 768 B + 768 C = exactly 24 / 16 / 24
 // blocks of N_T = 64 / 48 / 32.
 #ifndef DSR_MB_UNIT
-#define DSR_MB_UNIT 768
+#define DSR_MB_UNIT 3072
 #endif
 constexpr uint32_t kMbUnit = DSR_MB_UNIT;
+
+// Constructor of the reserved slots of one dsr_new_warp call for type T with
+// NF u32 fields (compile-time, so the field loop is unrolled and the column
+// offsets live in registers): chunk by chunk in lane order, lane j -> the
+// chunk's j-th reserved slot = the (done + cum + j)-th object of T in the unit.
+template <int NF, bool IN>
+__device__ __forceinline__ void mb_construct(const DevHeap& h, uint32_t T, const dsr_mb_new_args& a, uint64_t kp,
+                                             uint64_t ts, uint32_t nres, uint32_t off0, uint32_t off1, uint32_t done,
+                                             uint32_t bid, uint64_t mask) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t col[NF];
+#pragma unroll
+  for (int k = 0; k < NF; ++k) col[k] = h.types[T].col_off[k];
+  const uint32_t cnt = (uint32_t)__popcll(mask);
+  uint32_t cum = cnt;                                      // exclusive prefix in lane order
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, cum, o);
+    if (lane >= (uint32_t)o) cum += v;
+  }
+  cum -= cnt;
+  uint32_t chunks = __ballot_sync(0xffffffffu, mask != 0);
+  while (chunks) {
+    const uint32_t c = __ffs(chunks) - 1;
+    chunks &= chunks - 1;
+    const uint32_t cb = __shfl_sync(0xffffffffu, bid, c);
+    const uint64_t cm = shfl64(0xffffffffu, mask, c);
+    const uint32_t c0 = __shfl_sync(0xffffffffu, cum, c) + done;
+    const uint32_t cn = (uint32_t)__popcll(cm);
+    uint8_t* const blk = h.data + (size_t)cb * h.block_bytes;
+    for (uint32_t j = lane; j < cn; j += 32) {
+      const uint32_t s = nth_bit(cm, j);
+      const uint32_t i = c0 + j;                           // i-th object of T in the unit
+      const uint64_t t = nres == 2 ? ts + 4ull * (i >> 1) + ((i & 1) ? off1 : off0) : ts + 4ull * i + off0;
+      uint8_t* const obj = blk + 4u * s;
+      if (IN) {
+        const uint64_t ti = t - a.t0;
+        const uint32_t* src = a.in + 16 * (ti >> 2) + ((0xA630u >> (4 * (ti & 3))) & 0xFu);
+#pragma unroll
+        for (int k = 0; k < NF; ++k) *reinterpret_cast<uint32_t*>(obj + col[k]) = __ldg(src + k);
+      } else {
+#pragma unroll
+        for (int k = 0; k < NF; ++k) *reinterpret_cast<uint32_t*>(obj + col[k]) = (uint32_t)rng_key_p(kp, 5, t * 16 + k);
+      }
+    }
+  }
+}
 
 template <bool IN = false>
 __global__ void __launch_bounds__(256) k_mb_new_bulk(DevHeap h, uint64_t n, dsr_mb_new_args a) {
@@ -104,45 +151,15 @@ __global__ void __launch_bounds__(256) k_mb_new_bulk(DevHeap h, uint64_t n, dsr_
       // objects of T among ts .. ts + un - 1
       uint32_t need = off0 < un ? (un - off0 + 3) / 4 : 0;
       if (nres == 2) need += off1 < un ? (un - off1 + 3) / 4 : 0;
-      const uint32_t nf = h.types[T].nfields;
       uint32_t done = 0;
       while (done < need) {
         uint32_t bid;
         uint64_t mask;
         const uint32_t got = dsr_new_warp(h, T, need - done, &bid, &mask);
         if (!got) break;                                   // OOM (sticky error set)
-        const uint32_t cnt = (uint32_t)__popcll(mask);
-        uint32_t cum = cnt;                                // exclusive prefix in lane order
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t v = __shfl_up_sync(0xffffffffu, cum, o);
-          if (lane >= (uint32_t)o) cum += v;
-        }
-        cum -= cnt;
-        uint32_t chunks = __ballot_sync(0xffffffffu, mask != 0);
-        while (chunks) {
-          const uint32_t c = __ffs(chunks) - 1;
-          chunks &= chunks - 1;
-          const uint32_t cb = __shfl_sync(0xffffffffu, bid, c);
-          const uint64_t cm = shfl64(0xffffffffu, mask, c);
-          const uint32_t c0 = __shfl_sync(0xffffffffu, cum, c) + done;
-          const uint32_t cn = (uint32_t)__popcll(cm);
-          uint8_t* const blk = h.data + (size_t)cb * h.block_bytes;
-          for (uint32_t j = lane; j < cn; j += 32) {
-            const uint32_t s = nth_bit(cm, j);
-            const uint32_t i = c0 + j;                     // i-th object of T in the unit
-            const uint64_t t = nres == 2 ? ts + 4ull * (i >> 1) + ((i & 1) ? off1 : off0) : ts + 4ull * i + off0;
-            uint8_t* const obj = blk + 4u * s;
-            if (IN) {
-              const uint64_t ti = t - a.t0;
-              const uint32_t* src = a.in + 16 * (ti >> 2) + ((0xA630u >> (4 * (ti & 3))) & 0xFu);
-              for (uint32_t k = 0; k < nf; ++k) *reinterpret_cast<uint32_t*>(obj + h.types[T].col_off[k]) = __ldg(src + k);
-            } else {
-              for (uint32_t k = 0; k < nf; ++k)
-                *reinterpret_cast<uint32_t*>(obj + h.types[T].col_off[k]) = (uint32_t)rng_key_p(kp, 5, t * 16 + k);
-            }
-          }
-        }
+        if (T == 0) mb_construct<3, IN>(h, T, a, kp, ts, nres, off0, off1, done, bid, mask);
+        else if (T == 1) mb_construct<4, IN>(h, T, a, kp, ts, nres, off0, off1, done, bid, mask);
+        else mb_construct<6, IN>(h, T, a, kp, ts, nres, off0, off1, done, bid, mask);
         done += got;
       }
     }
@@ -225,6 +242,28 @@ struct MbFreeAll {
   DSR_NO_ACC
   static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args&, Acc&) {
     dsr_destroy_ro(h, make_handle(T, h.types[T].cap, b, s));   // never reads or writes the object
+  }
+};
+// The same two methods in quad form (k_doall_quad): a lane visits 4 slots,
+// reads field 0 of all of them with one 128-bit load, and destroys the chosen
+// ones with one block-aggregated mask (lanes of the same block combine into
+// one atomicAnd: 1 per 64-slot block instead of 2 for a 32-lane warp).
+struct MbFreeOddQ {
+  struct Args { uint64_t unused; };
+  DSR_NO_ACC
+  static __device__ __forceinline__ void run4(const DevHeap& h, uint32_t T, uint32_t b, uint32_t q, uint32_t m4,
+                                              const Args&, Acc&) {
+    const uint4 v = __ldcs(quad_u32(h, T, 0, b, q));
+    const uint32_t odd = (v.x & 1u) | ((v.y & 1u) << 1) | ((v.z & 1u) << 2) | ((v.w & 1u) << 3);
+    dsr_destroy_mask<false>(h, T, b, (uint64_t)(odd & m4) << (4 * q));   // control-dependent on the read
+  }
+};
+struct MbFreeAllQ {
+  struct Args { uint64_t unused; };
+  DSR_NO_ACC
+  static __device__ __forceinline__ void run4(const DevHeap& h, uint32_t T, uint32_t b, uint32_t q, uint32_t m4,
+                                              const Args&, Acc&) {
+    dsr_destroy_mask<false>(h, T, b, (uint64_t)m4 << (4 * q));           // never reads or writes the objects
   }
 };
 // handle collection (tests): out[atomic++] = this
@@ -427,8 +466,14 @@ bool mb_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot,
       count_launch();
       return true;
     }
-    case DSR_M_MB_FREE_ODD: launch_doall<MbFreeOdd>(c, T, snapshot, zero); return true;
-    case DSR_M_MB_FREE_ALL: launch_doall<MbFreeAll>(c, T, snapshot, zero); return true;
+    case DSR_M_MB_FREE_ODD:
+      if (c.h.flags & DSR_F_SCALAR_DOALL) launch_doall<MbFreeOdd>(c, T, snapshot, zero);
+      else launch_doall_quad<MbFreeOddQ>(c, T, snapshot, zero);
+      return true;
+    case DSR_M_MB_FREE_ALL:
+      if (c.h.flags & DSR_F_SCALAR_DOALL) launch_doall<MbFreeAll>(c, T, snapshot, zero);
+      else launch_doall_quad<MbFreeAllQ>(c, T, snapshot, zero);
+      return true;
     case DSR_M_COLLECT: launch_doall<Collect>(c, T, snapshot, args); return true;
     case DSR_M_INH_BUMP: case DSR_M_INH_SUM: case DSR_M_INH_SPAWN:
       for (uint32_t t = 0; t < c.h.ntypes; ++t)       // every type derives from a root {u32 id, u32 acc}
@@ -466,8 +511,8 @@ bool mb_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* a
       if (bytes != sizeof(dsr_mb_new_args) || c.h.ntypes < 3) { *ok = 0; return true; }
       const dsr_mb_new_args& ma = *(const dsr_mb_new_args*)args;
       if (ma.in && ((ma.t0 & 3) || ma.in_host)) { *ok = 0; return true; }   // host inputs are staged by dsr_launch
-      for (uint32_t t = 0; t < 3; ++t)
-        if (c.h.types[t].nfields > DSR_MAX_FIELDS) { *ok = 0; return true; }
+      for (uint32_t t = 0; t < 3; ++t)                  // A{3 x u32}, B{4 x u32}, C{6 x u32}
+        if (c.h.types[t].nfields != 3u + t + (t == 2) || c.h.types[t].fsize[0] != 4) { *ok = 0; return true; }
       if (cudaMemsetAsync(&c.h.ctrl[CTRL_WORK], 0, 8, c.st) != cudaSuccess) { *ok = 0; return true; }
       if (ma.in) k_mb_new_bulk<true><<<grid_for(c, n, k_mb_new_bulk<true>), 256, 0, c.st>>>(c.h, n, ma);
       else k_mb_new_bulk<false><<<grid_for(c, n, k_mb_new_bulk<false>), 256, 0, c.st>>>(c.h, n, ma);

@@ -176,6 +176,13 @@ __global__ void k_init_free(DevBitmap b, uint64_t nbits) {
   }
 }
 
+#ifdef DSR_DEBUG
+#define DSR_BUILD_KIND " debug"
+#elif defined(DSR_FAULT)
+#define DSR_BUILD_KIND " fault"
+#else
+#define DSR_BUILD_KIND ""
+#endif
 static dsr_status heap_init(dsr_heap* h, cudaStream_t st) {
   const dsr_layout& L = h->L;
   uint8_t* base = h->dev.data - L.off_data;
@@ -200,6 +207,15 @@ static void fill_bitmap(DevBitmap* b, uint64_t* words, const dsr_layout& L) {
   b->nlevels = L.nlevels;
   b->nbits = L.M;
 }
+static void fill_bitmaps(DevHeap& d, const dsr_layout& L, uint64_t* bm) {
+  fill_bitmap(&d.freebm, bm, L);
+  d.freebm.err = &d.ctrl[CTRL_ERR];
+  for (uint32_t t = 0; t < L.ntypes; ++t) {
+    fill_bitmap(&d.allocbm[t], bm + (1 + 2 * t) * L.bitmap_words, L);
+    fill_bitmap(&d.activebm[t], bm + (2 + 2 * t) * L.bitmap_words, L);
+    d.allocbm[t].err = d.activebm[t].err = &d.ctrl[CTRL_ERR];
+  }
+}
 
 static void apply_cfg(dsr_heap* h, const dsr_config* cfg) {
   h->dev.r_attempts = (cfg && cfg->active_retries) ? cfg->active_retries : 5;   // r = 5
@@ -214,6 +230,7 @@ extern "C" dsr_status dsr_heap_create(const dsr_type_desc* types, uint32_t ntype
   dsr_layout L;
   dsr_status s = dsr_layout_compute(types, ntypes, heap_bytes, &L);
   if (s != DSR_OK) return s;
+  if (cfg && cfg->max_blocks && cfg->max_blocks < L.M) place(&L, cfg->max_blocks, heap_bytes);   // fewer blocks fit
   if (L.nlevels > DSR_MAX_LEVELS) return DSR_ERR_INVALID;
   dsr_heap* h = new (std::nothrow) dsr_heap;
   if (!h) return DSR_ERR_INVALID;
@@ -239,11 +256,8 @@ extern "C" dsr_status dsr_heap_create(const dsr_type_desc* types, uint32_t ntype
   d.M = (uint32_t)L.M;
   d.block_bytes = L.block_bytes;
   d.ntypes = ntypes;
-  uint64_t* bm = (uint64_t*)(base + L.off_bitmaps);
-  fill_bitmap(&d.freebm, bm, L);
+  fill_bitmaps(d, L, (uint64_t*)(base + L.off_bitmaps));
   for (uint32_t t = 0; t < ntypes; ++t) {
-    fill_bitmap(&d.allocbm[t], bm + (1 + 2 * t) * L.bitmap_words, L);
-    fill_bitmap(&d.activebm[t], bm + (2 + 2 * t) * L.bitmap_words, L);
     DevType& ty = d.types[t];
     ty.cap = L.cap[t];
     ty.nfields = types[t].num_fields;
@@ -461,8 +475,15 @@ extern "C" dsr_status dsr_launch(dsr_heap* h, uint32_t kernel_id, uint64_t n, co
 __global__ void __launch_bounds__(256) k_reserve_blocks(DevHeap h, uint32_t T, uint64_t nblocks) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nblocks; i += stride) {
-    const int64_t bid = bm_clear_any(h, h.freebm, i * 0x9E3779B97F4A7C15ull + 1, 0);   // rotated per thread
-    if (bid < 0) return;                                                               // heap exhausted
+    int64_t bid = -1;
+    // a FAIL of clear() can be spurious while other threads clear bits of the
+    // same containers (transient level inconsistency): retry; give up
+    // only when the top-level word of the free bitmap is 0 (heap exhausted)
+    for (uint32_t k = 0; bid < 0 && k < 64; ++k) {
+      bid = bm_clear_any(h, h.freebm, i * 0x9E3779B97F4A7C15ull + 1, (uint64_t)k << 8);   // rotated per thread
+      if (bid < 0 && ld_relaxed(h.freebm.lvl[h.freebm.nlevels - 1]) == 0) return;
+    }
+    if (bid < 0) return;
     init_block(h, T, (uint32_t)bid);
     bm_set(h.allocbm[T], (uint64_t)bid);
     bm_set(h.activebm[T], (uint64_t)bid);
@@ -835,4 +856,4 @@ extern "C" const char* dsr_status_str(dsr_status s) {
   }
   return "DSR_ERR_?";
 }
-extern "C" const char* dsr_build_info(void) { return DSR_BUILD_INFO; }
+extern "C" const char* dsr_build_info(void) { return DSR_BUILD_INFO DSR_BUILD_KIND; }

@@ -27,6 +27,7 @@ struct DevBitmap {
   uint32_t nlevels;
   uint32_t pad_;
   uint64_t nbits;
+  unsigned long long* err;         // the heap's sticky error word (debug builds: bounded spins)
 };
 
 struct DevType {
@@ -150,6 +151,36 @@ __device__ __forceinline__ void backoff(uint32_t& ns) {
   __nanosleep(ns);
   ns = ns < 256 ? ns * 2 : 256;
 }
+// Debug builds (-DDSR_DEBUG, build(variant="debug")): illegal use (a
+// second net set / clear of a bitmap bit; destroying a slot that is
+// not allocated) deadlocks in the paper; here a spin gives up after 2^20
+// backoffs and the precondition of Alg. 7 is checked, both reported as
+// DSR_ERR_RETRY_BUDGET through the sticky error word.
+#ifdef DSR_DEBUG
+#define DSR_SPIN_GUARD(errp, n)                                         \
+  if (++(n) > (1u << 20)) {                                             \
+    atomicOr((errp), 2ull /* ERRB_BUDGET */);                           \
+    break;                                                              \
+  }
+#else
+#define DSR_SPIN_GUARD(errp, n)
+#endif
+// Fault-injection builds (-DDSR_FAULT): a pseudo-random pause of 0.5-8 us at
+// the linearisation points between which other threads can interleave
+// (found block -> reservation, Alg. 1 l.9; EMPTY -> invalidate, Alg. 2 l.7;
+// invalidate -> rollback, Alg. 9 l.8), so that the rare branches -- type
+// change rollback (Alg. 1 l.14), failed invalidation and its deferred
+// deactivation (Alg. 9 l.8-13) -- run in tests on tiny heaps.
+#ifdef DSR_FAULT
+__device__ __forceinline__ void fault_point(uint64_t salt) {
+  uint64_t z = ((uint64_t)clock64() ^ (salt << 32) ^ (threadIdx.x * 0x9E3779B97F4A7C15ull)) * 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 31;
+  if ((z & 3) == 0) __nanosleep(500 + (uint32_t)((z >> 8) & 7679));
+}
+#define DSR_FAULT_POINT(salt) fault_point(salt)
+#else
+#define DSR_FAULT_POINT(salt)
+#endif
 __device__ __forceinline__ void flag_error(const DevHeap& h, uint32_t bit) { atomicOr(&h.ctrl[CTRL_ERR], (ull)bit); }
 __device__ __forceinline__ void stat_add(const DevHeap& h, int which, uint64_t v) {
   if (h.flags & DSR_F_STATS) atomicAdd(&h.ctrl[CTRL_STATS + which], (ull)v);
@@ -244,8 +275,9 @@ __device__ __forceinline__ void bm_set_from(const DevBitmap& b, uint32_t l, uint
     uint64_t* w = b.lvl[l] + (pos >> 6);
     const uint64_t m = 1ull << (pos & 63);
     uint64_t prev = atom_or(w, m);     // first try blind (legal use: the bit is 0)
-    uint32_t ns = 32;
+    uint32_t ns = 32, spins = 0;
     while (prev & m) {
+      DSR_SPIN_GUARD(b.err, spins)
       backoff(ns);   // an in-flight clear of this bit is pending: wait for it, then retry
       if (!(ld_relaxed(w) & m)) prev = atom_or(w, m);
     }
@@ -258,8 +290,9 @@ __device__ __forceinline__ void bm_clear_from(const DevBitmap& b, uint32_t l, ui
     uint64_t* w = b.lvl[l] + (pos >> 6);
     const uint64_t m = 1ull << (pos & 63);
     uint64_t prev = atom_and(w, ~m);   // first try blind (legal use: the bit is 1)
-    uint32_t ns = 32;
+    uint32_t ns = 32, spins = 0;
     while (!(prev & m)) {
+      DSR_SPIN_GUARD(b.err, spins)
       backoff(ns);   // an in-flight set of this bit is pending
       if (ld_relaxed(w) & m) prev = atom_and(w, ~m);
     }
@@ -271,8 +304,9 @@ __device__ __forceinline__ void bm_clear_from(const DevBitmap& b, uint32_t l, ui
 __device__ __forceinline__ void bm_clear_finish(const DevBitmap& b, uint64_t pos, uint64_t prev) {
   uint64_t* w = b.lvl[0] + (pos >> 6);
   const uint64_t m = 1ull << (pos & 63);
-  uint32_t ns = 32;
+  uint32_t ns = 32, spins = 0;
   while (!(prev & m)) {
+    DSR_SPIN_GUARD(b.err, spins)
     backoff(ns);
     if (ld_relaxed(w) & m) prev = atom_and(w, ~m);
   }
@@ -281,8 +315,9 @@ __device__ __forceinline__ void bm_clear_finish(const DevBitmap& b, uint64_t pos
 __device__ __forceinline__ void bm_set_finish(const DevBitmap& b, uint64_t pos, uint64_t prev) {
   uint64_t* w = b.lvl[0] + (pos >> 6);
   const uint64_t m = 1ull << (pos & 63);
-  uint32_t ns = 32;
+  uint32_t ns = 32, spins = 0;
   while (prev & m) {
+    DSR_SPIN_GUARD(b.err, spins)
     backoff(ns);
     if (!(ld_relaxed(w) & m)) prev = atom_or(w, m);
   }
@@ -417,6 +452,7 @@ __device__ __forceinline__ bool block_invalidate(const DevHeap& h, uint32_t bid,
     const uint64_t pad = h.types[t].pad;
     if (before == pad) { *t_out = t; return true; }
     stat_add(h, ST_INVFAIL, 1);
+    DSR_FAULT_POINT(3);
     const uint64_t before_rb = atom_and(w, before);         // rollback exactly our bits
     if (before_rb != ~0ull) bm_clear(h.activebm[t], bid);   // deferred deactivation
     if ((before_rb & before) != pad) return false;          // not empty again
@@ -429,11 +465,19 @@ __device__ __forceinline__ bool block_invalidate(const DevHeap& h, uint32_t bid,
 // RELEASE = false: the relaxed form for dsr_destroy_ro (no fence).
 template <bool RELEASE = true>
 __device__ __forceinline__ void block_free(const DevHeap& h, uint32_t T, uint32_t bid, uint64_t mask) {
-  const uint64_t before = RELEASE ? atom_and_release(h.alloc_bm + bid, ~mask) : atom_and_relaxed(h.alloc_bm + bid, ~mask);
+  uint64_t before = RELEASE ? atom_and_release(h.alloc_bm + bid, ~mask) : atom_and_relaxed(h.alloc_bm + bid, ~mask);
+#ifdef DSR_DEBUG
+  if ((before & mask) != mask) {            // Alg. 7 precondition: slots not allocated
+    atomicOr(&h.ctrl[CTRL_ERR], (ull)ERRB_BUDGET);
+    mask &= before;
+    if (!mask) return;
+  }
+#endif
   const bool first = before == ~0ull;
   const bool empty = (before & ~mask) == h.types[T].pad;
   if (first) bm_set(h.activebm[T], bid);
   uint32_t t;
+  if (empty) DSR_FAULT_POINT(2);
   if (empty && block_invalidate(h, bid, &t)) {
     // Alg. 2 l.7-11: active[t].clear, allocated[t].clear, free.set -- three
     // independent leaf words, so the three blind first atomics are in flight
@@ -562,6 +606,7 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
       fresh = true;
     }
     uint64_t before = 0;
+    DSR_FAULT_POINT(1);
     long long c2 = prof ? clock64() : 0;
     // Slots inside the block: the lowest free ones by default; the paper also
     // rotates here (DSR_F_SLOT_ROTATE).  With per-warp hints a block
@@ -726,8 +771,9 @@ __device__ __forceinline__ void bm_set_many(const DevBitmap& b, uint64_t wi, uin
     const uint64_t m = late & (0ull - late);
     late &= late - 1;
     uint64_t pv = prev;
-    uint32_t ns = 32;
+    uint32_t ns = 32, spins = 0;
     while (pv & m) {
+      DSR_SPIN_GUARD(b.err, spins)
       backoff(ns);
       if (!(ld_relaxed(w) & m)) pv = atom_or(w, m);
     }
@@ -790,6 +836,7 @@ __device__ __forceinline__ uint32_t dsr_new_warp(const DevHeap& h, uint32_t T, u
       const uint32_t take = excl >= rem ? 0u : min(f, rem - excl);
       uint64_t got = 0;
       if (take) {
+        DSR_FAULT_POINT(4);
         uint64_t fr = ~cur;
         if ((uint32_t)__popcll(fr) > take) fr &= (2ull << nth_bit(fr, take - 1)) - 1ull;
         const uint64_t before = atom_or_acquire(h.alloc_bm + cand, fr);
@@ -859,23 +906,30 @@ __device__ __forceinline__ uint32_t dsr_new_warp(const DevHeap& h, uint32_t T, u
 // Device destroy: lanes freeing slots of the same block combine their
 // bits into one atomicAnd (coalesced version of Alg. 7).
 // RELEASE = false is dsr_destroy_ro below.
+// Destroy the objects `mask` of block `bid` of type T (several slots of one
+// block per lane: quad-mapped do-alls); lanes naming the same block combine
+// their masks into one atomicAnd.
 template <bool RELEASE = true>
-__device__ __forceinline__ void dsr_destroy_t(const DevHeap& h, uint64_t x) {
-  if (x == 0) return;
+__device__ __forceinline__ void dsr_destroy_mask(const DevHeap& h, uint32_t T, uint32_t bid, uint64_t bits) {
+  if (bits == 0) return;
   const uint32_t lane = lane_id();
   const uint32_t act = __activemask();
-  const uint64_t key = x >> 6;
+  const uint64_t key = ((uint64_t)T << 32) | bid;
   const uint32_t peers = (h.flags & DSR_F_NO_COALESCE) ? (1u << lane) : __match_any_sync(act, (ull)key);
   const uint32_t leader = __ffs(peers) - 1;
-  const uint64_t bit = 1ull << h_slot(x);
-  const uint32_t lo = __reduce_or_sync(peers, (uint32_t)bit);
-  const uint32_t hi = __reduce_or_sync(peers, (uint32_t)(bit >> 32));
+  const uint32_t lo = __reduce_or_sync(peers, (uint32_t)bits);
+  const uint32_t hi = __reduce_or_sync(peers, (uint32_t)(bits >> 32));
   __syncwarp(peers);   // memory ordering among the lanes: their object accesses precede the leader's release
   if (lane == leader) {
     const uint64_t mask = ((uint64_t)hi << 32) | lo;
-    block_free<RELEASE>(h, h_type(x), h_bid(x), mask);
+    block_free<RELEASE>(h, T, bid, mask);
     stat_add(h, ST_FREES, __popcll(mask));
   }
+}
+template <bool RELEASE = true>
+__device__ __forceinline__ void dsr_destroy_t(const DevHeap& h, uint64_t x) {
+  if (x == 0) return;
+  dsr_destroy_mask<RELEASE>(h, h_type(x), h_bid(x), 1ull << h_slot(x));
 }
 __device__ __forceinline__ void dsr_destroy(const DevHeap& h, uint64_t x) { dsr_destroy_t<true>(h, x); }
 // Destroy without the release fence (atom.release compiles to MEMBAR.ALL.GPU +

@@ -195,6 +195,65 @@ __global__ void __launch_bounds__(256, 8) k_doall(DevHeap h, uint32_t T, int sna
   Mth::flush(acc, a);
 }
 
+// Quad-mapped do-all body (vectorised, reading C31): element e is
+// the quad of slots 4q .. 4q+3 of block R[e / Q], Q = ceil(N_T / 4), so a warp
+// covers 128 consecutive slots and a u32 column segment of a quad is one
+// 16-B aligned 128-bit load (columns are 16-B aligned, R-LAYOUT).  The method
+// gets the quad's live-slot mask m4 (bit j = slot 4q + j visited; padding and
+// slots beyond N_T are never set) and must store only to visited slots (C31).
+// Grid-stride over the quads with an incremental (block, quad) pair.
+template <class Mth, int SCHED>
+__global__ void __launch_bounds__(256) k_doall_quad(DevHeap h, uint32_t T, int snapshot, int rk, typename Mth::Args a) {
+  uint32_t rb = 0, re;
+  if (rk < 0) {
+    re = ld_relaxed_u32((const uint32_t*)&h.ctrl[CTRL_RCOUNT]);
+  } else {
+    rb = ld_relaxed_u32((const uint32_t*)&h.ctrl[CTRL_RBEG + rk]);
+    re = ld_relaxed_u32((const uint32_t*)&h.ctrl[CTRL_RBEG + rk + 1]);
+  }
+  const uint32_t* R = h.R + rb;
+  const uint32_t Q = (h.types[T].cap + 3) >> 2;
+  const uint64_t valid = h.types[T].valid;
+  const uint64_t total = (uint64_t)(re - rb) * Q;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  typename Mth::Acc acc;
+  // kSchedCyclic: grid stride; kSchedBlocked: each warp owns one contiguous
+  // range of quads (passes that free whole blocks: concurrent warps then work
+  // on blocks far apart, so their block transitions hit different bitmap words)
+  uint64_t e, step, end;
+  if (SCHED == kSchedBlocked) {
+    const uint64_t nw = stride >> 5, w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t C = (total + 31) >> 5;
+    e = (w * C / nw) * 32 + (threadIdx.x & 31);
+    end = ((w + 1) * C / nw) * 32;
+    step = 32;
+  } else {
+    e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    end = total;
+    step = stride;
+  }
+  if (end > total) end = total;
+  uint64_t bi = e / Q;
+  uint32_t q = (uint32_t)(e - bi * Q);
+  const uint64_t dbi = step / Q;
+  const uint32_t dq = (uint32_t)(step - dbi * Q);
+  for (; e < end; e += step) {
+    const uint32_t b = __ldg(R + bi);
+    const uint64_t w = snapshot ? __ldg((const unsigned long long*)h.iter_bm + b) : (ld_relaxed(h.alloc_bm + b) & valid);
+    const uint32_t m4 = (uint32_t)(w >> (4 * q)) & 0xFu;
+    if (m4) Mth::run4(h, T, b, q, m4, a, acc);
+    bi += dbi;
+    q += dq;
+    if (q >= Q) { q -= Q; ++bi; }
+  }
+  Mth::flush(acc, a);
+}
+
+// the quad q of a u32 column f: one aligned 16-B segment (4 slots)
+__device__ __forceinline__ uint4* quad_u32(const DevHeap& h, uint32_t T, uint32_t f, uint32_t b, uint32_t q) {
+  return reinterpret_cast<uint4*>(h.data + (size_t)b * h.block_bytes + h.types[T].col_off[f] + 16u * q);
+}
+
 // Method helpers: most methods keep no per-thread accumulator.
 struct NoAcc {};
 #define DSR_NO_ACC                                                        \

@@ -81,4 +81,16 @@ inline void launch_doall(const LaunchCtx& c, uint32_t T, int snapshot, const voi
   count_launch();
 }
 
+// quad-mapped body (k_doall_quad): snapshot 3 -> blocked distribution, else cyclic
+template <class Mth>
+inline void launch_doall_quad(const LaunchCtx& c, uint32_t T, int snapshot, const void* args) {
+  typename Mth::Args a = *reinterpret_cast<const typename Mth::Args*>(args);
+  if (snapshot == 3)
+    k_doall_quad<Mth, kSchedBlocked><<<persistent_grid(c, k_doall_quad<Mth, kSchedBlocked>), 256, 0, c.st>>>(c.h, T, 1, c.rk, a);
+  else
+    k_doall_quad<Mth, kSchedCyclic><<<persistent_grid(c, k_doall_quad<Mth, kSchedCyclic>), 256, 0, c.st>>>(c.h, T, snapshot ? 1 : 0,
+                                                                                                           c.rk, a);
+  count_launch();
+}
+
 }  // namespace dsr

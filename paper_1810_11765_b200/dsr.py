@@ -22,6 +22,7 @@ OK, ERR_INVALID, ERR_OOM, ERR_CUDA, ERR_RETRY_BUDGET, ERR_INVARIANT, ERR_UNSUPPO
 # flags
 F_NO_ROTATE, F_NO_COALESCE, F_STATS, F_SPIN_ON_OOM, F_NO_HINT, F_CTA_NEW, F_HOME_ROT, F_SLOT_ROTATE = (
     0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40, 0x80)
+F_SCALAR_DOALL = 0x100
 
 # ids (mirror include/dsr.h)
 K_MB_NEW, M_MB_REDUCE, M_MB_FREE_ODD, M_MB_FREE_ALL = 1, 1, 2, 3
@@ -76,7 +77,8 @@ class Layout(C.Structure):
 
 
 class Config(C.Structure):
-    _fields_ = [("active_retries", C.c_uint32), ("flags", C.c_uint32), ("seed", C.c_uint64)]
+    _fields_ = [("active_retries", C.c_uint32), ("flags", C.c_uint32), ("seed", C.c_uint64),
+                ("max_blocks", C.c_uint64)]
 
 
 class Counters(C.Structure):
@@ -284,7 +286,7 @@ class Heap:
     allocates one large buffer on the GPU)."""
 
     def __init__(self, type_fields, heap_bytes, device=None, retries=5, flags=0, seed=0x5EED, stream=None,
-                 parents=None):
+                 parents=None, max_blocks=0):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("no CUDA device: the DynaSOAr hot path runs only on the GPU")
@@ -292,7 +294,7 @@ class Heap:
         self.ntypes = len(type_fields)
         self.device = torch.device(device or "cuda")
         self.buf = torch.empty(heap_bytes, dtype=torch.uint8, device=self.device)
-        self.cfg = Config(retries, flags, seed)
+        self.cfg = Config(retries, flags, seed, max_blocks)
         self.stream = stream
         h = C.c_void_p()
         with torch.cuda.device(self.device):

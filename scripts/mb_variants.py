@@ -7,8 +7,11 @@ from paper_1810_11765_b200 import dsr
 from paper_1810_11765_b200.microbench import Microbench, PHASES
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
-for name, kw in [("bulk", dict(bulk=True)), ("per_thread", dict(bulk=False)),
-                 ("per_thread_reserve", dict(bulk=False, reserve=True))]:
+which = sys.argv[2].split(",") if len(sys.argv) > 2 else ["bulk", "scalar_doall", "per_thread", "per_thread_reserve"]
+V = {"bulk": dict(bulk=True), "scalar_doall": dict(bulk=True, flags=dsr.F_SCALAR_DOALL),
+     "per_thread": dict(bulk=False), "per_thread_reserve": dict(bulk=False, reserve=True)}
+for name in which:
+    kw = V[name]
     s = torch.cuda.Stream()
     torch.cuda.set_stream(s)
     mb = Microbench(stream=s, **kw)
@@ -22,7 +25,7 @@ for name, kw in [("bulk", dict(bulk=True)), ("per_thread", dict(bulk=False)),
     ph = {p: round(statistics.median(ev[k][i][0].elapsed_time(ev[k][i][1]) for k in range(reps)), 4)
           for i, p in enumerate(PHASES)}
     assert mb.heap.poll_error() == dsr.OK
-    print(json.dumps({"variant": name, "step_ms": round(sum(ph.values()), 4), "phases": ph,
+    print(json.dumps({"variant": name, "lib": str(dsr.LIBPATH.name), "step_ms": round(sum(ph.values()), 4), "phases": ph,
                       "frag_blocks": mb.heap.fragmentation()[1]}), flush=True)
     del mb
     torch.cuda.empty_cache()

@@ -54,22 +54,29 @@ def replay_ops(rnd, ntypes, n, free_p=0.45):
     return ops
 
 
-@pytest.mark.parametrize("sizes,heap_bytes", [([12, 16, 24], 1 << 20), ([4, 256], 1 << 20), ([5, 8], 3 << 18),
-                                              ([8, 8, 40, 100], 1 << 21)])
-def test_single_thread_replay_matches_oracle(D, O, sizes, heap_bytes):
+@pytest.mark.parametrize("sizes,heap_bytes,M", [([12, 16, 24], 1 << 20, 700), ([4, 256], 1 << 20, 1037),
+                                                ([5, 8], 3 << 18, 333), ([8, 8, 40, 100], 1 << 21, 3005),
+                                                ([12, 16, 24], 1 << 20, 64), ([4, 8], 1 << 20, 65),
+                                                ([4, 256], 1 << 20, 40)])
+def test_single_thread_replay_matches_oracle(D, O, sizes, heap_bytes, M):
     """grid = 1x1, rotation and coalescing off: the CUDA allocator must produce
-    the oracle's words, type ids and handles exactly (Algs. 1-9)."""
+    the oracle's words, type ids and handles exactly (Algs. 1-9).  Both heaps
+    get the same block count M ("determined at compile time"), chosen
+    here (ragged, one-level and two-level bitmaps); small M also drives the
+    replay into OOM (null handles) and block re-typing."""
     tf = [split_fields(s) for s in sizes]
     rnd = random.Random(sum(sizes))
-    heap = D.Heap(tf, heap_bytes, flags=D.F_NO_ROTATE | D.F_NO_COALESCE | D.F_NO_HINT)
-    oh = O.PaperHeap(tf, heap_bytes)
+    heap = D.Heap(tf, heap_bytes, flags=D.F_NO_ROTATE | D.F_NO_COALESCE | D.F_NO_HINT, max_blocks=M)
+    assert heap.M == M
+    oh = O.PaperHeap(tf, M)
     ops = replay_ops(rnd, len(tf), 3000)
     want = []
     for op, arg in ops:
         if op == 0:
             want.append(oh.alloc(arg))
         else:
-            assert oh.dealloc(want[arg]) == 0
+            if want[arg]:                                       # destroy(null) is a no-op (OOM earlier)
+                assert oh.dealloc(want[arg]) == 0
             want.append(0)
     flat = np.array(ops, dtype=np.uint32).reshape(-1)
     d_ops = torch.from_numpy(flat.astype(np.int32)).cuda()
@@ -80,13 +87,13 @@ def test_single_thread_replay_matches_oracle(D, O, sizes, heap_bytes):
     assert np.array_equal(got, np.array(want, dtype=np.uint64))
     compare_state(D, heap, oh, len(tf))
     assert heap.check_invariants() == 0
-    assert heap.poll_error() == D.OK
+    assert heap.poll_error() == (D.ERR_OOM if 0 in [w for (op, _), w in zip(ops, want) if op == 0] else D.OK)
 
 
 def test_fresh_heap_state_and_invariants(D, O):
     tf = [[4, 4, 4], [4, 4, 4, 4], [4] * 6]
-    heap = D.Heap(tf, 1 << 26)
-    oh = O.PaperHeap(tf, 1 << 26)
+    heap = D.Heap(tf, 1 << 26, max_blocks=50_000)
+    oh = O.PaperHeap(tf, 50_000)
     compare_state(D, heap, oh, 3)
     assert heap.check_invariants() == 0
     assert [heap.live_count(t) for t in range(3)] == [0, 0, 0]

@@ -42,6 +42,18 @@ def test_capacity_formula_table1(O):
             O.layout([split_fields(s) for s in sizes], 1 << 26)
 
 
+def test_layout_worked_examples(O):
+    """Hand-worked layouts (tests/golden/layout_worked.json: N_T P:308, SOA
+    columns P:293, equal-size blocks P:303, per-block state P:291-293, P:464,
+    P:346-352, reading R-LAYOUT) for the three BASELINE apps' type sets."""
+    for c in golden("layout_worked.json")["cases"]:
+        L = O.layout(c["fields"], c["heap_bytes"])
+        assert L["cap"] == c["cap"], c["name"]
+        assert L["col_off"] == c["col_off"], c["name"]
+        assert L["block_bytes"] == c["block_bytes"], c["name"]
+        assert L["M"] == c["M"], c["name"]
+
+
 def test_layout_columns_are_disjoint_aligned_and_fit(O):
     rnd = random.Random(5)
     for _ in range(200):
@@ -60,39 +72,24 @@ def test_layout_columns_are_disjoint_aligned_and_fit(O):
                 off = L["col_off"][t][f]
                 colb = cap * s
                 assert off % 16 == 0                                    # R-LAYOUT (16-B vector loads)
+                if f:
+                    prev_end = L["col_off"][t][f - 1] + cap * tf[t][f - 1]
+                    assert prev_end <= off < prev_end + 16              # packed in declaration order
                 spans.append((off, off + colb))
-            spans.sort()
-            for a, b in zip(spans, spans[1:]):
-                assert a[1] <= b[0]                                     # SOA columns disjoint
             assert spans[-1][1] <= L["block_bytes"]
         assert L["block_bytes"] % 128 == 0
-        assert L["total_bytes"] <= heap
-        # regions in order and non-overlapping
-        M = L["M"]
-        regs = [(L["off_data"], M * L["block_bytes"]), (L["off_alloc_bm"], 8 * M), (L["off_iter_bm"], 8 * M),
-                (L["off_type"], M), (L["off_R"], 4 * M),
-                (L["off_bitmaps"], (1 + 2 * T) * L["bitmap_words"] * 8)]
-        for (o1, s1), (o2, _) in zip(regs, regs[1:]):
-            assert o1 + s1 <= o2
+        assert L["block_bytes"] - 128 < max(L["col_off"][t][-1] + L["cap"][t] * tf[t][-1] for t in range(T))
+        # the per-block state of M blocks fits in the heap, that of M + 1 does not
+        per_block_bits = 8 * (L["block_bytes"] + 21) + 1 + 2 * T
+        assert L["M"] * per_block_bits <= 8 * heap < (L["M"] + 1) * per_block_bits
         # level sizes: ceil(n/64) per level until n <= 64
-        n, lw = M, []
+        n, lw = L["M"], []
         while True:
             lw.append((n + 63) // 64)
             if n <= 64:
                 break
             n = (n + 63) // 64
         assert L["level_words"] == lw
-
-
-def test_layout_M_is_maximal(O):
-    # the next block count would not fit: shrinking the heap by the per-block
-    # cost must lose a block
-    tf = [[4, 4, 4], [4, 4, 4, 4], [4] * 6]
-    L = O.layout(tf, 1 << 31)              # >= 1 GiB: the hint table is at its maximum size
-    L2 = O.layout(tf, L["total_bytes"])
-    assert L2["M"] == L["M"]
-    L3 = O.layout(tf, L["total_bytes"] - 1)
-    assert L3["M"] < L["M"]
 
 
 # ------------------------------------------------------------------ bitmap
