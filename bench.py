@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="microbench", choices=["microbench", "wator", "gol", "gol16k", "gol16k-bits", "nbody"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-apps", action="store_true", help="skip the per-app block of the default line")
     return ap.parse_args()
 
 
@@ -58,26 +59,34 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes (read + write) of the roofline kernels from the
-    committed `ncu --set full` summary (profiles/<round>/ncu_summary.json)."""
+def ncu_traffic(build_src):
+    """Per-launch DRAM bytes (read + write), warp instructions and L2 atomic
+    requests of the roofline kernels from committed `ncu --set full` summaries
+    (profiles/<round>/ncu_summary.json) -- only those whose `build` (the
+    library's source hash, recorded when they were captured) equals this
+    library's; otherwise nothing (the counts would be stale)."""
     out = {}
     for p in sorted((ROOT / "profiles").glob("r*/ncu_summary.json")):
         try:
             rows = json.loads(p.read_text())
         except Exception:
             continue
-        for key in ("k_mb_new", "k_mb_reduce"):
-            v = [r["dram_bytes"] for r in rows if key in r.get("kernel", "") and "dram_bytes" in r]
-            if v:
-                out[key] = sum(v) / len(v)
-            v = [r["inst_executed"] for r in rows if key in r.get("kernel", "") and "inst_executed" in r]
-            if v:
-                out[key + ":inst"] = sum(v) / len(v)
-            v = [r["l2_atom_alu_requests"] for r in rows if key in r.get("kernel", "") and "l2_atom_alu_requests" in r]
-            if v:
-                out[key + ":atom"] = sum(v) / len(v)
+        rows = [r for r in rows if build_src and build_src in r.get("build", "")]
+        for key in ("k_mb_new_bulk", "k_mb_reduce"):
+            for name, field in (("", "dram_bytes"), (":inst", "inst_executed"), (":atom", "l2_atom_alu_requests")):
+                v = [r[field] for r in rows if key in r.get("kernel", "") and field in r]
+                if v:
+                    out[key + name] = sum(v) / len(v)
+                    out[key + ":source"] = str(p.relative_to(ROOT))
     return out
+
+
+def src_tag(info):
+    """'src:<hash>' of a dsr_build_info() string."""
+    for w in info.split():
+        if w.startswith("src:"):
+            return w
+    return ""
 
 
 class ClockSampler:
@@ -197,6 +206,21 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------- GPU leg
+def mb_step_ms(mb, stream, K, W):
+    """Device ms of one microbench step (K steps between events after W warm-up)."""
+    import torch
+    for _ in range(W):
+        mb.step(stream=stream)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(K):
+        mb.step(stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / K
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -211,6 +235,7 @@ def run_ours(args):
         build.build()
     if world > 1:
         dist.barrier()
+    build_info = dsr.lib().dsr_build_info().decode()
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     mb = Microbench(n1=N1, n2=N2, seed=SEED, stream=stream)
@@ -272,13 +297,10 @@ def run_ours(args):
 
     # blocks per type at the two reductions (one extra, untimed, instrumented step)
     blocks = []
-    mb.heap.reset(stream)
-    mb.out.zero_()
-    mb.heap.launch(mb.kernel, N1, dsr.MbNewArgs(SEED, 0), stream)
+    mb.step(stream=stream, stop=1)
     blocks.append(mb.heap.fragmentation(stream)[1])
-    for t in range(3):
-        mb.heap.parallel_do(t, dsr.M_MB_FREE_ODD, None, stream)
-    mb.heap.launch(mb.kernel, N2, dsr.MbNewArgs(SEED, N1), stream)
+    mb.heap.reset(stream)
+    mb.step(stream=stream, stop=4)
     frag5, b5 = mb.heap.fragmentation(stream)
     blocks.append(b5)
     # algorithmic bytes of the reduce bodies: live x size_T + 12 B per block
@@ -290,21 +312,35 @@ def run_ours(args):
     scan_ms = sum(body_ms)
     scan_gbs = scan_bytes / (scan_ms * 1e-3) / 1e9
     peak, peak_src = peaks()
-    # dominant kernel: k_mb_new (device new + constructor).  Algorithmic bytes =
-    # the constructed objects' fields + 16 B per block initialised (type id +
-    # object bitmap); its two launches are exactly phases new1 / new4.
+    # dominant kernel: k_mb_new_bulk (device new + constructors, phases new1 / new4).
+    # Algorithmic bytes = the constructed objects' fields + 16 B per block
+    # initialised (type id + object bitmap), SURVEY §8(d) D5.
     per_type = lambda n: [(n + 1) // 2, n // 4 + (1 if n % 4 > 2 else 0), n // 4]   # [A,A,B,C][t&3]
-    new_bytes = sum(c * s for c, s in zip(per_type(N1), sizes)) + sum(c * s for c, s in zip(per_type(N2), sizes))
-    new_bytes += 16 * (sum(int(b) for b in blocks[1]))
+    field_bytes = sum(c * s for c, s in zip(per_type(N1), sizes)) + sum(c * s for c, s in zip(per_type(N2), sizes))
+    new_bytes = field_bytes + 16 * sum(int(b) for b in blocks[1])
     new_ms = phase_ms[1] + phase_ms[4]
     new_gbs = new_bytes / (new_ms * 1e-3) / 1e9
-    traffic = ncu_traffic()
+    shares = {p: v / ms for p, v in zip(["init", "new1", "reduce2", "free3", "new4", "reduce5", "drain6"], phase_ms)}
+    traffic = ncu_traffic(src_tag(build_info))
+    sm_mhz = clk.get("sm_mhz") or 1965.0
+
+    # companions (untimed for the headline, timed the same way): the paper's per-thread device
+    # new (one coalesced request per warp and type, Alg. 1) with and without the host-side
+    # block reservation that round 1 used
+    variants = {}
+    if not args.no_apps:
+        for name, kw in (("per_thread_new", dict(bulk=False)), ("per_thread_new_host_reserve", dict(bulk=False, reserve=True))):
+            mv = Microbench(n1=N1, n2=N2, seed=SEED, stream=stream, **kw)
+            variants[name] = {"ms_per_step": mb_step_ms(mv, stream, 3, 2)}
+            assert mv.heap.poll_error() == dsr.OK
+            del mv
+            torch.cuda.empty_cache()
 
     # ---- e2e through the C ABI with HOST buffers: every step passes the host
     # (pinned) arrays of its 2^26 + 2^25 new objects' field values
-    # (inputs.mb_fields, 1.61 GB) to dsr_launch(K_MB_NEW, in_host = 1), which
-    # copies them into the heap's device staging buffers on its own copy stream
-    # (overlapping the work already queued), and reads the 144-byte result back.
+    # (inputs.mb_fields, 1.61 GB) to dsr_launch(K_MB_NEW_BULK, in_host = 1),
+    # which copies them into the heap's device staging buffers on its own copy
+    # stream (overlapping the work already queued), and reads the 144-byte result back.
     from paper_1810_11765_b200 import inputs as I
     in1_h = torch.from_numpy(I.mb_fields(SEED, 0, N1).view(np.int32)).pin_memory()
     in2_h = torch.from_numpy(I.mb_fields(SEED, N1, N2).view(np.int32)).pin_memory()
@@ -328,6 +364,7 @@ def run_ours(args):
     e2e_ms = e0.elapsed_time(e1) / K
     assert np.array_equal(e2e_res.numpy().view(np.uint64).reshape(2, 3, 3), res), \
         "host-input step differs from the device-key step"
+    del in1_h, in2_h
 
     # ---- aggregate over ranks (max time, sum of work)
     tot_updates, = reduce_over_ranks([float(updates)], "sum")
@@ -344,42 +381,50 @@ def run_ours(args):
         except Exception as e:   # the bench line must still print
             cpu = {"value": None, "unit": "object-updates/s", "cores": 1, "kind": "oracle", "sample": f"failed: {e}"}
 
+    apps = None
+    if world == 1 and not args.no_apps:
+        del mb
+        torch.cuda.empty_cache()
+        apps = app_block(stream, peak, peak_src, sm_mhz, want_cpu=not args.no_cpu_baseline)
+
     if rank == 0:
+        inst = traffic.get("k_mb_new_bulk:inst")
+        atom = traffic.get("k_mb_new_bulk:atom")
         line = {
             "metric": METRIC, "value": value, "unit": "object-updates/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": dict(CONFIG, heap_bytes=mb.heap.buf.numel(), M=mb.heap.M, caps=caps,
-                           parallelism=f"{world} independent heaps (one per GPU)"),
-            "allocs_per_s": (N1 + N2) * world / (sum(phase_ms[i] for i in (1, 4)) * 1e-3),
+            "config": dict(CONFIG, heap_bytes=mb_heap_bytes(), caps=caps,
+                           parallelism=f"{world} independent heaps (one per GPU)",
+                           allocation="warp-cooperative bulk device new (K_MB_NEW_BULK, reading R-BULK); "
+                                      "no host-side block reservation"),
+            "allocs_per_s": (N1 + N2) * world / (new_ms * 1e-3),
             "frees_per_s": counts["frees"] * world / (sum(phase_ms[i] for i in (3, 6)) * 1e-3),
             "scan_gbs": scan_gbs,
             "phase_ms": dict(zip(["init", "new1", "reduce2", "free3", "new4", "reduce5", "drain6"], phase_ms)),
+            "phase_share": shares,
             "fragmentation_after_phase4": frag5,
-            "roofline": {"bound": "hbm", "kernel": "k_mb_new (device new + constructors, 2 launches/step; "
-                                                     f"{100 * new_ms / ms:.0f}% of the step)",
+            "allocation_variants": variants,
+            "roofline": {"bound": "hbm", "kernel": "k_mb_new_bulk (device new + constructors, 2 launches/step; "
+                                                  f"{100 * new_ms / ms:.0f}% of the step)",
                          "achieved": new_gbs, "peak": peak, "unit": "GB/s", "frac": new_gbs / peak,
-                         "traffic": traffic.get("k_mb_new"), "peak_source": peak_src,
+                         "traffic": traffic.get("k_mb_new_bulk"), "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": new_bytes / 2,
-                         "note": "latency/contention-bound on the shared active-block bitmaps, not HBM"},
-            # the allocation kernel is instruction-issue bound (ncu: issue slots ~80 % busy): warp
-            # instructions per new1 launch (committed ncu --set full summary) / live new1 time, against
-            # 148 SMs x 4 schedulers x 1 warp-instruction/clk at the sampled SM clock
-            "roofline_issue": None if "k_mb_new:inst" not in traffic or not clk.get("sm_mhz") else {
-                "bound": "issue", "kernel": "k_mb_new (phase new1 launch)",
-                "achieved": traffic["k_mb_new:inst"] / (phase_ms[1] * 1e-3) / 1e9,
-                "peak": 148 * 4 * clk["sm_mhz"] * 1e6 / 1e9, "unit": "G warp-inst/s",
-                "frac": traffic["k_mb_new:inst"] / (phase_ms[1] * 1e-3) / (148 * 4 * clk["sm_mhz"] * 1e6),
-                "inst_per_launch": traffic["k_mb_new:inst"],
-                "note": "instruction count from the committed ncu summary of the same build (profiles/)"},
-            # the allocation kernel's L2 atomics (ncu request count of the same build, per new1
-            # launch) against the measured L2 atomic peak: not the bound, reported per SURVEY §8(d)
-            "roofline_atomics": {
-                "bound": "l2_atomics", "kernel": "k_mb_new (phase new1 launch)",
-                "achieved": traffic["k_mb_new:atom"] / (phase_ms[1] * 1e-3) / 1e9 if "k_mb_new:atom" in traffic else None,
-                "peak": atom_peak / 1e9, "unit": "G atomics/s",
-                "frac": traffic["k_mb_new:atom"] / (phase_ms[1] * 1e-3) / atom_peak if "k_mb_new:atom" in traffic else None,
-                "atomics_per_alloc": traffic["k_mb_new:atom"] / N1 if "k_mb_new:atom" in traffic else None,
+                         "traffic_source": traffic.get("k_mb_new_bulk:source"),
+                         "note": "constructor writes (fields + block headers); the kernel is issue-bound on the "
+                                 "workload's SplitMix64 field keys (roofline_issue)"},
+            # the allocation kernel's warp instructions (committed ncu summary of THIS build, per new1
+            # launch) / live new1 time, against 148 SMs x 4 schedulers x 1 warp-instruction/clk
+            "roofline_issue": None if inst is None else {
+                "bound": "issue", "kernel": "k_mb_new_bulk (phase new1 launch)",
+                "achieved": inst / (phase_ms[1] * 1e-3) / 1e9,
+                "peak": 148 * 4 * sm_mhz * 1e6 / 1e9, "unit": "G warp-inst/s",
+                "frac": inst / (phase_ms[1] * 1e-3) / (148 * 4 * sm_mhz * 1e6),
+                "inst_per_alloc": inst / N1, "source": traffic.get("k_mb_new_bulk:source")},
+            "roofline_atomics": None if atom is None else {
+                "bound": "l2_atomics", "kernel": "k_mb_new_bulk (phase new1 launch)",
+                "achieved": atom / (phase_ms[1] * 1e-3) / 1e9, "peak": atom_peak / 1e9, "unit": "G atomics/s",
+                "frac": atom / (phase_ms[1] * 1e-3) / atom_peak, "atomics_per_alloc": atom / N1,
                 "peak_source": "measured in this run: dsr_probe_atomics, hashed u64 atomicOr with return over 32 MiB"},
             "roofline_scan": {"bound": "hbm", "kernel": "k_mb_reduce<NF> (do-all field scan body, 6 launches/step; "
                                                         "the BASELINE >= 60% target)",
@@ -391,12 +436,231 @@ def run_ours(args):
                     "d2h_bytes_per_step": 144,
                     "what": "dsr_launch with HOST buffers: the new objects' field values (pinned host memory) "
                             "staged H2D by the library every step on its copy stream, result read back"},
+            "apps": apps,
             "gpu_launches": launches,
             "clocks": clk,
+            "build": build_info,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def mb_heap_bytes():
+    return max(64 << 20, int((N1 + N2) * 24 * 2.0))
+
+
+# ---------------------------------------------------------------- the other BASELINE configs (apps block)
+def timed_steps(step, K, W, stream, after=None):
+    """W untimed steps, then K steps each between its own pair of CUDA events on
+    `stream`; after(k) runs between steps, outside the events (live counts).
+    Returns the per-step device ms."""
+    import torch
+    for _ in range(W):
+        step()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for k in range(K):
+        if after is not None:
+            after(k)
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in ev]
+
+
+def hbm_roofline(kernel, nbytes, ms, peak, peak_src, note, bound="hbm"):
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    return {"bound": bound, "kernel": kernel, "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+            "algorithmic_bytes_per_step": nbytes, "peak_source": peak_src, "note": note}
+
+
+def app_block(stream, peak, peak_src, sm_mhz, want_cpu=True):
+    """BASELINE configs[0]-[3] on one GPU, each timed on the device (events
+    around every step; live counts between steps, outside the events):
+    object-updates/s, a roofline against MEASURED_PEAKS (SURVEY §8(d) D1-D4
+    algorithmic work) and the oracle on a bounded sample."""
+    import numpy as np
+    import torch
+    from paper_1810_11765_b200 import inputs as I
+    out = {}
+    live = torch.zeros(64, 3, dtype=torch.int64, device="cuda")
+
+    def cpu_of(fn):
+        if not want_cpu:
+            return None
+        try:
+            return fn()
+        except Exception as e:
+            return {"value": None, "kind": "oracle", "cores": 1, "sample": f"failed: {e}"}
+
+    # ---- GoL (configs[0] 64^2 x 100 gens; configs[3] 16384^2, handle grid and alive-bit mirror)
+    from paper_1810_11765_b200.gol import GameOfLife
+    for name, Wd, K, Wu, bits in (("gol_64", 64, 100, 5, False), ("gol_16384", 16384, 4, 1, False),
+                                  ("gol_16384_bits", 16384, 4, 1, True)):
+        a0 = I.gol_soup(Wd, Wd, 0.3 if Wd == 64 else 0.25, 1 if Wd == 64 else 42)
+        sim = GameOfLife(a0, stream=stream, bit_mirror=bits)
+        step = sim.generation
+        if Wd == 64:
+            sim.capture()
+            step = sim.graph.replay
+        cnt = torch.zeros(K, 2, dtype=torch.int64, device="cuda")
+
+        def after(k, sim=sim, cnt=cnt):
+            for t in range(2):
+                sim.heap.live_count_async(t, cnt[k, t], stream)
+        t = timed_steps(step, K, Wu, stream, after)
+        lv = cnt.cpu().numpy()
+        objs = lv.sum(axis=1)                                   # Alive + Candidate at each generation's start
+        ms = sum(t) / K
+        visits = 2 * int(objs.sum())                            # prepare + update visit per object
+        nbytes = 88 * float(objs.mean())                        # SURVEY D4: ~88 B per object and generation
+        out[name] = {
+            "config": f"BASELINE configs[{0 if Wd == 64 else 3}]: {Wd}^2 torus, Bernoulli("
+                      f"{0.3 if Wd == 64 else 0.25}) soup" + (", alive-bit mirror variant" if bits else "")
+                      + (", one generation replayed as a CUDA graph" if Wd == 64 else ""),
+            "value": visits / (sum(t) * 1e-3), "unit": "object-updates/s", "ms_per_step": ms, "steps": K,
+            "objects_per_step": float(objs.mean()),
+            "roofline": hbm_roofline("whole generation (4 do-alls + prologues)", nbytes, ms, peak, peak_src,
+                                     "launch/latency-bound: 4 do-alls over <= 4 K objects, no roofline target "
+                                     "(SURVEY D1)" if Wd == 64 else
+                                     "88 B/object/gen (own fields + 8 neighbour handles + update), SURVEY D4; "
+                                     "the neighbour gathers are scattered (objects sit in blocks in allocation, "
+                                     "not grid, order: P:794)" + ("; this variant reads a 1-bit mirror instead of "
+                                                                  "the 8 handles, same algorithmic definition" if bits else ""),
+                                     bound="latency" if Wd == 64 else "hbm"),
+        }
+        del sim
+        torch.cuda.empty_cache()
+        if bits:
+            continue
+
+        def gol_cpu(Wd=Wd):
+            from oracle import oracle as O
+            O.build()
+            b = I.gol_soup(Wd, Wd, 0.3 if Wd == 64 else 0.25, 1 if Wd == 64 else 42)
+            if Wd > 64:
+                b = np.ascontiguousarray(b[:4096, :4096])     # bounded sample: a 4096^2 corner as its own torus
+            G = 100 if Wd == 64 else 1
+            t0 = time.perf_counter()
+            O.gol_run(b, G)
+            dt = time.perf_counter() - t0
+            vis, a = 0, b
+            for _ in range(G):
+                n = sum(np.roll(np.roll(a, dy, 0), dx, 1) for dy in (-1, 0, 1) for dx in (-1, 0, 1)) - a
+                vis += 2 * (int(a.sum()) + int(((a == 0) & (n > 0)).sum()))
+                a = O.life_dense(a, 1)
+            return {"value": vis / dt, "unit": "object-updates/s", "cores": 1, "kind": "oracle",
+                    "sample": f"{G} generation(s) of " + (f"the {Wd}^2 run" if Wd == 64 else
+                                                         "a 4096^2 corner of the same soup (own torus)")
+                              + f", object oracle, {dt:.2f} s"}
+        out[name]["cpu_baseline"] = cpu_of(gol_cpu)
+
+    # ---- Wa-Tor 2048^2 (configs[1]); the static SOA baseline (P:763) beside it
+    from paper_1810_11765_b200.wator import WaTor, WaTorStatic
+    kind, egg, en = I.wator_init(2048, 2048, seed=42)
+    sim = WaTor(kind, egg, en, FB=6, SB=12, SS=6, seed=42, stream=stream)
+    sim.capture()
+    K = 40
+    cnt = torch.zeros(K, 2, dtype=torch.int64, device="cuda")
+
+    def after(k):
+        for t in range(2):
+            sim.heap.live_count_async(t, cnt[k, t], stream)
+    t = timed_steps(sim.graph.replay, K, 5, stream, after)
+    agents = cnt.cpu().numpy().sum(axis=1)
+    cells = 2048 * 2048
+    ms = sum(t) / K
+    visits = 4 * cells * K + 2 * int(agents.sum())
+    nbytes = 20 * cells + 100 * float(agents.mean())             # SURVEY D2
+    base = WaTorStatic(kind, egg, en, FB=6, SB=12, SS=6, seed=42, stream=stream)
+    tb = timed_steps(lambda: base.run(1), K, 5, stream)
+    out["wator_2048"] = {
+        "config": "BASELINE configs[1]: 2048^2 torus, FB 6 SB 12 SS 6, seed 42; one step (8 do-alls) replayed "
+                  "as a CUDA graph",
+        "value": visits / (sum(t) * 1e-3), "unit": "object-updates/s", "ms_per_step": ms, "steps": K,
+        "agents_per_step": float(agents.mean()),
+        "roofline": hbm_roofline("whole step (8 do-alls + prologues)", nbytes, ms, peak, peak_src,
+                                 "SURVEY D2: 2 x 5 B req clears + 2 x 5 B decides per cell + ~100 B per agent; "
+                                 "working set ~80 MB is L2-resident (126 MB), so HBM is not the bound"),
+        "static_baseline": {"ms_per_step": sum(tb) / K, "dynamic_over_static": ms / (sum(tb) / K),
+                            "what": "same rules on cell-indexed SOA arrays, no heap (P:763, dsr_wator_static_step)"},
+    }
+    del sim, base
+    torch.cuda.empty_cache()
+
+    def wator_cpu():
+        from oracle import oracle as O
+        O.build()
+        S = 2
+        t0 = time.perf_counter()
+        _, _, _, c = O.wator_run(kind, egg, en, FB=6, SB=12, SS=6, seed=42, steps=S)
+        dt = time.perf_counter() - t0
+        ag = [int((kind != 0).sum())] + [int(c[i, 0] + c[i, 1]) for i in range(S - 1)]
+        return {"value": (4 * cells * S + 2 * sum(ag)) / dt, "unit": "object-updates/s", "cores": 1,
+                "kind": "oracle", "sample": f"first {S} steps of the 2048^2 run (object oracle), {dt:.2f} s"}
+    out["wator_2048"]["cpu_baseline"] = cpu_of(wator_cpu)
+
+    # ---- N-body 65,536 bodies with merging (configs[2]); the force pass against the FP32 pipe
+    from paper_1810_11765_b200 import dsr
+    from paper_1810_11765_b200.nbody import NBody
+    st = I.nbody_init(65536, seed=7)
+    sim = NBody(st, merges=True, stream=stream, **I.NBODY_PARAMS)
+    K = 10
+    fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K + 3)]
+    kk = [0]
+
+    def nb_step():
+        e = fev[kk[0]]
+        sim.p_snapshot(stream)
+        e[0].record(stream)
+        sim.heap.parallel_do(0, dsr.M_NB_FORCE, sim.args, stream)
+        e[1].record(stream)
+        sim.heap.parallel_do(0, dsr.M_NB_MOVE, sim.args, stream)
+        sim.p_snapshot(stream)
+        sim.p_merge_search(stream)
+        sim.p_claim_absorb_delete(stream)
+        kk[0] += 1
+    cnt = torch.zeros(K, 1, dtype=torch.int64, device="cuda")
+
+    def after(k):
+        sim.heap.live_count_async(0, cnt[k, 0], stream)
+    t = timed_steps(nb_step, K, 3, stream, after)
+    lv = cnt.cpu().numpy()[:, 0]
+    ms = sum(t) / K
+    force_ms = sum(fev[3 + k][0].elapsed_time(fev[3 + k][1]) for k in range(K)) / K
+    pairs = 65536 * 65536                                       # the force pass evaluates every id pair (S0)
+    fp32_peak = 148 * 128 * sm_mhz * 1e6                        # FP32 lanes x SM clock (DESIGN.md §6)
+    ops = 9.0 * pairs                                           # 9 FP32 ops per pair + 1 MUFU.RSQ (DESIGN.md §6)
+    out["nbody_65536"] = {
+        "config": "BASELINE configs[2]: 65,536 fp32 bodies with merging, seed 7, inputs.NBODY_PARAMS",
+        "value": 8 * float(lv.sum()) / (sum(t) * 1e-3), "unit": "object-updates/s", "ms_per_step": ms, "steps": K,
+        "pair_interactions_per_s": 2 * pairs / (ms * 1e-3),
+        "roofline": {"bound": "alu", "kernel": f"k_nb_force_part (compute_force, device_do all-pairs; "
+                                               f"{100 * force_ms / ms:.0f}% of the step)",
+                     "achieved": ops / (force_ms * 1e-3) / 1e12, "peak": fp32_peak / 1e12, "unit": "T FP32 op/s",
+                     "frac": ops / (force_ms * 1e-3) / fp32_peak, "force_ms": force_ms,
+                     "peak_source": "148 SMs x 128 FP32 lanes x sampled SM clock (B200_PROFILING.md unit counts)",
+                     "note": "9 FP32 ops per pair (2 FADD, 2 FFMA for r^2, 3 FMUL, 2 FFMA accumulate) on packed "
+                             "f32x2 pairs; the snapshot is SMEM/L2-resident"},
+    }
+    del sim
+    torch.cuda.empty_cache()
+
+    def nbody_cpu():
+        from oracle import oracle as O
+        O.build()
+        n = 8192
+        s2 = I.nbody_init(n, seed=7)
+        t0 = time.perf_counter()
+        O.nbody_run(s2, merges=True, steps=1, **I.NBODY_PARAMS)
+        dt = time.perf_counter() - t0
+        return {"value": 8 * n / dt, "unit": "object-updates/s", "cores": 1, "kind": "oracle",
+                "sample": f"one step of {n} bodies (fp32 state, fp64 arithmetic; {2 * n * n / dt:.3g} pairs/s), "
+                          f"{dt:.2f} s"}
+    out["nbody_65536"]["cpu_baseline"] = cpu_of(nbody_cpu)
+    return out
 
 
 # ---------------------------------------------------------------- per-app lines (not the default)

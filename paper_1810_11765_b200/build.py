@@ -35,6 +35,17 @@ def _git_rev() -> str:
         return "nogit"
 
 
+def src_hash() -> str:
+    """sha1 (12 hex) of the library's sources and header: identifies a build
+    independently of git (the GPU box gets the tree without .git); profiles
+    record it so bench.py only reuses ncu counts of the same code."""
+    import hashlib
+    h = hashlib.sha1()
+    for f in [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "dsr.h"]:
+        h.update(f.read_bytes())
+    return h.hexdigest()[:12]
+
+
 def _stale() -> bool:
     if not OUT.exists():
         return True
@@ -55,7 +66,7 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False, var
     if not force and not tag and not _stale():
         return OUT
     BUILD.mkdir(exist_ok=True)
-    info = f'-DDSR_BUILD_INFO="sm_100a {_git_rev()} {time.strftime("%Y-%m-%d")}"'
+    info = f'-DDSR_BUILD_INFO="sm_100a src:{src_hash()} {_git_rev()} {time.strftime("%Y-%m-%d")}"'
     extra = (["-DDSR_PROFILE"] if profile else []) + [f"-D{d}" for d in defines]
 
     def compile_one(src: str) -> Path:

@@ -165,7 +165,8 @@ __device__ __forceinline__ void backoff(uint32_t& ns) {
 #else
 #define DSR_SPIN_GUARD(errp, n)
 #endif
-// Fault-injection builds (-DDSR_FAULT): a pseudo-random pause of 0.5-8 us at
+// Fault-injection builds (-DDSR_FAULT): a pseudo-random pause of 0.5-8 us (up to ~40 us
+// after a block was found) at
 // the linearisation points between which other threads can interleave
 // (found block -> reservation, Alg. 1 l.9; EMPTY -> invalidate, Alg. 2 l.7;
 // invalidate -> rollback, Alg. 9 l.8), so that the rare branches -- type
@@ -176,6 +177,9 @@ __device__ __forceinline__ void fault_point(uint64_t salt) {
   uint64_t z = ((uint64_t)clock64() ^ (salt << 32) ^ (threadIdx.x * 0x9E3779B97F4A7C15ull)) * 0xBF58476D1CE4E5B9ull;
   z ^= z >> 31;
   if ((z & 3) == 0) __nanosleep(500 + (uint32_t)((z >> 8) & 7679));
+  // a found block held across a long pause: time for it to be emptied, freed
+  // and re-initialised for another type (the type-change rollback's window)
+  if (salt == 1 && (z & 0x70) == 0) for (int k = 0; k < 8; ++k) __nanosleep(4000);
 }
 #define DSR_FAULT_POINT(salt) fault_point(salt)
 #else
@@ -463,11 +467,23 @@ __device__ __forceinline__ bool block_invalidate(const DevHeap& h, uint32_t bid,
 // FIRST iff before == ~0; EMPTY iff the remaining bits are padding only;
 // both at once: activate, then invalidate (reading R-FIRSTEMPTY / C17).
 // RELEASE = false: the relaxed form for dsr_destroy_ro (no fence).
-template <bool RELEASE = true>
+// USER = false: the rollback of a reservation (Alg. 1 l.14), whose block may
+// still be finishing its own allocated.set (debug checks off).
+template <bool RELEASE = true, bool USER = true>
 __device__ __forceinline__ void block_free(const DevHeap& h, uint32_t T, uint32_t bid, uint64_t mask) {
+#ifdef DSR_DEBUG
+  // An object's block is in allocated[T] from before the object is handed out
+  // until the block is freed, which needs every object destroyed: a destroy
+  // into a block that is not allocated is a double destroy whose block was
+  // freed (and invalidated to all ones, so the bitmap check below cannot see it).
+  if (USER && !bm_get(h.allocbm[T], bid)) {
+    atomicOr(&h.ctrl[CTRL_ERR], (ull)ERRB_BUDGET);
+    return;
+  }
+#endif
   uint64_t before = RELEASE ? atom_and_release(h.alloc_bm + bid, ~mask) : atom_and_relaxed(h.alloc_bm + bid, ~mask);
 #ifdef DSR_DEBUG
-  if ((before & mask) != mask) {            // Alg. 7 precondition: slots not allocated
+  if (USER && (before & mask) != mask) {    // Alg. 7 precondition: slots not allocated
     atomicOr(&h.ctrl[CTRL_ERR], (ull)ERRB_BUDGET);
     mask &= before;
     if (!mask) return;
@@ -632,7 +648,7 @@ static __device__ __forceinline__ uint64_t reserve_chunk(const DevHeap& h, uint3
       *bid_out = (uint32_t)bid;
       return got;
     }
-    block_free(h, t, (uint32_t)bid, got);                                     // type changed: rollback (l.14)
+    block_free<true, false>(h, t, (uint32_t)bid, got);                                     // type changed: rollback (l.14)
     stat_add(h, ST_ROLLBACKS, 1);
   }
 }
@@ -845,7 +861,7 @@ __device__ __forceinline__ uint32_t dsr_new_warp(const DevHeap& h, uint32_t T, u
           const uint32_t t = ld_relaxed_u8(h.type + cand) - 1u;       // volatile read (Alg. 1 l.10)
           if ((before | got) == ~0ull) bm_clear(h.activebm[t], (uint64_t)cand);   // FULL (l.12)
           if (t != T) {                                               // type changed: rollback (l.14)
-            block_free(h, t, (uint32_t)cand, got);
+            block_free<true, false>(h, t, (uint32_t)cand, got);
             stat_add(h, ST_ROLLBACKS, 1);
             got = 0;
           }

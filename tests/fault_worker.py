@@ -61,19 +61,39 @@ def torture(seed, nthreads, iters, max_blocks, bulk_check):
 
 
 def double_destroy():
-    """Destroying a slot twice (illegal, Alg. 7 precondition P:1000): the debug
-    build reports DSR_ERR_RETRY_BUDGET and leaves the heap consistent."""
-    heap = dsr.Heap([[4, 4]], 1 << 22)
+    """Destroying an object twice is illegal (Alg. 7 precondition).
+    (a) the object's block still holds other objects: its bit is already 0
+    when the second destroy's atomicAnd runs -- the debug build's precondition
+    check reports it; (b) the whole block was freed in between: its bitmap is
+    invalidated (all ones), so the precondition cannot see it, the second
+    destroy "frees" a free block and its allocated.clear spins -- the
+    debug build's spin bound reports it.  Both: DSR_ERR_RETRY_BUDGET."""
+    out = {}
+    heap = dsr.Heap([[4, 4]], 1 << 22, flags=dsr.F_STATS)
+    hs = torch.zeros(64, dtype=torch.int64, device="cuda")
+    heap.launch(dsr.K_LS_ALLOC, 64, dsr.LsArgs(hs.data_ptr(), 1, 0))
+    one = hs[5:6].clone()
+    heap.launch(dsr.K_LS_FREE, 1, dsr.LsArgs(one.data_ptr(), 1, 0))
+    torch.cuda.synchronize()
+    out["a_first"] = heap.poll_error()
+    heap.launch(dsr.K_LS_FREE, 1, dsr.LsArgs(one.data_ptr(), 1, 0))
+    torch.cuda.synchronize()
+    out["a_second"] = heap.poll_error()
+    out["a_live"] = heap.live_count(0)
+    out["a_audit"] = heap.check_invariants()
+    heap2 = dsr.Heap([[4, 4]], 1 << 22, flags=dsr.F_STATS)
     n = 100
-    hs = torch.zeros(n, dtype=torch.int64, device="cuda")
-    heap.launch(dsr.K_LS_ALLOC, n, dsr.LsArgs(hs.data_ptr(), 1, 0))
-    heap.launch(dsr.K_LS_FREE, n, dsr.LsArgs(hs.data_ptr(), 1, 0))
+    hs2 = torch.zeros(n, dtype=torch.int64, device="cuda")
+    heap2.launch(dsr.K_LS_ALLOC, n, dsr.LsArgs(hs2.data_ptr(), 1, 0))
+    heap2.launch(dsr.K_LS_FREE, n, dsr.LsArgs(hs2.data_ptr(), 1, 0))
     torch.cuda.synchronize()
-    first = heap.poll_error()
-    heap.launch(dsr.K_LS_FREE, n, dsr.LsArgs(hs.data_ptr(), 1, 0))      # the same handles again
+    out["b_first"] = heap2.poll_error()
+    out["b_stats_first"] = {k: int(v) for k, v in heap2.stats().items() if k in ("allocs", "frees", "block_inits",
+                                                                                  "block_frees")}
+    heap2.launch(dsr.K_LS_FREE, n, dsr.LsArgs(hs2.data_ptr(), 1, 0))      # the same handles again
     torch.cuda.synchronize()
-    return {"first_free": first, "second_free": heap.poll_error(), "audit": heap.check_invariants(),
-            "live": heap.live_count(0)}
+    out["b_second"] = heap2.poll_error()
+    return out
 
 
 if __name__ == "__main__":
