@@ -305,6 +305,15 @@ static LaunchCtx ctx(dsr_heap* h, void* stream) {
   return c;
 }
 
+// do-all prologue grid: one warp per level-1 container of the block bitmaps
+// (4096 blocks), at most one wave of resident CTAs (k_compact strides)
+static int compact_grid(const dsr_heap* h) {
+  const uint64_t n1 = ((h->L.M + 63) / 64 + 63) / 64;
+  const uint64_t ctas = (n1 + kCompactThreads / 32 - 1) / (kCompactThreads / 32);
+  const uint64_t cap = (uint64_t)h->sms * (uint64_t)resident_ctas((const void*)k_compact, kCompactThreads);
+  return (int)(ctas < 1 ? 1 : (ctas < cap ? ctas : cap));
+}
+
 // ---------------------------------------------------------------- operations
 static bool method_info(uint32_t method_id, MethodInfo* mi) {
   return mb_method_info(method_id, mi) || gol_method_info(method_id, mi) || wt_method_info(method_id, mi) ||
@@ -318,9 +327,7 @@ extern "C" dsr_status dsr_doall_prologue(dsr_heap* h, uint32_t type, uint32_t me
   cudaStream_t st = (cudaStream_t)stream;
   // R := compact(allocated[T]) (+ iteration-bitmap snapshot when the method may allocate)
   CUDA_TRY(cudaMemsetAsync(&h->dev.ctrl[CTRL_RCOUNT], 0, 8, st));
-  const uint64_t nwords = (h->L.M + 63) / 64;
-  k_compact<<<(int)((nwords + kCompactThreads - 1) / kCompactThreads), kCompactThreads, 0, st>>>(h->dev, type,
-                                                                                                  mi.snapshot);
+  k_compact<<<compact_grid(h), kCompactThreads, 0, st>>>(h->dev, type, mi.snapshot);
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return DSR_OK;
@@ -383,10 +390,8 @@ extern "C" dsr_status dsr_parallel_do(dsr_heap* h, uint32_t type, uint32_t metho
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaMemsetAsync(&h->dev.ctrl[CTRL_RCOUNT], 0, 8, st));
   CUDA_TRY(cudaMemsetAsync(&h->dev.ctrl[CTRL_RBEG], 0, 8, st));
-  const uint64_t nwords = (h->L.M + 63) / 64;
   for (uint32_t k = 0; k < ns; ++k) {
-    k_compact<<<(int)((nwords + kCompactThreads - 1) / kCompactThreads), kCompactThreads, 0, st>>>(h->dev, sub[k],
-                                                                                                    mi.snapshot);
+    k_compact<<<compact_grid(h), kCompactThreads, 0, st>>>(h->dev, sub[k], mi.snapshot);
     count_launch();
     CUDA_TRY(cudaMemcpyAsync(&h->dev.ctrl[CTRL_RBEG + k + 1], &h->dev.ctrl[CTRL_RCOUNT], 8, cudaMemcpyDeviceToDevice,
                              st));
@@ -788,8 +793,7 @@ extern "C" dsr_status dsr_canonical_dump(dsr_heap* h, uint32_t type, void* host_
   unsigned long long* cursor = (unsigned long long*)(d + cur_off);
   CUDA_TRY(cudaMemsetAsync(cursor, 0, 8, st));
   CUDA_TRY(cudaMemsetAsync(&h->dev.ctrl[CTRL_RCOUNT], 0, 8, st));
-  const uint64_t nwords = (h->L.M + 63) / 64;
-  k_compact<<<(int)((nwords + kCompactThreads - 1) / kCompactThreads), kCompactThreads, 0, st>>>(h->dev, type, 0);
+  k_compact<<<compact_grid(h), kCompactThreads, 0, st>>>(h->dev, type, 0);
   k_dump_records<<<h->sms * 8, 256, 0, st>>>(h->dev, type, rb, d, cursor);
   count_launch(2);
   std::vector<uint8_t> tmp(*used);

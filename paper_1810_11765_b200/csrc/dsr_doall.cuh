@@ -19,83 +19,115 @@
 
 namespace dsr {
 
-constexpr int kCompactThreads = 64;
 #ifndef DSR_DOALL_CHUNK
 #define DSR_DOALL_CHUNK 2
 #endif
 constexpr uint32_t kDoallChunk = DSR_DOALL_CHUNK;   // dynamic work unit of allocating passes: 2 x 32 elements per warp (sweep 1/2/4/8 -> 2)
+constexpr int kCompactThreads = 256;
 
+// Prologue driven from the nested level (Alg. 5's recursion, and
+// the paper's atomic cursor), so its cost follows the allocated blocks,
+// not the heap size M: a persistent grid of warps strides over the
+// level-1 containers of allocated[T]; a zero level-1 word (64 leaf words,
+// 4096 blocks) costs one load.  For a non-zero one, lane l reads leaf words
+// l and l + 32 (only those whose level-1 bit is set), the warp prefix-sums
+// their popcounts, reserves its range of R with ONE atomicAdd, and expands the
+// leaf words into R cooperatively (lane j writes bit j / j + 32 of each word:
+// coalesced).  snapshot: iter_bm[b] = alloc_bm[b] & valid(N_T) for the same
+// blocks (C12) as a separate batch of independent coalesced loads (inside
+// the expansion each word's load -> store chain would serialise the warp).
+// The count r stays on the device (ctrl[CTRL_RCOUNT]).
 static __global__ void __launch_bounds__(kCompactThreads) k_compact(DevHeap h, uint32_t T, int snapshot) {
-  __shared__ uint64_t s_word[kCompactThreads];
-  __shared__ uint32_t s_off[kCompactThreads];
-  __shared__ uint32_t s_warp[kCompactThreads / 32];
-  __shared__ uint32_t s_base;
   const DevBitmap& ab = h.allocbm[T];
   const uint64_t nwords = ((uint64_t)h.M + 63) / 64;
-  const uint64_t i = (uint64_t)blockIdx.x * kCompactThreads + threadIdx.x;
-  uint64_t w = 0;
-  if (i < nwords) {
-    bool any = true;
-    if (ab.nlevels > 1) any = (ab.lvl[1][i >> 6] >> (i & 63)) & 1ull;    // hierarchical skip
-    if (any) w = ab.lvl[0][i];
-  }
-  const uint32_t cnt = __popcll(w);
-  // CTA exclusive scan of cnt
-  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint32_t inc = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= (uint32_t)o) inc += v;
-  }
-  if (lane == 31) s_warp[wid] = inc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t run = 0;
-    for (int k = 0; k < kCompactThreads / 32; ++k) { const uint32_t t = s_warp[k]; s_warp[k] = run; run += t; }
-    s_base = run ? atomicAdd((unsigned int*)&h.ctrl[CTRL_RCOUNT], run) : 0u;
-  }
-  __syncthreads();
-  s_word[threadIdx.x] = w;
-  s_off[threadIdx.x] = s_base + s_warp[wid] + inc - cnt;
-  __syncwarp();
-  // warp-cooperative expansion of this warp's 32 containers
+  const uint64_t n1 = (nwords + 63) / 64;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t valid = h.types[T].valid;
-  for (int k = 0; k < 32; ++k) {
-    const uint32_t src = wid * 32 + k;
-    const uint64_t wk = s_word[src];
-    if (wk == 0) continue;
-    const uint32_t off = s_off[src];
-    const uint64_t cidx = (uint64_t)blockIdx.x * kCompactThreads + src;
+  for (uint64_t i1 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i1 < n1; i1 += nw) {
+    uint64_t w1;
+    if (ab.nlevels > 1) {
+      w1 = __ldg((const unsigned long long*)ab.lvl[1] + i1);
+    } else {                                                       // one level: every leaf word (nwords <= 64)
+      w1 = nwords >= 64 ? ~0ull : ((1ull << nwords) - 1ull);
+    }
+    if (w1 == 0) continue;
+    const uint64_t base_word = i1 * 64;
+    const uint64_t wa = ((w1 >> lane) & 1ull) ? __ldg((const unsigned long long*)ab.lvl[0] + base_word + lane) : 0ull;
+    const uint64_t wb = ((w1 >> (lane + 32)) & 1ull) ? __ldg((const unsigned long long*)ab.lvl[0] + base_word + lane + 32)
+                                                      : 0ull;
+    const uint32_t ca = __popcll(wa), c = ca + __popcll(wb);
+    uint32_t incl = c;
 #pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (uint32_t)o) incl += v;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) continue;
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd((unsigned int*)&h.ctrl[CTRL_RCOUNT], total);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const uint32_t offa = base + incl - c, offb = offa + ca;
+    // expansion: leaf word k (= lane k % 32's word a or b) -> its blocks, lane j takes bits j and j + 32
+    uint32_t srcs = __ballot_sync(0xffffffffu, wa != 0), srcs_b = __ballot_sync(0xffffffffu, wb != 0);
     for (int half = 0; half < 2; ++half) {
-      const uint32_t bit = lane + 32 * half;
-      if ((wk >> bit) & 1ull) {
-        const uint32_t pos = off + __popcll(wk & ((1ull << bit) - 1ull));
-        const uint32_t b = (uint32_t)(cidx * 64 + bit);
-        h.R[pos] = b;
+      uint32_t m = half ? srcs_b : srcs;
+      while (m) {
+        const uint32_t k = __ffs(m) - 1;
+        m &= m - 1;
+        const uint64_t wk = shfl64(0xffffffffu, half ? wb : wa, k);
+        const uint32_t off = __shfl_sync(0xffffffffu, half ? offb : offa, k);
+        const uint64_t bw = (base_word + k + 32u * half) * 64;           // first block of leaf word
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const uint32_t bit = lane + 32 * hh;
+          if ((wk >> bit) & 1ull) h.R[off + __popcll(wk & ((1ull << bit) - 1ull))] = (uint32_t)(bw + bit);
+        }
       }
     }
-  }
-  if (snapshot) {
-    // iteration-bitmap snapshot of this warp's 2048 blocks as independent,
-    // coalesced loads (a 256-B row of alloc_bm per warp and step, 8 rows in
-    // flight): done inside the loop above, each container's load -> store
-    // chain serialised the warp (Wa-Tor prologues 51 us with, 21 us without)
-    const uint64_t b0 = ((uint64_t)blockIdx.x * kCompactThreads + wid * 32) * 64;
-    for (int j0 = 0; j0 < 64; j0 += 8) {
-      uint64_t v[8];
-      bool on[8];
+    if (snapshot) {
+      // iteration bitmaps of the same blocks: rows of 32 consecutive u64 per
+      // step, 8 rows' loads in flight before their stores
+      for (int half = 0; half < 2; ++half) {
+        uint32_t m = half ? srcs_b : srcs;
+        while (m) {
+          uint64_t v[8], wkk[8];
+          uint32_t ks[8];
+          int n = 0;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int j = j0 + u;
-        on[u] = (s_word[wid * 32 + (j >> 1)] >> (lane + 32 * (j & 1))) & 1ull;
-        v[u] = on[u] ? __ldg((const unsigned long long*)h.alloc_bm + b0 + 64 * (j >> 1) + lane + 32 * (j & 1)) : 0ull;
-      }
+          for (int u = 0; u < 8; ++u) {
+            ks[u] = 0;
+            wkk[u] = 0;
+            v[u] = 0;
+            if (m) {
+              ks[u] = __ffs(m) - 1;
+              m &= m - 1;
+              n = u + 1;
+            }
+          }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int j = j0 + u;
-        if (on[u]) h.iter_bm[b0 + 64 * (j >> 1) + lane + 32 * (j & 1)] = v[u] & valid;
+          for (int u = 0; u < 8; ++u) {
+            if (u < n) {
+              wkk[u] = shfl64(0xffffffffu, half ? wb : wa, ks[u]);
+            }
+          }
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const uint32_t bit = lane + 32 * hh;
+              const uint64_t b = (base_word + ks[u] + 32u * half) * 64 + bit;
+              v[u] = (u < n && ((wkk[u] >> bit) & 1ull)) ? __ldg((const unsigned long long*)h.alloc_bm + b) : 0ull;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const uint32_t bit = lane + 32 * hh;
+              const uint64_t b = (base_word + ks[u] + 32u * half) * 64 + bit;
+              if (u < n && ((wkk[u] >> bit) & 1ull)) h.iter_bm[b] = v[u] & valid;
+            }
+          }
+        }
       }
     }
   }

@@ -99,11 +99,45 @@ def rel_pos_err(a, b):
     return float(np.max(np.abs(a.astype(np.float64) - b.astype(np.float64)) / den))
 
 
+def test_nbody_65536_ten_steps_baseline_config(P):
+    """BASELINE configs[2] itself -- 65,536 bodies, seed 7, inputs.NBODY_PARAMS
+    (G 1e-12, dt 0.5, eps 2.5e-4, R 1e-3), merges on -- for the 10 steps at
+    which BASELINE states its tolerance: surviving ids equal, positions <= 1e-4
+    relative, total mass <= 1e-5 relative.  The reference state is the
+    oracle's (tests/golden/nbody65536_10steps.npz, written by
+    scripts/make_nbody_golden.py, which calls only oracle/: ~8 min on one
+    core, too slow to recompute in every run)."""
+    from pathlib import Path
+    from paper_1810_11765_b200 import inputs as I, nbody
+    g = np.load(Path(__file__).parent / "golden" / "nbody65536_10steps.npz")
+    assert list(g["meta"]) == [65536, 7, 10]
+    assert list(g["params"]) == [I.NBODY_PARAMS[k] for k in ("G", "dt", "eps", "R")]
+    st = I.nbody_init(65536, seed=7)
+    sim = nbody.NBody(st, merges=True, **I.NBODY_PARAMS)
+    sim.run(10)
+    got = sim.state()
+    assert np.array_equal(got["alive"], g["alive"])
+    al = g["alive"] == 1
+    assert (~al).sum() > 1000                                  # merges happened (1,769 bodies absorbed)
+    for k in ("x", "y"):
+        assert rel_pos_err(got[k][al], g[k][al]) <= 1e-4, k
+    m0 = float(st["m"].astype(np.float64).sum())
+    assert abs(float(got["m"][al].astype(np.float64).sum()) - m0) <= 1e-5 * m0
+    assert abs(float(got["m"][al].astype(np.float64).sum()) - float(g["m"][al].astype(np.float64).sum())) <= 1e-5 * m0
+    assert sim.heap.live_count(0) == int(al.sum())
+    assert sim.heap.check_invariants() == 0
+
+
 @pytest.mark.parametrize("n,steps,merges", [(2048, 10, True), (4096, 10, False), (1000, 10, True)])
 def test_nbody_against_oracle(P, O, n, steps, merges):
-    """Scaled-down configs[2]: G and eps chosen so the 10-step trajectories
-    are not chaotic (max |dp| per step well below R); forces are checked
-    through the velocities they produce, positions at the BJ tolerance."""
+    """Scaled-down configs[2] (n <= 4096 on the same [-1, 1)^2 domain): with
+    the BASELINE constants (R 1e-3, G 1e-12) so few bodies would hardly ever
+    meet (n^2/2 * pi R^2 / 4 ~ 1.6 pairs within R at n = 2048, against ~1,700
+    at 65,536), so R is scaled up to 0.02 (~660 pairs) to exercise merges, and
+    G, eps with it (2e-9, 0.01) so that the 10-step trajectories stay
+    non-chaotic (max |dp| per step well below R).  The BASELINE constants
+    themselves are tested at full size above.  Forces are checked through the
+    velocities they produce, positions at the BJ tolerance."""
     from paper_1810_11765_b200 import inputs as I, nbody
     st = I.nbody_init(n, seed=7)
     prm = dict(G=2e-9, dt=0.5, eps=0.01, R=0.02 if merges else 1e-3)
