@@ -48,7 +48,27 @@ def parse():
     ap.add_argument("--workload", default="microbench", choices=["microbench", "wator", "gol", "gol16k", "gol16k-bits", "nbody"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-apps", action="store_true", help="skip the per-app block of the default line")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="no GPU work: exercise the launch / rank aggregation / JSON path (gloo; tests)")
     return ap.parse_args()
+
+
+def free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def maybe_spawn(args):
+    """--gpus N > 1 without a torchrun environment: re-launch this command
+    under torch.distributed.run with N ranks on this node (127.0.0.1), so
+    `python bench.py --gpus N` and the driver's torchrun launch are the same."""
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={free_port()}", str(ROOT / "bench.py"), *sys.argv[1:]]
+        sys.stdout.flush()
+        os.execv(sys.executable, cmd)
 
 
 def peaks():
@@ -140,26 +160,33 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def dist_init(n):
+def dist_init(n, backend=None):
     import torch
     import torch.distributed as dist
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
-    if world > 1:
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
-    if torch.cuda.is_available():
+    if world != n:
+        raise SystemExit(f"bench.py --gpus {n} but WORLD_SIZE={world}")
+    if torch.cuda.is_available() and backend != "gloo":
         torch.cuda.set_device(local)
+    if world > 1:
+        be = backend or ("nccl" if torch.cuda.is_available() else "gloo")
+        dist.init_process_group(be)
+        print(f"[bench] rank {rank}/{world} local {local} backend {be} (torch.distributed process group; "
+              f"NCCL_DEBUG=INFO shows the communicator)", file=sys.stderr, flush=True)
     return rank, world, local
 
 
-def reduce_over_ranks(vals, op, device="cuda"):
+def reduce_over_ranks(vals, op, device=None):
     """Sum ("sum") or max ("max") of a list of floats over all ranks (identity
     without an initialised process group)."""
     import torch
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return list(vals)
+    if device is None:
+        device = "cuda" if dist.get_backend() == "nccl" else "cpu"
     t = torch.tensor(vals, dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX)
     return t.tolist()
@@ -197,7 +224,10 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "object-updates/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": CONFIG,
+        "config": dict(CONFIG, n1=N1 // 4, n2=N2 // 4, full_workload={"n1": N1, "n2": N2},
+                       sample="each step runs the microbench phases on a quarter of the workload "
+                              "(n1 = 2^24, n2 = 2^23); object-updates/s is per object, so it compares "
+                              "with the full-size line"),
         "cpu_baseline": {"value": v, "unit": "object-updates/s", "cores": 1, "kind": "oracle",
                          "sample": f"each step: the microbench phases on n1 = 2^24, n2 = 2^23 (a quarter of the "
                                    f"workload), oracle/ plain C single-threaded object store, {t:.2f} s/step"},
@@ -837,9 +867,28 @@ def app_cpu_baseline(workload):
     return {"value": visits / t, "unit": "object-updates/s", "cores": 1, "kind": "oracle", "sample": sample}
 
 
+def run_dry(args):
+    """--dry-run: the multi-rank plumbing without a GPU (gloo): every rank
+    'processes' N1 + N2 objects in (1 + rank) ms; rank 0 prints the line with
+    the summed work and the max-over-ranks time (tests/test_multiproc_cpu.py)."""
+    import torch.distributed as dist
+    rank, world, _ = dist_init(args.gpus, backend="gloo")
+    work, = reduce_over_ranks([float(N1 + N2)], "sum", device="cpu")
+    ms, = reduce_over_ranks([1.0 + rank], "max", device="cpu")
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": work / (ms * 1e-3), "unit": "object-updates/s", "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                          "scaling": "weak", "dry_run": True, "config": CONFIG}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
+    maybe_spawn(args)
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     elif args.workload != "microbench":
         run_app(args)

@@ -10,6 +10,7 @@
 #define DSR_BUILD_INFO "sm_100a"
 #endif
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX: no-ops unless a profiler is attached
 #include <algorithm>
 #include <mutex>
 #include <vector>
@@ -305,11 +306,11 @@ static LaunchCtx ctx(dsr_heap* h, void* stream) {
   return c;
 }
 
-// do-all prologue grid: one warp per level-1 container of the block bitmaps
-// (4096 blocks), at most one wave of resident CTAs (k_compact strides)
+// do-all prologue grid: one warp per half level-1 container of the block
+// bitmaps (2048 blocks), at most one wave of resident CTAs (k_compact strides)
 static int compact_grid(const dsr_heap* h) {
-  const uint64_t n1 = ((h->L.M + 63) / 64 + 63) / 64;
-  const uint64_t ctas = (n1 + kCompactThreads / 32 - 1) / (kCompactThreads / 32);
+  const uint64_t items = 2 * (((h->L.M + 63) / 64 + 63) / 64);       // halves of level-1 containers
+  const uint64_t ctas = (items + kCompactThreads / 32 - 1) / (kCompactThreads / 32);
   const uint64_t cap = (uint64_t)h->sms * (uint64_t)resident_ctas((const void*)k_compact, kCompactThreads);
   return (int)(ctas < 1 ? 1 : (ctas < cap ? ctas : cap));
 }
@@ -321,6 +322,8 @@ static bool method_info(uint32_t method_id, MethodInfo* mi) {
 }
 
 extern "C" dsr_status dsr_doall_prologue(dsr_heap* h, uint32_t type, uint32_t method_id, void* stream) {
+  nvtxRangePushA("dsr doall_prologue");
+  struct Pop { ~Pop() { nvtxRangePop(); } } pop_;
   if (!h || type >= h->L.ntypes) return DSR_ERR_INVALID;
   MethodInfo mi;
   if (!method_info(method_id, &mi)) return DSR_ERR_UNSUPPORTED;
@@ -354,6 +357,8 @@ static dsr_status doall_body(dsr_heap* h, uint32_t type, uint32_t method_id, con
 
 extern "C" dsr_status dsr_doall_body(dsr_heap* h, uint32_t type, uint32_t method_id, const void* args,
                                      size_t args_bytes, void* stream) {
+  nvtxRangePushA("dsr doall_body");
+  struct Pop { ~Pop() { nvtxRangePop(); } } pop_;
   return doall_body(h, type, method_id, args, args_bytes, stream, -1);
 }
 
@@ -371,8 +376,20 @@ static uint32_t subtree(const dsr_heap* h, uint32_t type, uint32_t* out) {
   return n;
 }
 
+// NVTX range per do-all / user-kernel launch (name = operation, type, id),
+// so nsys / ncu timelines show each pass of a step
+struct NvtxRange {
+  explicit NvtxRange(const char* what, uint32_t type, uint32_t id) {
+    char name[64];
+    snprintf(name, sizeof(name), "dsr %s T%u #%u", what, type, id);
+    nvtxRangePushA(name);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 extern "C" dsr_status dsr_parallel_do(dsr_heap* h, uint32_t type, uint32_t method_id, const void* args,
                                       size_t args_bytes, void* stream) {
+  NvtxRange nv("parallel_do", type, method_id);
   MethodInfo mi;
   if (!h || type >= h->L.ntypes) return DSR_ERR_INVALID;
   if (!method_info(method_id, &mi)) return DSR_ERR_UNSUPPORTED;
@@ -406,6 +423,7 @@ extern "C" dsr_status dsr_parallel_do(dsr_heap* h, uint32_t type, uint32_t metho
 
 extern "C" dsr_status dsr_parallel_new(dsr_heap* h, uint32_t type, uint64_t n, uint32_t ctor_id, const void* args,
                                        size_t args_bytes, void* stream) {
+  NvtxRange nv("parallel_new", type, ctor_id);
   if (!h || type >= h->L.ntypes) return DSR_ERR_INVALID;
   if (n == 0) return DSR_OK;
   LaunchCtx c = ctx(h, stream);
@@ -450,6 +468,7 @@ static dsr_status stage_host_input(dsr_heap* h, uint64_t n, dsr_mb_new_args* a, 
 
 extern "C" dsr_status dsr_launch(dsr_heap* h, uint32_t kernel_id, uint64_t n, const void* args, size_t args_bytes,
                                  void* stream) {
+  NvtxRange nv("launch", 0, kernel_id);
   if (!h || !args) return DSR_ERR_INVALID;
   if (n == 0) return DSR_OK;
   LaunchCtx c = ctx(h, stream);

@@ -28,11 +28,11 @@ constexpr int kCompactThreads = 256;
 // Prologue driven from the nested level (Alg. 5's recursion, and
 // the paper's atomic cursor), so its cost follows the allocated blocks,
 // not the heap size M: a persistent grid of warps strides over the
-// level-1 containers of allocated[T]; a zero level-1 word (64 leaf words,
-// 4096 blocks) costs one load.  For a non-zero one, lane l reads leaf words
-// l and l + 32 (only those whose level-1 bit is set), the warp prefix-sums
-// their popcounts, reserves its range of R with ONE atomicAdd, and expands the
-// leaf words into R cooperatively (lane j writes bit j / j + 32 of each word:
+// halves of the level-1 containers of allocated[T]; a zero half (32 leaf
+// words, 2048 blocks) costs one load.  For a non-zero one, lane l reads leaf
+// word l (only if its level-1 bit is set), the warp prefix-sums the
+// popcounts, reserves its range of R with ONE atomicAdd, and expands the leaf
+// words into R cooperatively (lane j writes bit j / j + 32 of each word:
 // coalesced).  snapshot: iter_bm[b] = alloc_bm[b] & valid(N_T) for the same
 // blocks (C12) as a separate batch of independent coalesced loads (inside
 // the expansion each word's load -> store chain would serialise the warp).
@@ -44,19 +44,21 @@ static __global__ void __launch_bounds__(kCompactThreads) k_compact(DevHeap h, u
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t valid = h.types[T].valid;
-  for (uint64_t i1 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i1 < n1; i1 += nw) {
+  // work item = half a level-1 container: 32 leaf words, lane l <-> leaf word l
+  for (uint64_t it = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < 2 * n1; it += nw) {
+    const uint64_t i1 = it >> 1;
+    const uint32_t half = (uint32_t)(it & 1);
     uint64_t w1;
     if (ab.nlevels > 1) {
       w1 = __ldg((const unsigned long long*)ab.lvl[1] + i1);
     } else {                                                       // one level: every leaf word (nwords <= 64)
       w1 = nwords >= 64 ? ~0ull : ((1ull << nwords) - 1ull);
     }
-    if (w1 == 0) continue;
-    const uint64_t base_word = i1 * 64;
-    const uint64_t wa = ((w1 >> lane) & 1ull) ? __ldg((const unsigned long long*)ab.lvl[0] + base_word + lane) : 0ull;
-    const uint64_t wb = ((w1 >> (lane + 32)) & 1ull) ? __ldg((const unsigned long long*)ab.lvl[0] + base_word + lane + 32)
-                                                      : 0ull;
-    const uint32_t ca = __popcll(wa), c = ca + __popcll(wb);
+    const uint32_t w32 = (uint32_t)(w1 >> (32 * half));
+    if (w32 == 0) continue;
+    const uint64_t word = i1 * 64 + 32 * half + lane;
+    const uint64_t wl = ((w32 >> lane) & 1u) ? __ldg((const unsigned long long*)ab.lvl[0] + word) : 0ull;
+    const uint32_t c = __popcll(wl);
     uint32_t incl = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -68,64 +70,53 @@ static __global__ void __launch_bounds__(kCompactThreads) k_compact(DevHeap h, u
     uint32_t base = 0;
     if (lane == 0) base = atomicAdd((unsigned int*)&h.ctrl[CTRL_RCOUNT], total);
     base = __shfl_sync(0xffffffffu, base, 0);
-    const uint32_t offa = base + incl - c, offb = offa + ca;
-    // expansion: leaf word k (= lane k % 32's word a or b) -> its blocks, lane j takes bits j and j + 32
-    uint32_t srcs = __ballot_sync(0xffffffffu, wa != 0), srcs_b = __ballot_sync(0xffffffffu, wb != 0);
-    for (int half = 0; half < 2; ++half) {
-      uint32_t m = half ? srcs_b : srcs;
-      while (m) {
-        const uint32_t k = __ffs(m) - 1;
-        m &= m - 1;
-        const uint64_t wk = shfl64(0xffffffffu, half ? wb : wa, k);
-        const uint32_t off = __shfl_sync(0xffffffffu, half ? offb : offa, k);
-        const uint64_t bw = (base_word + k + 32u * half) * 64;           // first block of leaf word
+    const uint32_t off = base + incl - c;
+    const uint32_t srcs = __ballot_sync(0xffffffffu, wl != 0);
+    // expansion: leaf word k -> its blocks, lane j takes bits j and j + 32 (coalesced R stores)
+    uint32_t m = srcs;
+    while (m) {
+      const uint32_t k = __ffs(m) - 1;
+      m &= m - 1;
+      const uint64_t wk = shfl64(0xffffffffu, wl, k);
+      const uint32_t ok = __shfl_sync(0xffffffffu, off, k);
+      const uint64_t bw = (i1 * 64 + 32 * half + k) * 64;                // first block of leaf word k
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const uint32_t bit = lane + 32 * hh;
-          if ((wk >> bit) & 1ull) h.R[off + __popcll(wk & ((1ull << bit) - 1ull))] = (uint32_t)(bw + bit);
-        }
+      for (int hh = 0; hh < 2; ++hh) {
+        const uint32_t bit = lane + 32 * hh;
+        if ((wk >> bit) & 1ull) h.R[ok + __popcll(wk & ((1ull << bit) - 1ull))] = (uint32_t)(bw + bit);
       }
     }
     if (snapshot) {
-      // iteration bitmaps of the same blocks: rows of 32 consecutive u64 per
-      // step, 8 rows' loads in flight before their stores
-      for (int half = 0; half < 2; ++half) {
-        uint32_t m = half ? srcs_b : srcs;
-        while (m) {
-          uint64_t v[8], wkk[8];
-          uint32_t ks[8];
-          int n = 0;
+      // iteration bitmaps of the same blocks: rows of 32 consecutive u64,
+      // 8 leaf words' loads in flight before their stores
+      m = srcs;
+      while (m) {
+        uint64_t v[8][2], wkk[8];
+        uint32_t ks[8];
+        uint32_t n = 0;
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            ks[u] = 0;
-            wkk[u] = 0;
-            v[u] = 0;
-            if (m) {
-              ks[u] = __ffs(m) - 1;
-              m &= m - 1;
-              n = u + 1;
-            }
-          }
+        for (int u = 0; u < 8; ++u) {
+          ks[u] = m ? (uint32_t)(__ffs(m) - 1) : 0u;
+          if (m) { m &= m - 1; n = u + 1; }
+          wkk[u] = shfl64(0xffffffffu, wl, ks[u]);
+          if ((uint32_t)u >= n) wkk[u] = 0;
+        }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            if (u < n) {
-              wkk[u] = shfl64(0xffffffffu, half ? wb : wa, ks[u]);
-            }
-          }
+        for (int u = 0; u < 8; ++u) {
+          const uint64_t bw = (i1 * 64 + 32 * half + ks[u]) * 64;
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
+            const uint32_t bit = lane + 32 * hh;
+            v[u][hh] = ((wkk[u] >> bit) & 1ull) ? __ldg((const unsigned long long*)h.alloc_bm + bw + bit) : 0ull;
+          }
+        }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const uint32_t bit = lane + 32 * hh;
-              const uint64_t b = (base_word + ks[u] + 32u * half) * 64 + bit;
-              v[u] = (u < n && ((wkk[u] >> bit) & 1ull)) ? __ldg((const unsigned long long*)h.alloc_bm + b) : 0ull;
-            }
+        for (int u = 0; u < 8; ++u) {
+          const uint64_t bw = (i1 * 64 + 32 * half + ks[u]) * 64;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const uint32_t bit = lane + 32 * hh;
-              const uint64_t b = (base_word + ks[u] + 32u * half) * 64 + bit;
-              if (u < n && ((wkk[u] >> bit) & 1ull)) h.iter_bm[b] = v[u] & valid;
-            }
+          for (int hh = 0; hh < 2; ++hh) {
+            const uint32_t bit = lane + 32 * hh;
+            if ((wkk[u] >> bit) & 1ull) h.iter_bm[bw + bit] = v[u][hh] & valid;
           }
         }
       }

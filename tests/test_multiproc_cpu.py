@@ -151,3 +151,26 @@ def test_wator_halo_exchange_routes_segments(world):
             assert (h[i:i + n] == 10 * up + 2).all(), seg
             assert (h[i + n:i + 2 * n] == 10 * down + 1).all(), seg
             assert (h[o:o + n] == 10 * r + 1).all()              # out segments untouched
+
+
+def test_bench_self_spawns_ranks_dry_run():
+    """`python bench.py --gpus 2` (no torchrun environment) re-launches itself
+    under torch.distributed.run with two ranks; the dry run (gloo, no GPU work)
+    goes through the same rank aggregation: n_gpus = 2, work summed over the
+    ranks, time = the max over ranks (1 + rank ms)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR",
+                                                            "MASTER_PORT")}
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--dry-run", "--steps", "3",
+                        "--warmup", "3"], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1                                     # rank 0 alone prints
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["dry_run"]
+    assert d["ms_per_step"] == 2.0
+    assert d["value"] == 2 * ((1 << 26) + (1 << 25)) / 2e-3
