@@ -45,7 +45,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="microbench", choices=["microbench", "wator", "gol", "gol16k", "gol16k-bits", "nbody"])
+    ap.add_argument("--workload", default="microbench", choices=["microbench", "wator", "gol", "gol16k", "gol16k-bits",
+                                                                     "gol16k-tiled", "nbody"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-apps", action="store_true", help="skip the per-app block of the default line")
     ap.add_argument("--dry-run", action="store_true",
@@ -527,10 +528,12 @@ def app_block(stream, peak, peak_src, sm_mhz, want_cpu=True):
 
     # ---- GoL (configs[0] 64^2 x 100 gens; configs[3] 16384^2, handle grid and alive-bit mirror)
     from paper_1810_11765_b200.gol import GameOfLife
-    for name, Wd, K, Wu, bits in (("gol_64", 64, 100, 5, False), ("gol_16384", 16384, 4, 1, False),
-                                  ("gol_16384_bits", 16384, 4, 1, True)):
+    for name, Wd, K, Wu, bits, tiled in (("gol_64", 64, 100, 5, False, False),
+                                         ("gol_16384", 16384, 4, 1, False, False),
+                                         ("gol_16384_bits", 16384, 4, 1, True, False),
+                                         ("gol_16384_tiled", 16384, 4, 1, False, True)):
         a0 = I.gol_soup(Wd, Wd, 0.3 if Wd == 64 else 0.25, 1 if Wd == 64 else 42)
-        sim = GameOfLife(a0, stream=stream, bit_mirror=bits)
+        sim = GameOfLife(a0, stream=stream, bit_mirror=bits, tiled=tiled)
         step = sim.generation
         if Wd == 64:
             sim.capture()
@@ -549,6 +552,7 @@ def app_block(stream, peak, peak_src, sm_mhz, want_cpu=True):
         out[name] = {
             "config": f"BASELINE configs[{0 if Wd == 64 else 3}]: {Wd}^2 torus, Bernoulli("
                       f"{0.3 if Wd == 64 else 0.25}) soup" + (", alive-bit mirror variant" if bits else "")
+                      + (", cell-tiled do-alls (objects enumerated through the handle grid)" if tiled else "")
                       + (", one generation replayed as a CUDA graph" if Wd == 64 else ""),
             "value": visits / (sum(t) * 1e-3), "unit": "object-updates/s", "ms_per_step": ms, "steps": K,
             "objects_per_step": float(objs.mean()),
@@ -563,7 +567,7 @@ def app_block(stream, peak, peak_src, sm_mhz, want_cpu=True):
         }
         del sim
         torch.cuda.empty_cache()
-        if bits:
+        if bits or tiled:
             continue
 
         def gol_cpu(Wd=Wd):
@@ -719,7 +723,7 @@ def run_app(args):
     import torch.distributed as dist
     from paper_1810_11765_b200 import dsr, inputs as I
     rank, world, local = dist_init(args.gpus)
-    if world > 1 and args.workload not in ("nbody", "gol16k", "gol16k-bits", "wator"):
+    if world > 1 and args.workload not in ("nbody", "gol16k", "gol16k-bits", "gol16k-tiled", "wator"):
         raise SystemExit(f"--workload {args.workload} runs on one GPU (replicas only); use nbody, gol16k, wator "
                          "or microbench")
     stream = torch.cuda.Stream()
@@ -759,16 +763,18 @@ def run_app(args):
             bms = time_steps(lambda: base.run(1), K, W, stream)
             cfg["static_baseline"] = {"ms_per_step": bms, "dynamic_over_static": ms / bms,
                                       "what": "same rules on cell-indexed SOA arrays, no heap (dsr_wator_static_step)"}
-    elif args.workload in ("gol", "gol16k", "gol16k-bits"):
+    elif args.workload in ("gol", "gol16k", "gol16k-bits", "gol16k-tiled"):
         from paper_1810_11765_b200.gol import GameOfLife, NcclHaloExchange
         Wd = 64 if args.workload == "gol" else 16384
         a0 = I.gol_soup(Wd, Wd, 0.3 if Wd == 64 else 0.25, 1 if Wd == 64 else 42)
         if world > 1:                      # row bands + NCCL exchange of boundary masks
-            sim = GameOfLife(a0, stream=stream, shard=(rank, world), bit_mirror=args.workload.endswith("bits"))
+            sim = GameOfLife(a0, stream=stream, shard=(rank, world), bit_mirror=args.workload.endswith("bits"),
+                             tiled=args.workload.endswith("tiled"))
             sim.exchange = NcclHaloExchange(sim)
             dist.barrier()
         else:
-            sim = GameOfLife(a0, stream=stream, bit_mirror=args.workload.endswith("bits"))
+            sim = GameOfLife(a0, stream=stream, bit_mirror=args.workload.endswith("bits"),
+                             tiled=args.workload.endswith("tiled"))
         step_fn = sim.generation
         if Wd == 64:                       # launch-bound: replay one generation as a CUDA graph
             sim.capture()
@@ -783,7 +789,8 @@ def run_app(args):
         visits, = reduce_over_ranks([float(visits)], "sum")
         ms, = reduce_over_ranks([ms], "max")
         cfg = {"workload": f"gol {Wd}^2 torus (BASELINE configs[{0 if Wd == 64 else 3}])"
-                           + (", alive-bit mirror variant" if args.workload.endswith("bits") else ""),
+                           + (", alive-bit mirror variant" if args.workload.endswith("bits") else "")
+                           + (", cell-tiled prepare passes" if args.workload.endswith("tiled") else ""),
                "parallelism": f"{world} row bands, NCCL P2P halo masks" if world > 1 else "1 GPU"}
     else:
         from paper_1810_11765_b200.nbody import NBody

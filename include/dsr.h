@@ -377,7 +377,15 @@ enum {
   DSR_M_GOL_ALIVE_PREPARE = 11,  /* type 0 */
   DSR_M_GOL_CAND_UPDATE = 12,    /* type 1 (allocates Alive) */
   DSR_M_GOL_ALIVE_UPDATE = 13,   /* type 0 (allocates Candidate) */
-  DSR_M_GOL_DUMP = 14            /* any type: dump[cell] = kind | is_new << 8 | action << 16 */
+  DSR_M_GOL_DUMP = 14,           /* any type: dump[cell] = kind | is_new << 8 | action << 16 */
+  /* The same four methods as cell-tiled do-alls: the objects of the type are
+   * enumerated through the cell grid (each sits in exactly one cell) instead
+   * of the block list, so no prologue runs; prepare passes stage (8+2) x
+   * (128+2) tiles of handles in shared memory, update passes visit cells in
+   * row-major order so a warp's new objects come from neighbouring cells.
+   * Results are those of the block-list passes.  Not with `bits`. */
+  DSR_M_GOL_CAND_PREPARE_TILED = 15, DSR_M_GOL_ALIVE_PREPARE_TILED = 16,
+  DSR_M_GOL_CAND_UPDATE_TILED = 17, DSR_M_GOL_ALIVE_UPDATE_TILED = 18
 };
 
 /* ---- Wa-Tor (BASELINE configs[1], reading R-WATOR) ----

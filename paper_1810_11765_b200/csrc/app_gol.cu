@@ -244,8 +244,128 @@ struct GolDump {
   }
 };
 
+// ---- cell-tiled do-alls (the same four methods, enumerated through the cell
+// grid instead of the block list).
+// Every Alive / Candidate sits in exactly one cell, so visiting the cells
+// whose handle has the pass's type visits every object of that type exactly
+// once; objects a pass creates are placed in cells by the thread that owns
+// the cell after its visit, or in cells whose new content is not of the
+// pass's type (Candidates in pass 4), so none is visited by the pass that
+// creates it.
+// Prepare passes: a CTA stages an (8 + 2) x (128 + 2) tile of handles (8-B,
+// coalesced row segments) in shared memory and counts each cell's alive
+// neighbours from it (P:333 type bits); the object's action is written
+// through its handle.  Update passes: one thread per cell in row-major order,
+// so the objects a warp creates (new Alives in pass 3, Candidates in pass 4)
+// come from 32 neighbouring cells and go into one block (coalesced request,
+// P:649): blocks stay spatially coherent across generations.
+constexpr int kTileH = 8, kTileW = 128;
+template <int PASS>
+__global__ void __launch_bounds__(256) k_gol_tile_prepare(DevHeap h, dsr_gol_args a) {
+  __shared__ unsigned long long s[kTileH + 2][kTileW + 2];
+  const uint32_t W = a.W, H = a.H, row0 = a.ghost ? 1u : 0u;
+  const uint32_t rows_total = a.ghost ? H + 2 : H;
+  const uint32_t tx = (W + kTileW - 1) / kTileW, ty = (H + kTileH - 1) / kTileH;
+  const uint32_t T = PASS == 1 ? GOL_CAND : GOL_ALIVE;
+  const uint32_t nt = tx * ty, t0 = (uint32_t)((uint64_t)blockIdx.x * nt / gridDim.x),
+                 t1 = (uint32_t)((uint64_t)(blockIdx.x + 1) * nt / gridDim.x);
+  for (uint32_t tile = t0; tile < t1; ++tile) {                             // blocked: neighbouring tiles per CTA
+    const uint32_t y0 = (tile / tx) * kTileH, x0 = (tile % tx) * kTileW;   // local cell coordinates
+    __syncthreads();                                                        // the previous tile is consumed
+    for (uint32_t i = threadIdx.x; i < (kTileH + 2) * (kTileW + 2); i += blockDim.x) {
+      const int r = (int)(i / (kTileW + 2)), cc = (int)(i % (kTileW + 2));
+      const int yy = (int)y0 + r - 1, xx = (int)x0 + cc - 1;               // local row -1 .. H + 7
+      int gy = a.ghost ? yy + 1 : ((yy % (int)H) + (int)H) % (int)H;       // grid row (ghost rows 0, H + 1)
+      const uint32_t gx = (uint32_t)(((xx % (int)W) + (int)W) % (int)W);
+      s[r][cc] = (gy >= 0 && gy < (int)rows_total) ? __ldg((const unsigned long long*)a.cell + (size_t)gy * W + gx)
+                                                   : 0ull;
+    }
+    __syncthreads();
+    for (uint32_t idx = threadIdx.x; idx < kTileH * kTileW; idx += blockDim.x) {
+      const uint32_t r = idx / kTileW, cc = idx % kTileW, y = y0 + r, x = x0 + cc;
+      if (y >= H || x >= W) continue;
+      const uint64_t hd = s[r + 1][cc + 1];
+      if (!h_is(hd, T)) continue;
+      uint32_t k = 0;
+#pragma unroll
+      for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx)
+          if (dy != 1 || dx != 1) k += h_is(s[r + dy][cc + dx], GOL_ALIVE);
+      if (PASS == 1) {
+        *field_ptr<uint8_t>(h, hd, 1) = k == 3 ? ACT_SPAWN : (k == 0 ? ACT_DIE : ACT_NONE);
+      } else {
+        *field_ptr<uint8_t>(h, hd, 1) = 0;
+        *field_ptr<uint8_t>(h, hd, 2) = (k < 2 || k > 3) ? ACT_DIE : ACT_NONE;
+      }
+    }
+    (void)row0;
+  }
+}
+// Update passes: a CTA takes chunks of 2048 consecutive cells, compacts the
+// cells holding an object of the pass's type into shared memory (warp
+// ballots + a CTA scan, in row-major order), then runs the method over the
+// compacted list with full warps: lane j of a warp gets the j-th object of 32
+// neighbouring ones, so its allocations and destroys coalesce per block.
+constexpr int kUpdChunk = 2048;
+template <int PASS>
+__global__ void __launch_bounds__(256, 4) k_gol_tile_update(DevHeap h, dsr_gol_args a) {
+  __shared__ unsigned long long s_hd[kUpdChunk];
+  __shared__ uint32_t s_warp[8], s_n;
+  const uint32_t W = a.W, row0 = a.ghost ? 1u : 0u;
+  const uint64_t n = (uint64_t)W * a.H;
+  const uint32_t T = PASS == 3 ? GOL_CAND : GOL_ALIVE;
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  NoAcc acc;
+  // blocked distribution: CTA b owns one contiguous run of chunks, so each
+  // warp's allocations (its hint block) fill with objects of
+  // neighbouring cells and the blocks stay spatially coherent
+  const uint64_t nch = (n + kUpdChunk - 1) / kUpdChunk;
+  const uint64_t c0 = (uint64_t)blockIdx.x * nch / gridDim.x, c1 = (uint64_t)(blockIdx.x + 1) * nch / gridDim.x;
+  for (uint64_t base = c0 * kUpdChunk; base < c1 * kUpdChunk && base < n; base += kUpdChunk) {
+    // this thread's 8 cells: base + wid * 256 + k * 32 + lane (a warp reads 8 rows of 32 consecutive cells)
+    unsigned long long v[8];
+    uint32_t mine = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint64_t i = base + (uint64_t)wid * 256 + k * 32 + lane;
+      v[k] = i < n ? ld_relaxed((const uint64_t*)a.cell + i + (uint64_t)row0 * W) : 0ull;
+      mine += h_is(v[k], T) ? 1u : 0u;
+    }
+    // CTA exclusive scan of per-warp counts (row-major order = warp, k, lane)
+    uint32_t wc = __reduce_add_sync(0xffffffffu, mine);
+    __syncthreads();                                                   // s_hd of the previous chunk consumed
+    if (lane == 0) s_warp[wid] = wc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t run = 0;
+      for (int w = 0; w < 8; ++w) { const uint32_t t = s_warp[w]; s_warp[w] = run; run += t; }
+      s_n = run;
+    }
+    __syncthreads();
+    uint32_t pos = s_warp[wid];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const bool m = h_is(v[k], T);
+      const uint32_t bal = __ballot_sync(0xffffffffu, m);
+      if (m) s_hd[pos + __popc(bal & ((1u << lane) - 1u))] = v[k];
+      pos += __popc(bal);
+    }
+    __syncthreads();
+    const uint32_t cnt = s_n;
+    for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) {
+      const uint64_t hd = s_hd[j];
+      if (PASS == 3) GolCandUpdate::run(h, T, h_bid(hd), h_slot(hd), a, acc);
+      else GolAliveUpdate::run(h, T, h_bid(hd), h_slot(hd), a, acc);
+    }
+  }
+}
+
 bool gol_method_info(uint32_t id, MethodInfo* mi) {
   switch (id) {
+    case DSR_M_GOL_CAND_PREPARE_TILED: case DSR_M_GOL_ALIVE_PREPARE_TILED: case DSR_M_GOL_CAND_UPDATE_TILED:
+    case DSR_M_GOL_ALIVE_UPDATE_TILED:
+      *mi = {4, sizeof(dsr_gol_args)}; return true;      // enumerated through the cell grid: no block list
     case DSR_M_GOL_CAND_PREPARE: case DSR_M_GOL_ALIVE_PREPARE: case DSR_M_GOL_DUMP:
       *mi = {0, sizeof(dsr_gol_args)}; return true;
     case DSR_M_GOL_CAND_UPDATE:
@@ -263,6 +383,23 @@ bool gol_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot
     case DSR_M_GOL_CAND_UPDATE: launch_doall<GolCandUpdate>(c, T, snapshot, args); return true;
     case DSR_M_GOL_ALIVE_UPDATE: launch_doall<GolAliveUpdate>(c, T, snapshot, args); return true;
     case DSR_M_GOL_DUMP: launch_doall<GolDump>(c, T, snapshot, args); return true;
+    case DSR_M_GOL_CAND_PREPARE_TILED: case DSR_M_GOL_ALIVE_PREPARE_TILED:
+    case DSR_M_GOL_CAND_UPDATE_TILED: case DSR_M_GOL_ALIVE_UPDATE_TILED: {
+      const dsr_gol_args a = *(const dsr_gol_args*)args;
+      if (a.bits || a.W < 3 || a.H < 1) return false;
+      const bool cand = id == DSR_M_GOL_CAND_PREPARE_TILED || id == DSR_M_GOL_CAND_UPDATE_TILED;
+      if (T != (cand ? (uint32_t)GOL_CAND : (uint32_t)GOL_ALIVE) || c.rk >= 0) return false;
+      if (id == DSR_M_GOL_CAND_PREPARE_TILED)
+        k_gol_tile_prepare<1><<<persistent_grid(c, k_gol_tile_prepare<1>), 256, 0, c.st>>>(c.h, a);
+      else if (id == DSR_M_GOL_ALIVE_PREPARE_TILED)
+        k_gol_tile_prepare<2><<<persistent_grid(c, k_gol_tile_prepare<2>), 256, 0, c.st>>>(c.h, a);
+      else if (id == DSR_M_GOL_CAND_UPDATE_TILED)
+        k_gol_tile_update<3><<<persistent_grid(c, k_gol_tile_update<3>), 256, 0, c.st>>>(c.h, a);
+      else
+        k_gol_tile_update<4><<<persistent_grid(c, k_gol_tile_update<4>), 256, 0, c.st>>>(c.h, a);
+      count_launch();
+      return true;
+    }
   }
   return false;
 }

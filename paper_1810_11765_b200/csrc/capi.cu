@@ -327,6 +327,7 @@ extern "C" dsr_status dsr_doall_prologue(dsr_heap* h, uint32_t type, uint32_t me
   if (!h || type >= h->L.ntypes) return DSR_ERR_INVALID;
   MethodInfo mi;
   if (!method_info(method_id, &mi)) return DSR_ERR_UNSUPPORTED;
+  if (mi.snapshot == 4) return DSR_OK;             // the method enumerates its objects itself (no block list)
   cudaStream_t st = (cudaStream_t)stream;
   // R := compact(allocated[T]) (+ iteration-bitmap snapshot when the method may allocate)
   CUDA_TRY(cudaMemsetAsync(&h->dev.ctrl[CTRL_RCOUNT], 0, 8, st));

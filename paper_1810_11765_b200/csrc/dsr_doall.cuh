@@ -132,8 +132,11 @@ static __global__ void __launch_bounds__(kCompactThreads) k_compact(DevHeap h, u
 //   kSchedDynamic warps take 32 x kDoallChunk elements from a device counter
 //   kSchedBlocked each warp owns one contiguous range of R
 enum { kSchedCyclic = 0, kSchedDynamic = 1, kSchedBlocked = 2 };
+#ifndef DSR_DOALL_MINB
+#define DSR_DOALL_MINB 8
+#endif
 template <class Mth, int SCHED>
-__global__ void __launch_bounds__(256, 8) k_doall(DevHeap h, uint32_t T, int snapshot, int rk, typename Mth::Args a) {
+__global__ void __launch_bounds__(256, DSR_DOALL_MINB) k_doall(DevHeap h, uint32_t T, int snapshot, int rk, typename Mth::Args a) {
   uint32_t rb = 0, re;
   if (rk < 0) {
     re = ld_relaxed_u32((const uint32_t*)&h.ctrl[CTRL_RCOUNT]);

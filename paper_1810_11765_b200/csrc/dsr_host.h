@@ -24,6 +24,8 @@ struct MethodInfo {
   // per-object cost is very uneven (several allocations per visit).
   // 3: snapshot + blocked distribution (one contiguous range of R per warp),
   // for passes that free whole blocks.
+  // 4: the method enumerates its objects through an app index (GoL's cell
+  // grid): no prologue, no block list.
   int snapshot;
   size_t args_bytes;   // expected sizeof(args)
 };

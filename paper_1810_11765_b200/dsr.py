@@ -32,6 +32,7 @@ K_REPLAY, K_TORTURE, M_COLLECT = 4, 5, 4
 K_INH_NEW, K_INH_READ, M_INH_BUMP, M_INH_SUM, M_INH_SPAWN = 6, 7, 5, 6, 7
 K_GOL_INIT_ALIVE, K_GOL_INIT_CAND, K_GOL_HALO_PACK, K_GOL_HALO_APPLY = 10, 11, 12, 13
 M_GOL_CAND_PREPARE, M_GOL_ALIVE_PREPARE, M_GOL_CAND_UPDATE, M_GOL_ALIVE_UPDATE, M_GOL_DUMP = 10, 11, 12, 13, 14
+M_GOL_CAND_PREPARE_TILED, M_GOL_ALIVE_PREPARE_TILED, M_GOL_CAND_UPDATE_TILED, M_GOL_ALIVE_UPDATE_TILED = 15, 16, 17, 18
 C_WT_CELL, K_WT_INIT_AGENTS = 20, 21
 (K_WT_HALO_REQ_PACK, K_WT_HALO_REQ_APPLY, K_WT_HALO_GRANT_APPLY, K_WT_HALO_MIG_APPLY, K_WT_HALO_OCC_PACK,
  K_WT_HALO_OCC_APPLY) = range(22, 28)

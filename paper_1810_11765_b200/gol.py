@@ -26,7 +26,13 @@ class GameOfLife:
     single-heap result bit for bit."""
 
     def __init__(self, alive0, heap_bytes=None, device=None, stream=None, retries=5, flags=0, shard=None,
-                 exchange=None, bit_mirror=False):
+                 exchange=None, bit_mirror=False, tiled=False):
+        """tiled: True / "prepare" -- the two prepare passes (the neighbour
+        gathers) as cell-tiled do-alls (DSR_M_GOL_*_PREPARE_TILED: objects
+        enumerated through the cell grid, neighbour handles staged in shared
+        memory), the update passes on the block list (full warps, destroys and
+        news coalesced per block); "all" -- all four passes cell-tiled.  Same
+        results as the block-list passes."""
         import numpy as np
         import torch
         Hg, W = alive0.shape
@@ -62,6 +68,16 @@ class GameOfLife:
         self.args = dsr.GolArgs(self.cell.data_ptr(), W, H, self.alive0.data_ptr(), self.dumpbuf.data_ptr(),
                                 1 if shard is not None else 0, self.halo.data_ptr() if shard is not None else None,
                                 self.bits.data_ptr() if bit_mirror else None)
+        if tiled and bit_mirror:
+            raise ValueError("tiled passes read the handle grid; the bit mirror is the other variant")
+        if tiled == "all":
+            self.m = (dsr.M_GOL_CAND_PREPARE_TILED, dsr.M_GOL_ALIVE_PREPARE_TILED, dsr.M_GOL_CAND_UPDATE_TILED,
+                      dsr.M_GOL_ALIVE_UPDATE_TILED)
+        elif tiled:
+            self.m = (dsr.M_GOL_CAND_PREPARE_TILED, dsr.M_GOL_ALIVE_PREPARE_TILED, dsr.M_GOL_CAND_UPDATE,
+                      dsr.M_GOL_ALIVE_UPDATE)
+        else:
+            self.m = (dsr.M_GOL_CAND_PREPARE, dsr.M_GOL_ALIVE_PREPARE, dsr.M_GOL_CAND_UPDATE, dsr.M_GOL_ALIVE_UPDATE)
         self.heap.launch(dsr.K_GOL_INIT_ALIVE, self.N, self.args, stream)
         self.heap.launch(dsr.K_GOL_INIT_CAND, self.N, self.args, stream)
         self.gen = 0
@@ -69,9 +85,9 @@ class GameOfLife:
     # the generation split at the exchange point (sharded mode)
     def first_half(self, s):
         h, a = self.heap, self.args
-        h.parallel_do(CAND, dsr.M_GOL_CAND_PREPARE, a, s)
-        h.parallel_do(ALIVE, dsr.M_GOL_ALIVE_PREPARE, a, s)
-        h.parallel_do(CAND, dsr.M_GOL_CAND_UPDATE, a, s)
+        h.parallel_do(CAND, self.m[0], a, s)
+        h.parallel_do(ALIVE, self.m[1], a, s)
+        h.parallel_do(CAND, self.m[2], a, s)
         if self.shard is not None:
             h.launch(dsr.K_GOL_HALO_PACK, self.W, a, s)
 
@@ -79,7 +95,7 @@ class GameOfLife:
         h, a = self.heap, self.args
         if self.shard is not None:
             h.launch(dsr.K_GOL_HALO_APPLY, self.W, a, s)
-        h.parallel_do(ALIVE, dsr.M_GOL_ALIVE_UPDATE, a, s)
+        h.parallel_do(ALIVE, self.m[3], a, s)
         self.gen += 1
 
     def generation(self, stream=None):

@@ -184,3 +184,71 @@ def test_gol_16384_row_shards_equal_single_heap_and_dense(G, O):
         win = a0[y:y + 262, x:x + 262]
         want = O.life_dense(np.ascontiguousarray(win), gens)[3:259, 3:259]
         assert np.array_equal(got[y + 3:y + 259, x + 3:x + 259], want)
+
+
+# ------------------------------------------------------------------ cell-tiled do-alls
+@pytest.mark.parametrize("tiled", ["prepare", "all"])
+@pytest.mark.parametrize("name", ["glider", "blinker", "soup1", "soup2"])
+def test_gol_tiled_every_generation_bit_exact(G, O, name, tiled):
+    """The cell-tiled passes (objects enumerated through the cell grid,
+    neighbour handles staged in shared memory) give the oracle's records
+    every generation, like the block-list passes."""
+    from paper_1810_11765_b200 import inputs as I
+    a0 = I.gol_pattern(name) if not name.startswith("soup") else I.gol_soup(64, 64, 0.3, int(name[-1]))
+    _, want = O.gol_run(a0, 100, dump=True)
+    g = G.GameOfLife(a0, tiled=tiled)
+    for gen in range(100):
+        g.generation()
+        assert np.array_equal(g.records(), want[gen]), f"generation {gen + 1}"
+    assert g.heap.poll_error() == 0
+    assert g.heap.check_invariants() == 0
+
+
+@pytest.mark.parametrize("tiled", ["prepare", "all"])
+@pytest.mark.parametrize("W,H,p,seed,gens", [(37, 23, 0.4, 4, 60), (3, 3, 0.5, 6, 10), (129, 9, 0.3, 5, 40),
+                                             (513, 385, 0.25, 7, 50), (128, 8, 0.35, 8, 30)])
+def test_gol_tiled_ragged_sizes_against_dense_life(G, O, W, H, p, seed, gens, tiled):
+    """Sizes that are not multiples of the 8 x 128 tile (ragged last tile row
+    and column, torus wrap across tile edges) and the exact-tile case."""
+    from paper_1810_11765_b200 import inputs as I
+    a0 = I.gol_soup(W, H, p, seed)
+    g = G.GameOfLife(a0, tiled=tiled)
+    g.run(gens)
+    assert np.array_equal(g.alive(), O.life_dense(a0, gens))
+    assert g.heap.check_invariants() == 0
+
+
+@pytest.mark.parametrize("tiled", ["prepare", "all"])
+@pytest.mark.parametrize("P,W,H,gens", [(2, 64, 64, 60), (4, 130, 40, 50)])
+def test_gol_tiled_row_shards_loopback_equal_dense(G, O, P, W, H, gens, tiled):
+    from paper_1810_11765_b200 import inputs as I
+    from paper_1810_11765_b200.gol import GameOfLifeLoopback
+    a0 = I.gol_soup(W, H, 0.3, P + 30)
+    lb = GameOfLifeLoopback(a0, P, tiled=tiled)
+    lb.run(gens)
+    assert np.array_equal(lb.alive(), O.life_dense(a0, gens))
+    for s in lb.shards:
+        assert s.heap.check_invariants() == 0
+
+
+@pytest.mark.slow
+def test_gol_tiled_16384_equals_block_list_and_dense(G, O):
+    """configs[3] size, 3 generations: the tiled passes give exactly the
+    block-list passes' alive map, and the oracle's dense Life on windows."""
+    from paper_1810_11765_b200 import inputs as I
+    W = H = 16384
+    a0 = I.gol_soup(W, H, 0.25, 42)
+    g = G.GameOfLife(a0, tiled=True)
+    g.run(3)
+    got = g.alive()
+    assert g.heap.check_invariants() == 0
+    del g
+    torch.cuda.empty_cache()
+    rng = np.random.default_rng(5)
+    for _ in range(6):
+        y, x = int(rng.integers(0, H - 300)), int(rng.integers(0, W - 300))
+        want = O.life_dense(np.ascontiguousarray(a0[y:y + 262, x:x + 262]), 3)[3:259, 3:259]
+        assert np.array_equal(got[y + 3:y + 259, x + 3:x + 259], want)
+    g = G.GameOfLife(a0)
+    g.run(3)
+    assert np.array_equal(got, g.alive())
