@@ -149,6 +149,67 @@ struct WtCellDecide {
   }
 };
 
+// The two Cell methods in quad form (k_doall_quad, reading C31):
+// a lane owns 4 consecutive cells of a block; each u8 request column is one
+// 32-bit word per quad (a warp's request is 128 B = 4 sectors instead of 32 B
+// byte loads), stores only to the visited slots.
+struct WtCellPrepareQ {
+  typedef dsr_wator_args Args;
+  DSR_NO_ACC
+  static __device__ __forceinline__ void run4(const DevHeap& h, uint32_t T, uint32_t b, uint32_t q, uint32_t m4,
+                                              const Args&, Acc&) {
+    uint8_t* base = h.data + (size_t)b * h.block_bytes + 4u * q;
+#pragma unroll
+    for (uint32_t k = 0; k < 5; ++k) {
+      uint8_t* col = base + h.types[T].col_off[2 + k];
+      if (m4 == 0xFu) {
+        *reinterpret_cast<uint32_t*>(col) = 0u;                 // columns are 16-B aligned (R-LAYOUT)
+      } else {
+#pragma unroll
+        for (uint32_t j = 0; j < 4; ++j)
+          if ((m4 >> j) & 1u) col[j] = 0;
+      }
+    }
+  }
+};
+template <int PHASE>
+struct WtCellDecideQ {
+  typedef dsr_wator_args Args;
+  DSR_NO_ACC
+  static __device__ __forceinline__ void run4(const DevHeap& h, uint32_t T, uint32_t b, uint32_t q, uint32_t m4,
+                                              const Args& a, Acc& acc) {
+    const uint8_t* base = h.data + (size_t)b * h.block_bytes + 4u * q;
+    uint32_t r[5];
+#pragma unroll
+    for (uint32_t k = 0; k < 5; ++k) r[k] = __ldg(reinterpret_cast<const uint32_t*>(base + h.types[T].col_off[2 + k]));
+    // slots with a request and no "own agent stays" (req[4]) among the visited ones
+    uint32_t todo = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < 4; ++j) {
+      const uint32_t any = ((r[0] | r[1] | r[2] | r[3]) >> (8 * j)) & 0xFFu;
+      if (((m4 >> j) & 1u) && any && !((r[4] >> (8 * j)) & 0xFFu)) todo |= 1u << j;
+    }
+    while (todo) {
+      const uint32_t j = __ffs(todo) - 1;
+      todo &= todo - 1;
+      uint32_t D[4], nd = 0;
+#pragma unroll
+      for (uint32_t d = 0; d < 4; ++d)
+        if ((r[d] >> (8 * j)) & 0xFFu) D[nd++] = d;
+      const uint32_t id = *reinterpret_cast<const uint32_t*>(base + h.types[T].col_off[0] + 12u * q + 4u * j);
+      if (!wt_local(a, id)) continue;                                 // ghost cell: its owner decides
+      const uint32_t d = wt_pick(D, nd, rng_key(a.seed, wt_step(a), PHASE, wt_gid(a, id)));
+      const uint32_t nb = wt_nbr(a, id, d);
+      if (!wt_local(a, nb)) {                                         // a neighbour shard's agent: grant it
+        wt_halo(a, DSR_WT_HALO_GRANT_OUT(a.W), nb == id - a.W ? 0 : 1)[nb % a.W] = 1;
+        continue;
+      }
+      const uint64_t ag = *wt_agent(h, a, nb);
+      *field_ptr<uint32_t>(h, ag, 1) = id;                            // Fish/Shark.target (field 1 of both)
+    }
+  }
+};
+
 struct WtFishPrepare {
   typedef dsr_wator_args Args;
   DSR_NO_ACC
@@ -361,12 +422,21 @@ bool wt_method_info(uint32_t id, MethodInfo* mi) {
 
 bool wt_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot, const void* args) {
   switch (id) {
-    case DSR_M_WT_CELL_PREPARE: launch_doall<WtCellPrepare>(c, T, snapshot, args); return true;
+    case DSR_M_WT_CELL_PREPARE:
+      if (c.h.flags & DSR_F_SCALAR_DOALL) launch_doall<WtCellPrepare>(c, T, snapshot, args);
+      else launch_doall_quad<WtCellPrepareQ>(c, T, snapshot, args);
+      return true;
     case DSR_M_WT_FISH_PREPARE: launch_doall<WtFishPrepare>(c, T, snapshot, args); return true;
-    case DSR_M_WT_CELL_DECIDE_FISH: launch_doall<WtCellDecide<PH_FISH_DEC>>(c, T, snapshot, args); return true;
+    case DSR_M_WT_CELL_DECIDE_FISH:
+      if (c.h.flags & DSR_F_SCALAR_DOALL) launch_doall<WtCellDecide<PH_FISH_DEC>>(c, T, snapshot, args);
+      else launch_doall_quad<WtCellDecideQ<PH_FISH_DEC>>(c, T, snapshot, args);
+      return true;
     case DSR_M_WT_FISH_UPDATE: launch_doall<WtFishUpdate>(c, T, snapshot, args); return true;
     case DSR_M_WT_SHARK_PREPARE: launch_doall<WtSharkPrepare>(c, T, snapshot, args); return true;
-    case DSR_M_WT_CELL_DECIDE_SHARK: launch_doall<WtCellDecide<PH_SHARK_DEC>>(c, T, snapshot, args); return true;
+    case DSR_M_WT_CELL_DECIDE_SHARK:
+      if (c.h.flags & DSR_F_SCALAR_DOALL) launch_doall<WtCellDecide<PH_SHARK_DEC>>(c, T, snapshot, args);
+      else launch_doall_quad<WtCellDecideQ<PH_SHARK_DEC>>(c, T, snapshot, args);
+      return true;
     case DSR_M_WT_SHARK_UPDATE: launch_doall<WtSharkUpdate>(c, T, snapshot, args); return true;
     case DSR_M_WT_DUMP: launch_doall<WtDump>(c, T, snapshot, args); return true;
   }
