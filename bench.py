@@ -569,6 +569,12 @@ def app_block(stream, peak, peak_src, sm_mhz, want_cpu=True):
         torch.cuda.empty_cache()
         if bits or tiled:
             continue
+        from paper_1810_11765_b200.gol import GameOfLifeStatic
+        base = GameOfLifeStatic(a0, stream=stream)
+        tb = timed_steps(lambda: base.run(1), K, Wu, stream)
+        out[name]["static_baseline"] = {"ms_per_step": sum(tb) / K, "dynamic_over_static": ms / (sum(tb) / K),
+                                        "what": "B3/S23 on a u8 cell grid, no objects (P:763, dsr_gol_static_step)"}
+        del base
 
         def gol_cpu(Wd=Wd):
             from oracle import oracle as O
@@ -681,6 +687,13 @@ def app_block(stream, peak, peak_src, sm_mhz, want_cpu=True):
     }
     del sim
     torch.cuda.empty_cache()
+    from paper_1810_11765_b200.nbody import NBodyStatic
+    base = NBodyStatic(st, merges=True, stream=stream, **I.NBODY_PARAMS)
+    tb = timed_steps(lambda: base.run(1), K, 3, stream)
+    out["nbody_65536"]["static_baseline"] = {"ms_per_step": sum(tb) / K, "dynamic_over_static": ms / (sum(tb) / K),
+                                             "what": "the same passes on id-indexed SOA arrays, no heap (P:763, "
+                                                     "dsr_nbody_static_step)"}
+    del base
 
     def nbody_cpu():
         from oracle import oracle as O

@@ -509,6 +509,33 @@ typedef struct {
  * for fish, then sharks) on `stream` (cudaStream_t as void*, NULL = default). */
 dsr_status dsr_wator_static_step(const dsr_wator_static_args* args, uint32_t steps, void* stream);
 
+/* ---- Static-allocation baseline of N-body ----
+ * The six passes of reading R-NBODY on id-indexed SOA device arrays, no heap:
+ *   S[4*id + {0,1,2,3}] = (x, y, m, 0)  (in/out; m = 0: dead id)
+ *   V[2*id + {0,1}]     = (vx, vy)      (in/out)
+ *   target, incoming    u32[n] scratch
+ *   scratch             f32, >= 2 * ceil(n / 4096) * n (all-pairs partials)
+ * The all-pairs passes are the heap version's kernels over S; the per-body
+ * passes repeat its operations in its order, so the state after any number of
+ * steps equals the heap version's (dsr_nbody_args runs) bit for bit.
+ * Caller-owned device memory; enqueues work on `stream` only. */
+typedef struct {
+  float* S; float* V; uint32_t* target; uint32_t* incoming; float* scratch;
+  float G, dt, eps, R;
+  uint32_t n;
+  uint32_t merges;      /* 0: App2 N-Body (force + move only) */
+} dsr_nbody_static_args;
+dsr_status dsr_nbody_static_step(const dsr_nbody_static_args* args, uint32_t steps, void* stream);
+
+/* ---- Static-allocation baseline of Game of Life (NEXT-4) ----
+ * B3/S23 on a W x H torus of u8 cells (0 dead, 1 alive): `cur` and `next`
+ * (device, W*H bytes each, caller-owned) are swapped every step; after the
+ * call the state is in `cur` (odd step counts end with one device copy).
+ * One kernel per generation, (8 + 2) x (128 + 2) cell tiles in shared memory.
+ * Equals the object version's alive map (and textbook Life) every step. */
+typedef struct { uint32_t W, H; uint8_t* cur; uint8_t* next; } dsr_gol_static_args;
+dsr_status dsr_gol_static_step(const dsr_gol_static_args* args, uint32_t steps, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

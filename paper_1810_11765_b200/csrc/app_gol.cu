@@ -424,4 +424,48 @@ bool gol_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* 
   return true;
 }
 
+// ---- static-allocation baseline: Life on a u8 cell grid, no objects
+__global__ void __launch_bounds__(256) k_gol_static(uint32_t W, uint32_t H, const uint8_t* cur, uint8_t* next) {
+  __shared__ uint8_t s[kTileH + 2][kTileW + 2];
+  const uint32_t tx = (W + kTileW - 1) / kTileW, ty = (H + kTileH - 1) / kTileH;
+  for (uint32_t tile = blockIdx.x; tile < tx * ty; tile += gridDim.x) {
+    const uint32_t y0 = (tile / tx) * kTileH, x0 = (tile % tx) * kTileW;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < (kTileH + 2) * (kTileW + 2); i += blockDim.x) {
+      const int r = (int)(i / (kTileW + 2)), cc = (int)(i % (kTileW + 2));
+      const uint32_t gy = (uint32_t)((((int)y0 + r - 1) % (int)H + (int)H) % (int)H);
+      const uint32_t gx = (uint32_t)((((int)x0 + cc - 1) % (int)W + (int)W) % (int)W);
+      s[r][cc] = __ldg(cur + (size_t)gy * W + gx);
+    }
+    __syncthreads();
+    for (uint32_t idx = threadIdx.x; idx < kTileH * kTileW; idx += blockDim.x) {
+      const uint32_t r = idx / kTileW, cc = idx % kTileW, y = y0 + r, x = x0 + cc;
+      if (y >= H || x >= W) continue;
+      const uint32_t k = s[r][cc] + s[r][cc + 1] + s[r][cc + 2] + s[r + 1][cc] + s[r + 1][cc + 2] + s[r + 2][cc] +
+                         s[r + 2][cc + 1] + s[r + 2][cc + 2];
+      next[(size_t)y * W + x] = (k == 3 || (k == 2 && s[r + 1][cc + 1])) ? 1 : 0;
+    }
+  }
+}
+
 }  // namespace dsr
+
+extern "C" dsr_status dsr_gol_static_step(const dsr_gol_static_args* a, uint32_t steps, void* stream) {
+  using namespace dsr;
+  if (!a || !a->cur || !a->next || a->W < 3 || a->H < 3) return DSR_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return DSR_ERR_CUDA;
+  const uint64_t tiles = (uint64_t)((a->W + kTileW - 1) / kTileW) * ((a->H + kTileH - 1) / kTileH);
+  const int g = (int)(tiles < (uint64_t)sms * 8 ? tiles : (uint64_t)sms * 8);
+  uint8_t *c = a->cur, *n = a->next;
+  for (uint32_t k = 0; k < steps; ++k) {
+    k_gol_static<<<g, 256, 0, st>>>(a->W, a->H, c, n);
+    count_launch();
+    uint8_t* t = c; c = n; n = t;
+  }
+  if (c != a->cur && cudaMemcpyAsync(a->cur, c, (size_t)a->W * a->H, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    return DSR_ERR_CUDA;
+  return cudaGetLastError() == cudaSuccess ? DSR_OK : DSR_ERR_CUDA;
+}

@@ -11,6 +11,8 @@
 // Merge bookkeeping (target / incoming) lives in id-indexed arrays so that the
 // same kernels serve one GPU and an id-range-sharded multi-GPU run (where S,
 // V and target are all-gathered between passes).
+#include <algorithm>
+#include <cstring>
 #include "dsr_host.h"
 
 namespace dsr {
@@ -149,10 +151,21 @@ __global__ void k_nb_force_sum(DevHeap h, dsr_nbody_args a) {
       ay += v.y;
     }
     const uint32_t b = h_bid(hd), s = h_slot(hd);
-    const float gm = a.G * bf<float>(h, b, s, NB_M);
-    bf<float>(h, b, s, NB_FX) = gm * ax;
-    bf<float>(h, b, s, NB_FY) = gm * ay;
+    const float gm = __fmul_rn(a.G, bf<float>(h, b, s, NB_M));
+    bf<float>(h, b, s, NB_FX) = __fmul_rn(gm, ax);
+    bf<float>(h, b, s, NB_FY) = __fmul_rn(gm, ay);
   }
+}
+
+// Per-body arithmetic with explicit rounding (no FMA contraction), so the
+// heap version and the static baseline below perform identical operations
+// whatever the compiler contracts in each kernel (bit-exact comparison).
+__device__ __forceinline__ float nb_step_v(float v, float f, float m, float dt) {
+  return __fadd_rn(v, __fmul_rn(__fdiv_rn(f, m), dt));
+}
+__device__ __forceinline__ float nb_step_p(float p, float v, float dt) { return __fadd_rn(p, __fmul_rn(v, dt)); }
+__device__ __forceinline__ float nb_mix(float m, float u, float mi, float ui, float mn) {
+  return __fdiv_rn(__fadd_rn(__fmul_rn(m, u), __fmul_rn(mi, ui)), mn);
 }
 
 struct NbMove {   // semi-implicit Euler, velocity first
@@ -160,12 +173,12 @@ struct NbMove {   // semi-implicit Euler, velocity first
   DSR_NO_ACC
   static __device__ __forceinline__ void run(const DevHeap& h, uint32_t, uint32_t b, uint32_t s, const Args& a, Acc&) {
     const float m = bf<float>(h, b, s, NB_M);
-    const float vx = bf<float>(h, b, s, NB_VX) + bf<float>(h, b, s, NB_FX) / m * a.dt;
-    const float vy = bf<float>(h, b, s, NB_VY) + bf<float>(h, b, s, NB_FY) / m * a.dt;
+    const float vx = nb_step_v(bf<float>(h, b, s, NB_VX), bf<float>(h, b, s, NB_FX), m, a.dt);
+    const float vy = nb_step_v(bf<float>(h, b, s, NB_VY), bf<float>(h, b, s, NB_FY), m, a.dt);
     bf<float>(h, b, s, NB_VX) = vx;
     bf<float>(h, b, s, NB_VY) = vy;
-    bf<float>(h, b, s, NB_X) = bf<float>(h, b, s, NB_X) + vx * a.dt;
-    bf<float>(h, b, s, NB_Y) = bf<float>(h, b, s, NB_Y) + vy * a.dt;
+    bf<float>(h, b, s, NB_X) = nb_step_p(bf<float>(h, b, s, NB_X), vx, a.dt);
+    bf<float>(h, b, s, NB_Y) = nb_step_p(bf<float>(h, b, s, NB_Y), vy, a.dt);
     bf<uint32_t>(h, b, s, NB_TARGET) = kNone;
     bf<uint32_t>(h, b, s, NB_INCOMING) = kNone;
     bf<uint8_t>(h, b, s, NB_MERGED) = 0;
@@ -254,11 +267,11 @@ struct NbAbsorb { // perfectly inelastic merge: momentum and centre of mass
     const float4 pi = s4(a, i);
     const float2 vi = reinterpret_cast<const float2*>(a.V)[i];
     const float m = bf<float>(h, b, s, NB_M), mi = pi.z;
-    const float mn = m + mi;
-    bf<float>(h, b, s, NB_VX) = (m * bf<float>(h, b, s, NB_VX) + mi * vi.x) / mn;
-    bf<float>(h, b, s, NB_VY) = (m * bf<float>(h, b, s, NB_VY) + mi * vi.y) / mn;
-    bf<float>(h, b, s, NB_X) = (m * bf<float>(h, b, s, NB_X) + mi * pi.x) / mn;
-    bf<float>(h, b, s, NB_Y) = (m * bf<float>(h, b, s, NB_Y) + mi * pi.y) / mn;
+    const float mn = __fadd_rn(m, mi);
+    bf<float>(h, b, s, NB_VX) = nb_mix(m, bf<float>(h, b, s, NB_VX), mi, vi.x, mn);
+    bf<float>(h, b, s, NB_VY) = nb_mix(m, bf<float>(h, b, s, NB_VY), mi, vi.y, mn);
+    bf<float>(h, b, s, NB_X) = nb_mix(m, bf<float>(h, b, s, NB_X), mi, pi.x, mn);
+    bf<float>(h, b, s, NB_Y) = nb_mix(m, bf<float>(h, b, s, NB_Y), mi, pi.y, mn);
     bf<float>(h, b, s, NB_M) = mn;
   }
 };
@@ -349,4 +362,108 @@ bool nb_ctor_launch(uint32_t id, const LaunchCtx& c, uint32_t T, uint64_t n, con
   return true;
 }
 
+// ---- static-allocation baseline: the same
+// six passes on id-indexed SOA arrays (S = (x, y, m, 0), V = (vx, vy); a dead
+// id has m = 0), no heap, no objects.  The all-pairs kernels are the ones
+// above (they read S only); the per-body passes are array loops with the
+// operations and order of NbMove / k_nb_merge_pick / NbAbsorb /
+// NbDeleteMerged, so a run equals the heap version bit for bit.
+__global__ void k_nbs_force_move(dsr_nbody_args a) {
+  const uint32_t n = a.n_total, chunks = (n + kChunk - 1) / kChunk;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    a.target[i] = kNone;
+    a.incoming[i] = kNone;
+    float4 p = reinterpret_cast<float4*>(a.S)[i];
+    if (p.z == 0.f) continue;                                     // dead id
+    float ax = 0.f, ay = 0.f;
+    for (uint32_t c = 0; c < chunks; ++c) {
+      const float2 v = reinterpret_cast<const float2*>(a.scratch)[(size_t)c * n + i];
+      ax += v.x;
+      ay += v.y;
+    }
+    const float gm = __fmul_rn(a.G, p.z);
+    const float fx = __fmul_rn(gm, ax), fy = __fmul_rn(gm, ay);
+    float2 v = reinterpret_cast<float2*>(a.V)[i];
+    v.x = nb_step_v(v.x, fx, p.z, a.dt);
+    v.y = nb_step_v(v.y, fy, p.z, a.dt);
+    p.x = nb_step_p(p.x, v.x, a.dt);
+    p.y = nb_step_p(p.y, v.y, a.dt);
+    reinterpret_cast<float2*>(a.V)[i] = v;
+    reinterpret_cast<float4*>(a.S)[i] = p;
+  }
+}
+__global__ void k_nbs_merge_pick(dsr_nbody_args a) {
+  const uint32_t n = a.n_total, chunks = (n + kChunk - 1) / kChunk;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (reinterpret_cast<const float4*>(a.S)[i].z == 0.f) continue;
+    uint32_t best = kNone;
+    float bd = 0.f;
+    for (uint32_t c = 0; c < chunks; ++c) {
+      const uint2 v = reinterpret_cast<const uint2*>(a.scratch)[(size_t)c * n + i];
+      const float d = __uint_as_float(v.x);
+      if (v.y != kNone && (best == kNone || d < bd)) { best = v.y; bd = d; }
+    }
+    a.target[i] = best;
+  }
+}
+__global__ void k_nbs_absorb(dsr_nbody_args a) {
+  for (uint32_t id = blockIdx.x * blockDim.x + threadIdx.x; id < a.n_total; id += gridDim.x * blockDim.x) {
+    const uint32_t i = a.incoming[id];
+    if (i == kNone || a.target[id] != kNone) continue;
+    float4 p = reinterpret_cast<float4*>(a.S)[id];
+    float2 v = reinterpret_cast<float2*>(a.V)[id];
+    const float4 pi = reinterpret_cast<const float4*>(a.S)[i];     // i merges away: nobody writes it here
+    const float2 vi = reinterpret_cast<const float2*>(a.V)[i];
+    const float m = p.z, mi = pi.z, mn = __fadd_rn(m, mi);
+    v.x = nb_mix(m, v.x, mi, vi.x, mn);
+    v.y = nb_mix(m, v.y, mi, vi.y, mn);
+    p.x = nb_mix(m, p.x, mi, pi.x, mn);
+    p.y = nb_mix(m, p.y, mi, pi.y, mn);
+    p.z = mn;
+    reinterpret_cast<float2*>(a.V)[id] = v;
+    reinterpret_cast<float4*>(a.S)[id] = p;
+  }
+}
+__global__ void k_nbs_delete(dsr_nbody_args a) {
+  for (uint32_t id = blockIdx.x * blockDim.x + threadIdx.x; id < a.n_total; id += gridDim.x * blockDim.x) {
+    const uint32_t t = a.target[id];
+    if (t != kNone && a.incoming[t] == id && a.target[t] == kNone) reinterpret_cast<float4*>(a.S)[id].z = 0.f;
+  }
+}
+
 }  // namespace dsr
+
+extern "C" dsr_status dsr_nbody_static_step(const dsr_nbody_static_args* sa, uint32_t steps, void* stream) {
+  using namespace dsr;
+  if (!sa || !sa->S || !sa->V || !sa->target || !sa->incoming || !sa->scratch || sa->n == 0) return DSR_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  dsr_nbody_args a;
+  memset(&a, 0, sizeof(a));
+  a.S = sa->S;
+  a.V = sa->V;
+  a.target = sa->target;
+  a.incoming = sa->incoming;
+  a.scratch = sa->scratch;
+  a.G = sa->G; a.dt = sa->dt; a.eps = sa->eps; a.R = sa->R;
+  a.n_total = sa->n;
+  a.id_lo = 0;
+  a.id_hi = sa->n;
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return DSR_ERR_CUDA;
+  const int g = (int)std::min<uint64_t>((sa->n + 255) / 256, (uint64_t)sms * 8);
+  for (uint32_t k = 0; k < steps; ++k) {
+    k_nb_force_part<<<pair_grid(a), kPairThreads, 0, st>>>(a);           // compute_force over S0
+    k_nbs_force_move<<<g, 256, 0, st>>>(a);                             // + move: S becomes S1
+    if (sa->merges) {
+      k_nb_merge_part<<<pair_grid(a), kPairThreads, 0, st>>>(a);        // prepare_merge over S1
+      k_nbs_merge_pick<<<g, 256, 0, st>>>(a);
+      k_nb_claim_all<<<g, 256, 0, st>>>(a.n_total, a);
+      k_nbs_absorb<<<g, 256, 0, st>>>(a);
+      k_nbs_delete<<<g, 256, 0, st>>>(a);
+      count_launch(5);
+    }
+    count_launch(2);
+  }
+  return cudaGetLastError() == cudaSuccess ? DSR_OK : DSR_ERR_CUDA;
+}

@@ -138,6 +138,16 @@ class WatorArgs(C.Structure):
                 ("halo", C.c_void_p), ("step_dev", C.c_void_p)]
 
 
+class NbodyStaticArgs(C.Structure):
+    _fields_ = [("S", C.c_void_p), ("V", C.c_void_p), ("target", C.c_void_p), ("incoming", C.c_void_p),
+                ("scratch", C.c_void_p), ("G", C.c_float), ("dt", C.c_float), ("eps", C.c_float), ("R", C.c_float),
+                ("n", C.c_uint32), ("merges", C.c_uint32)]
+
+
+class GolStaticArgs(C.Structure):
+    _fields_ = [("W", C.c_uint32), ("H", C.c_uint32), ("cur", C.c_void_p), ("next", C.c_void_p)]
+
+
 class WatorStaticArgs(C.Structure):
     _fields_ = [("W", C.c_uint32), ("H", C.c_uint32), ("FB", C.c_uint32), ("SB", C.c_uint32), ("SS", C.c_uint32),
                 ("step", C.c_uint32), ("seed", C.c_uint64), ("kind", C.c_void_p), ("egg", C.c_void_p),
@@ -190,6 +200,10 @@ def lib():
             L.dsr_probe_atomics.argtypes = [vp, C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64), vp]
         L.dsr_wator_static_step.restype = st
         L.dsr_wator_static_step.argtypes = [C.POINTER(WatorStaticArgs), C.c_uint32, vp]
+        L.dsr_nbody_static_step.restype = st
+        L.dsr_nbody_static_step.argtypes = [C.POINTER(NbodyStaticArgs), C.c_uint32, vp]
+        L.dsr_gol_static_step.restype = st
+        L.dsr_gol_static_step.argtypes = [C.POINTER(GolStaticArgs), C.c_uint32, vp]
         L.dsr_parallel_new.restype = st
         L.dsr_parallel_new.argtypes = [vp, C.c_uint32, C.c_uint64, C.c_uint32, vp, C.c_size_t, vp]
         L.dsr_parallel_do.restype = st

@@ -162,6 +162,32 @@ class GameOfLife:
         return np.stack([c, v & 0xFF, (v >> 8) & 0xFF, (v >> 16) & 0xFF], axis=1).astype(np.uint32)
 
 
+class GameOfLifeStatic:
+    """The paper's static-allocation baseline of Game of Life: B3/S23
+    on a u8 cell grid, no objects (dsr_gol_static_step)."""
+
+    def __init__(self, alive0, device=None, stream=None):
+        import ctypes as C
+        import numpy as np
+        import torch
+        self.H, self.W = alive0.shape
+        dev = torch.device(device if device is not None else "cuda")
+        self.cur = torch.from_numpy(np.ascontiguousarray(alive0, dtype=np.uint8).reshape(-1)).to(dev)
+        self.next = torch.zeros_like(self.cur)
+        self.stream, self._C = stream, C
+        self.args = dsr.GolStaticArgs(self.W, self.H, self.cur.data_ptr(), self.next.data_ptr())
+
+    def run(self, gens, stream=None):
+        s = stream if stream is not None else self.stream
+        dsr.check("dsr_gol_static_step", dsr.lib().dsr_gol_static_step(self._C.byref(self.args), gens,
+                                                                       dsr._stream_ptr(s)))
+
+    def alive(self):
+        import torch
+        torch.cuda.synchronize()
+        return self.cur.cpu().numpy().reshape(self.H, self.W)
+
+
 class NcclHaloExchange:
     """Halo exchange between row-band shards over torch.distributed (NCCL on
     GPUs): my first row's masks go to the shard above, my last row's to the

@@ -142,6 +142,45 @@ class NBody:
                 "m": o[:, 4].copy(), "alive": (o[:, 5] > 0).astype(np.uint8)}
 
 
+class NBodyStatic:
+    """The paper's static-allocation baseline of N-body: the same
+    passes on id-indexed SOA arrays, no heap (dsr_nbody_static_step); its
+    state after any number of steps equals NBody's bit for bit."""
+
+    def __init__(self, state, G, dt, eps, R, merges=True, device=None, stream=None):
+        import ctypes as C
+        import numpy as np
+        import torch
+        n = len(state["x"])
+        dev = torch.device(device if device is not None else "cuda")
+        self.n, self.stream, self._C = n, stream, C
+        S = np.zeros((n, 4), np.float32)
+        alive = np.asarray(state.get("alive", np.ones(n, np.uint8))) != 0
+        S[:, 0], S[:, 1], S[:, 2] = state["x"], state["y"], np.where(alive, state["m"], 0)
+        self.S = torch.from_numpy(S).to(dev)
+        self.V = torch.from_numpy(np.stack([state["vx"], state["vy"]], 1).astype(np.float32)).to(dev)
+        self.target = torch.full((n,), -1, dtype=torch.int32, device=dev)
+        self.incoming = torch.full((n,), -1, dtype=torch.int32, device=dev)
+        self.scratch = torch.zeros(2 * ((n + 4095) // 4096) * n, dtype=torch.float32, device=dev)
+        self.args = dsr.NbodyStaticArgs(self.S.data_ptr(), self.V.data_ptr(), self.target.data_ptr(),
+                                        self.incoming.data_ptr(), self.scratch.data_ptr(), G, dt, eps, R, n,
+                                        1 if merges else 0)
+
+    def run(self, steps, stream=None):
+        s = stream if stream is not None else self.stream
+        dsr.check("dsr_nbody_static_step", dsr.lib().dsr_nbody_static_step(self._C.byref(self.args), steps,
+                                                                           dsr._stream_ptr(s)))
+
+    def state(self):
+        import numpy as np
+        import torch
+        torch.cuda.synchronize()
+        S, V = self.S.cpu().numpy(), self.V.cpu().numpy()
+        alive = (S[:, 2] > 0).astype(np.uint8)
+        z = lambda v: np.where(alive == 1, v, 0).astype(np.float32)
+        return {"x": z(S[:, 0]), "y": z(S[:, 1]), "vx": z(V[:, 0]), "vy": z(V[:, 1]), "m": z(S[:, 2]), "alive": alive}
+
+
 class NBodyLoopback:
     """P id-range shards of the N-body step on ONE GPU: P heaps, the same
     kernels and phase order as the multi-GPU run, the all-gathers replaced by
