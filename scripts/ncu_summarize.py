@@ -23,6 +23,12 @@ KEYS = {
 UNIT = {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "s": 1.0, "nsecond": 1e-9,
         "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 
+# the library build the reports were captured from (scripts/prof_targets.py writes it):
+# bench.py reuses counts only from summaries of its own source hash
+try:
+    BUILD = open("gpurun_out/build_info.txt").read().strip()
+except OSError:
+    BUILD = ""
 out = []
 for rep in sys.argv[2:]:
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -32,7 +38,7 @@ for rep in sys.argv[2:]:
     h, units = rows[0], rows[1]
     stall_cols = [i for i, n in enumerate(h) if n.startswith("smsp__average_warps_issue_stalled_") and n.endswith("_per_issue_active.ratio")]
     for r in rows[2:]:
-        d = {"report": rep.split("/")[-1], "kernel": r[h.index("Kernel Name")][:90]}
+        d = {"report": rep.split("/")[-1], "kernel": r[h.index("Kernel Name")][:90], "build": BUILD}
         for k, name in KEYS.items():
             if k in h:
                 i = h.index(k)
