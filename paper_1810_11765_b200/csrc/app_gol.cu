@@ -302,62 +302,56 @@ __global__ void __launch_bounds__(256) k_gol_tile_prepare(DevHeap h, dsr_gol_arg
     (void)row0;
   }
 }
-// Update passes: a CTA takes chunks of 2048 consecutive cells, compacts the
-// cells holding an object of the pass's type into shared memory (warp
-// ballots + a CTA scan, in row-major order), then runs the method over the
-// compacted list with full warps: lane j of a warp gets the j-th object of 32
-// neighbouring ones, so its allocations and destroys coalesce per block.
-constexpr int kUpdChunk = 2048;
+// Update passes: warp-level, no CTA barriers.  Each warp owns one contiguous
+// run of 256-cell chunks (blocked over all warps of the grid, so a warp's
+// allocations -- its hint block, P:649 -- fill with objects of neighbouring
+// cells and blocks stay spatially coherent across generations).  Per chunk
+// the warp loads the 256 handles (8 coalesced rows of 32), compacts those of
+// the pass's type into its shared-memory list with ballots (row-major order),
+// and runs the method over the list with full warps: lane j gets the j-th of
+// 32 neighbouring objects, so destroys and news coalesce per block.  (The
+// previous CTA-wide compaction of 2048-cell chunks needed four barriers per
+// chunk and left the allocation latency exposed.)
+constexpr int kUpdChunk = 256;
+#ifndef DSR_GOL_UPD_MINB
+#define DSR_GOL_UPD_MINB 4
+#endif
 template <int PASS>
-__global__ void __launch_bounds__(256, 4) k_gol_tile_update(DevHeap h, dsr_gol_args a) {
-  __shared__ unsigned long long s_hd[kUpdChunk];
-  __shared__ uint32_t s_warp[8], s_n;
+__global__ void __launch_bounds__(256, DSR_GOL_UPD_MINB) k_gol_tile_update(DevHeap h, dsr_gol_args a) {
+  __shared__ unsigned long long s_hd[8][kUpdChunk];
   const uint32_t W = a.W, row0 = a.ghost ? 1u : 0u;
   const uint64_t n = (uint64_t)W * a.H;
   const uint32_t T = PASS == 3 ? GOL_CAND : GOL_ALIVE;
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long* const lst = s_hd[wid];
   NoAcc acc;
-  // blocked distribution: CTA b owns one contiguous run of chunks, so each
-  // warp's allocations (its hint block) fill with objects of
-  // neighbouring cells and the blocks stay spatially coherent
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5, gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nch = (n + kUpdChunk - 1) / kUpdChunk;
-  const uint64_t c0 = (uint64_t)blockIdx.x * nch / gridDim.x, c1 = (uint64_t)(blockIdx.x + 1) * nch / gridDim.x;
-  for (uint64_t base = c0 * kUpdChunk; base < c1 * kUpdChunk && base < n; base += kUpdChunk) {
-    // this thread's 8 cells: base + wid * 256 + k * 32 + lane (a warp reads 8 rows of 32 consecutive cells)
+  const uint64_t c0 = gw * nch / nw, c1 = (gw + 1) * nch / nw;
+  const unsigned long long* cells = (const unsigned long long*)a.cell + (uint64_t)row0 * W;
+  for (uint64_t ch = c0; ch < c1; ++ch) {
+    const uint64_t base = ch * kUpdChunk;
     unsigned long long v[8];
-    uint32_t mine = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const uint64_t i = base + (uint64_t)wid * 256 + k * 32 + lane;
-      v[k] = i < n ? ld_relaxed((const uint64_t*)a.cell + i + (uint64_t)row0 * W) : 0ull;
-      mine += h_is(v[k], T) ? 1u : 0u;
+      const uint64_t i = base + k * 32 + lane;
+      v[k] = i < n ? ld_relaxed((const uint64_t*)cells + i) : 0ull;
     }
-    // CTA exclusive scan of per-warp counts (row-major order = warp, k, lane)
-    uint32_t wc = __reduce_add_sync(0xffffffffu, mine);
-    __syncthreads();                                                   // s_hd of the previous chunk consumed
-    if (lane == 0) s_warp[wid] = wc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t run = 0;
-      for (int w = 0; w < 8; ++w) { const uint32_t t = s_warp[w]; s_warp[w] = run; run += t; }
-      s_n = run;
-    }
-    __syncthreads();
-    uint32_t pos = s_warp[wid];
+    uint32_t pos = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const bool m = h_is(v[k], T);
       const uint32_t bal = __ballot_sync(0xffffffffu, m);
-      if (m) s_hd[pos + __popc(bal & ((1u << lane) - 1u))] = v[k];
+      if (m) lst[pos + __popc(bal & ((1u << lane) - 1u))] = v[k];
       pos += __popc(bal);
     }
-    __syncthreads();
-    const uint32_t cnt = s_n;
-    for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) {
-      const uint64_t hd = s_hd[j];
+    __syncwarp();
+    for (uint32_t j = lane; j < pos; j += 32) {
+      const uint64_t hd = lst[j];
       if (PASS == 3) GolCandUpdate::run(h, T, h_bid(hd), h_slot(hd), a, acc);
       else GolAliveUpdate::run(h, T, h_bid(hd), h_slot(hd), a, acc);
     }
+    __syncwarp();                                                      // lst consumed before the next chunk
   }
 }
 

@@ -407,10 +407,19 @@ __device__ __forceinline__ int64_t leaf_next(uint64_t c, uint64_t pos) {
   const uint32_t i = ffs_from(c, r);
   return (int64_t)((pos & ~63ull) | i);
 }
-// clear(): find + try_clear until the clear succeeds (reading R-CLEARANY)
+// clear(): find + try_clear until the clear succeeds (reading R-CLEARANY).
+// Used on the free bitmap only.  The rotation there applies to the lowest
+// DSR_FREE_ROT_LEVELS levels (reading R-FREEROT); above them the search takes
+// the lowest container with a free block, so new blocks fill the heap from its
+// low end instead of being scattered over all of it: the blocks an app uses
+// then span a range set by the live data, not by the heap size.
+#ifndef DSR_FREE_ROT_LEVELS
+#define DSR_FREE_ROT_LEVELS 3
+#endif
 __device__ __forceinline__ int64_t bm_clear_any(const DevHeap& h, const DevBitmap& b, uint64_t who, uint64_t retry0) {
+  const uint64_t keep = DSR_FREE_ROT_LEVELS >= 10 ? ~0ull : ((1ull << (6 * DSR_FREE_ROT_LEVELS)) - 1ull);
   for (uint64_t k = 0;; ++k) {
-    const int64_t i = bm_try_find_set(b, rot_hash(h, who, retry0 + k));
+    const int64_t i = bm_try_find_set(b, rot_hash(h, who, retry0 + k) & keep);
     if (i < 0) return -1;
     if (bm_try_clear(b, (uint64_t)i)) return i;
   }
