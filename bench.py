@@ -501,6 +501,31 @@ def timed_steps(step, K, W, stream, after=None):
     return [a.elapsed_time(b) for a, b in ev]
 
 
+def app_traffic(name, kernels=None):
+    """DRAM bytes (read + write) per step of an app from the committed ncu
+    summary profiles/<round>/ncu_<name>.json (one generation / step of the
+    app's passes, scripts/gpu_ncu_apps.sh), only if it was captured from this
+    library build (source hash); kernels: only those kernel names (per launch)."""
+    if not name:
+        return None
+    from paper_1810_11765_b200 import dsr
+    tag = src_tag(dsr.lib().dsr_build_info().decode())
+    best = None
+    for p in sorted((ROOT / "profiles").glob(f"r*/ncu_{name}.json")):
+        try:
+            rows = [r for r in json.loads(p.read_text()) if tag and tag in r.get("build", "")]
+        except Exception:
+            continue
+        if kernels:
+            rows = [r for r in rows if any(k in r.get("kernel", "") for k in kernels)]
+        if rows:
+            tot = sum(r.get("dram_bytes", 0.0) for r in rows)
+            best = {"traffic": tot / len(rows) if kernels else tot,
+                    "traffic_source": f"{p.relative_to(ROOT)} ({len(rows)} launches, "
+                                      + ("per launch" if kernels else "one step") + ")"}
+    return best
+
+
 def hbm_roofline(kernel, nbytes, ms, peak, peak_src, note, bound="hbm"):
     gbs = nbytes / (ms * 1e-3) / 1e9
     return {"bound": bound, "kernel": kernel, "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
@@ -528,10 +553,14 @@ def app_block(stream, peak, peak_src, sm_mhz, want_cpu=True):
 
     # ---- GoL (configs[0] 64^2 x 100 gens; configs[3] 16384^2, handle grid and alive-bit mirror)
     from paper_1810_11765_b200.gol import GameOfLife
+    # gol_16384: the prepare passes (the neighbour gathers) as cell-tiled do-alls
+    # staging handle tiles in shared memory, the update passes on the block list
+    # (DESIGN.md §6); gol_16384_blocklist: all four passes as the paper's
+    # block-list do-all; gol_16384_bits: block list + the alive-bit mirror
     for name, Wd, K, Wu, bits, tiled in (("gol_64", 64, 100, 5, False, False),
-                                         ("gol_16384", 16384, 4, 1, False, False),
-                                         ("gol_16384_bits", 16384, 4, 1, True, False),
-                                         ("gol_16384_tiled", 16384, 4, 1, False, True)):
+                                         ("gol_16384", 16384, 4, 1, False, "prepare"),
+                                         ("gol_16384_blocklist", 16384, 4, 1, False, False),
+                                         ("gol_16384_bits", 16384, 4, 1, True, False)):
         a0 = I.gol_soup(Wd, Wd, 0.3 if Wd == 64 else 0.25, 1 if Wd == 64 else 42)
         sim = GameOfLife(a0, stream=stream, bit_mirror=bits, tiled=tiled)
         step = sim.generation
@@ -552,7 +581,9 @@ def app_block(stream, peak, peak_src, sm_mhz, want_cpu=True):
         out[name] = {
             "config": f"BASELINE configs[{0 if Wd == 64 else 3}]: {Wd}^2 torus, Bernoulli("
                       f"{0.3 if Wd == 64 else 0.25}) soup" + (", alive-bit mirror variant" if bits else "")
-                      + (", cell-tiled do-alls (objects enumerated through the handle grid)" if tiled else "")
+                      + (", prepare passes as cell-tiled do-alls (objects enumerated through the handle grid, "
+                         "(8+2) x (128+2) handle tiles in shared memory), update passes on the block list" if tiled
+                         else (", all passes on the block list" if Wd > 64 and not bits else ""))
                       + (", one generation replayed as a CUDA graph" if Wd == 64 else ""),
             "value": visits / (sum(t) * 1e-3), "unit": "object-updates/s", "ms_per_step": ms, "steps": K,
             "objects_per_step": float(objs.mean()),
@@ -565,9 +596,13 @@ def app_block(stream, peak, peak_src, sm_mhz, want_cpu=True):
                                                                   "the 8 handles, same algorithmic definition" if bits else ""),
                                      bound="latency" if Wd == 64 else "hbm"),
         }
+        tr = app_traffic({"gol_16384": "gol16k-tiled", "gol_16384_blocklist": "gol16k",
+                          "gol_16384_bits": "gol16k-bits"}.get(name))
+        if tr:
+            out[name]["roofline"].update(tr)
         del sim
         torch.cuda.empty_cache()
-        if bits or tiled:
+        if name != "gol_64" and name != "gol_16384":
             continue
         from paper_1810_11765_b200.gol import GameOfLifeStatic
         base = GameOfLifeStatic(a0, stream=stream)
@@ -626,7 +661,11 @@ def app_block(stream, peak, peak_src, sm_mhz, want_cpu=True):
                                  "working set ~80 MB is L2-resident (126 MB), so HBM is not the bound"),
         "static_baseline": {"ms_per_step": sum(tb) / K, "dynamic_over_static": ms / (sum(tb) / K),
                             "what": "same rules on cell-indexed SOA arrays, no heap (P:763, dsr_wator_static_step)"},
+        "fragmentation": sim.heap.fragmentation()[0],
     }
+    tr = app_traffic("wator")
+    if tr:
+        out["wator_2048"]["roofline"].update(tr)
     del sim, base
     torch.cuda.empty_cache()
 
@@ -685,6 +724,9 @@ def app_block(stream, peak, peak_src, sm_mhz, want_cpu=True):
                      "note": "9 FP32 ops per pair (2 FADD, 2 FFMA for r^2, 3 FMUL, 2 FFMA accumulate) on packed "
                              "f32x2 pairs; the snapshot is SMEM/L2-resident"},
     }
+    tr = app_traffic("nbody", kernels=("k_nb_force_part",))
+    if tr:
+        out["nbody_65536"]["roofline"].update(tr)
     del sim
     torch.cuda.empty_cache()
     from paper_1810_11765_b200.nbody import NBodyStatic

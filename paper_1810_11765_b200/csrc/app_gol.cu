@@ -122,13 +122,26 @@ __global__ void __launch_bounds__(256) k_gol_init(DevHeap h, uint64_t n, dsr_gol
   }
 }
 
+// Alive.prepare's stores: is_new = 0, action = DIE iff k < 2 or k > 3.  Every
+// Alive enters pass 2 with action NONE (created with NONE; pass 4 destroys the
+// old ones marked DIE, and a new one is created after pass 2), and is_new is
+// 1 only for the Alives pass 3 created: the stores are made only where they
+// change the byte (a store of an unchanged byte still dirties its sector).
+__device__ __forceinline__ void gol_alive_prepare_store(const DevHeap& h, uint64_t hd, uint32_t k) {
+  uint8_t* const is_new = field_ptr<uint8_t>(h, hd, 1);
+  if (*is_new) *is_new = 0;
+  if (k < 2 || k > 3) *field_ptr<uint8_t>(h, hd, 2) = ACT_DIE;
+}
+
 struct GolCandPrepare {   // pass 1
   typedef dsr_gol_args Args;
   DSR_NO_ACC
   static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args& a, Acc&) {
     const uint32_t c = *field_ptr<uint32_t>(h, T, 0, b, s);
     const uint32_t k = gol_alive_nbrs(a, c);
-    *field_ptr<uint8_t>(h, T, 1, b, s) = k == 3 ? ACT_SPAWN : (k == 0 ? ACT_DIE : ACT_NONE);
+    // every Candidate enters pass 1 with action NONE (created with NONE; pass 3
+    // destroys the ones whose action is not NONE), so NONE needs no store
+    if (k == 3 || k == 0) *field_ptr<uint8_t>(h, T, 1, b, s) = k == 3 ? ACT_SPAWN : ACT_DIE;
   }
 };
 struct GolAlivePrepare {  // pass 2
@@ -137,8 +150,7 @@ struct GolAlivePrepare {  // pass 2
   static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args& a, Acc&) {
     const uint32_t c = *field_ptr<uint32_t>(h, T, 0, b, s);
     const uint32_t k = gol_alive_nbrs(a, c);
-    *field_ptr<uint8_t>(h, T, 1, b, s) = 0;
-    *field_ptr<uint8_t>(h, T, 2, b, s) = (k < 2 || k > 3) ? ACT_DIE : ACT_NONE;
+    gol_alive_prepare_store(h, make_handle(T, h.types[T].cap, b, s), k);
   }
 };
 struct GolCandUpdate {    // pass 3 (allocates Alive)
@@ -162,11 +174,19 @@ struct GolAliveUpdate {   // pass 4 (allocates Candidate)
     const uint32_t c = *field_ptr<uint32_t>(h, T, 0, b, s);
     uint32_t todo = 0;                                   // bit d: create a Candidate at neighbour d; bit 8: at c
     if (*field_ptr<uint8_t>(h, T, 1, b, s)) {            // new Alive: claim the empty neighbours
+      // the 8 neighbour loads first (independent, all in flight), then a CAS
+      // only on the cells that read empty
+      uint64_t nb[8];
+#pragma unroll
       for (int d = 0; d < 8; ++d) {
         const uint32_t e = gol_nbr(a.W, a.H, c, d, a.ghost);
-        if (!gol_local(a, e)) continue;                  // a neighbour shard's cell: its owner creates it
-        unsigned long long* pe = (unsigned long long*)a.cell + e;
-        if (ld_relaxed((const uint64_t*)pe) == 0 && atomicCAS(pe, 0ull, kReserved) == 0ull) todo |= 1u << d;
+        nb[d] = gol_local(a, e) ? ld_relaxed((const uint64_t*)a.cell + e) : 1ull;   // a neighbour shard's cell: its owner creates it
+      }
+#pragma unroll
+      for (int d = 0; d < 8; ++d) {
+        if (nb[d] != 0) continue;
+        unsigned long long* pe = (unsigned long long*)a.cell + gol_nbr(a.W, a.H, c, d, a.ghost);
+        if (atomicCAS(pe, 0ull, kReserved) == 0ull) todo |= 1u << d;
       }
     } else if (*field_ptr<uint8_t>(h, T, 2, b, s) == ACT_DIE) {
       dsr_destroy_ro(h, after_load(make_handle(T, h.types[T].cap, b, s), c));   // read-only, c consumed
@@ -293,10 +313,9 @@ __global__ void __launch_bounds__(256) k_gol_tile_prepare(DevHeap h, dsr_gol_arg
         for (int dx = 0; dx < 3; ++dx)
           if (dy != 1 || dx != 1) k += h_is(s[r + dy][cc + dx], GOL_ALIVE);
       if (PASS == 1) {
-        *field_ptr<uint8_t>(h, hd, 1) = k == 3 ? ACT_SPAWN : (k == 0 ? ACT_DIE : ACT_NONE);
+        if (k == 3 || k == 0) *field_ptr<uint8_t>(h, hd, 1) = k == 3 ? ACT_SPAWN : ACT_DIE;   // NONE: unchanged
       } else {
-        *field_ptr<uint8_t>(h, hd, 1) = 0;
-        *field_ptr<uint8_t>(h, hd, 2) = (k < 2 || k > 3) ? ACT_DIE : ACT_NONE;
+        gol_alive_prepare_store(h, hd, k);
       }
     }
     (void)row0;

@@ -416,10 +416,10 @@ __device__ __forceinline__ int64_t leaf_next(uint64_t c, uint64_t pos) {
 #ifndef DSR_FREE_ROT_LEVELS
 #define DSR_FREE_ROT_LEVELS 3
 #endif
+constexpr uint64_t kFreeRotMask = DSR_FREE_ROT_LEVELS >= 10 ? ~0ull : ((1ull << (6 * DSR_FREE_ROT_LEVELS)) - 1ull);
 __device__ __forceinline__ int64_t bm_clear_any(const DevHeap& h, const DevBitmap& b, uint64_t who, uint64_t retry0) {
-  const uint64_t keep = DSR_FREE_ROT_LEVELS >= 10 ? ~0ull : ((1ull << (6 * DSR_FREE_ROT_LEVELS)) - 1ull);
   for (uint64_t k = 0;; ++k) {
-    const int64_t i = bm_try_find_set(b, rot_hash(h, who, retry0 + k) & keep);
+    const int64_t i = bm_try_find_set(b, rot_hash(h, who, retry0 + k) & kFreeRotMask);
     if (i < 0) return -1;
     if (bm_try_clear(b, (uint64_t)i)) return i;
   }
@@ -887,7 +887,7 @@ __device__ __forceinline__ uint32_t dsr_new_warp(const DevHeap& h, uint32_t T, u
     const uint32_t nb = min((rem + cap - 1u) / cap, (uint32_t)__popc(freelanes));
     const uint32_t leader = __ffs(freelanes) - 1;
     uint64_t got = 0, wi = 0;
-    if (lane == leader) got = bm_clear_many(h.freebm, rot_hash(h, who, 0x100000ull + round), nb, &wi);
+    if (lane == leader) got = bm_clear_many(h.freebm, rot_hash(h, who, 0x100000ull + round) & kFreeRotMask, nb, &wi);
     got = shfl64(0xffffffffu, got, leader);
     wi = shfl64(0xffffffffu, wi, leader);
     if (!got) {

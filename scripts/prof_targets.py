@@ -6,7 +6,9 @@ import torch
 from paper_1810_11765_b200 import inputs as I
 
 w = sys.argv[1]
-if w == "mb":
+if w == "none":
+    pass
+elif w == "mb":
     from paper_1810_11765_b200.microbench import Microbench
     mb = Microbench()
     for _ in range(2):
