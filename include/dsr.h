@@ -97,6 +97,7 @@ typedef struct {
 #define DSR_F_HOME_ROT    0x40u /* ablation: SM-affine rotation (searches start in the SM's range of level-1 containers) */
 #define DSR_F_SLOT_ROTATE 0x80u /* paper: also rotate a block's object bitmap before choosing its free slots; off by default */
 #define DSR_F_SCALAR_DOALL 0x100u /* ablation: one thread per object in methods that also have a quad-mapped (vectorised) body */
+#define DSR_F_QUAD_FREE   0x200u /* ablation: microbench free passes as quad-mapped do-alls (lanes of a block combine their masks) instead of block-mapped (one lane per block) */
 
 typedef struct {
   uint32_t active_retries;   /* r: try_find_set attempts before the slow path (Fig. 11); 0 -> 5 */

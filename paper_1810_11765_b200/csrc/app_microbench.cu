@@ -107,9 +107,8 @@ __device__ __forceinline__ void mb_construct(const DevHeap& h, uint32_t T, const
     const uint32_t c0 = __shfl_sync(0xffffffffu, cum, c) + done;
     const uint32_t cn = (uint32_t)__popcll(cm);
     uint8_t* const blk = h.data + (size_t)cb * h.block_bytes;
-    for (uint32_t j = lane; j < cn; j += 32) {
-      const uint32_t s = nth_bit(cm, j);
-      const uint32_t i = c0 + j;                           // i-th object of T in the unit
+    // object i (the i-th of T in the unit) goes to slot s of the chunk's block
+    auto construct = [&](uint32_t s, uint32_t i) {
       const uint64_t t = nres == 2 ? ts + 4ull * (i >> 1) + ((i & 1) ? off1 : off0) : ts + 4ull * i + off0;
       uint8_t* const obj = blk + 4u * s;
       if (IN) {
@@ -121,6 +120,19 @@ __device__ __forceinline__ void mb_construct(const DevHeap& h, uint32_t T, const
 #pragma unroll
         for (int k = 0; k < NF; ++k) *reinterpret_cast<uint32_t*>(obj + col[k]) = (uint32_t)rng_key_p(kp, 5, t * 16 + k);
       }
+    };
+    // the chunk's mask is warp-uniform: one run of slots (a fresh block, the
+    // free tail of a block) -> lane j takes slot lo + j; otherwise lane p takes
+    // slot p (and p + 32) if it is in the mask, ranked by a popc of the bits
+    // below it (no per-object n-th-bit search)
+    const uint32_t lo = ctz64(cm);
+    const uint64_t run = cm >> lo;
+    if ((run & (run + 1ull)) == 0) {
+      for (uint32_t j = lane; j < cn; j += 32) construct(lo + j, c0 + j);
+    } else {
+#pragma unroll
+      for (uint32_t p = lane; p < 64; p += 32)
+        if ((cm >> p) & 1ull) construct(p, c0 + (uint32_t)__popcll(cm & ((1ull << p) - 1ull)));
     }
   }
 }
@@ -264,6 +276,40 @@ struct MbFreeAllQ {
   static __device__ __forceinline__ void run4(const DevHeap& h, uint32_t T, uint32_t b, uint32_t q, uint32_t m4,
                                               const Args&, Acc&) {
     dsr_destroy_mask<false>(h, T, b, (uint64_t)m4 << (4 * q));           // never reads or writes the objects
+  }
+};
+// MbFreeAll in block form (k_doall_block): the lane that owns a block
+// destroys all its visited objects with one block_free (Alg. 7 + Alg. 2 for
+// the whole mask; the objects are never read or written, so no release)
+struct MbFreeAllB {
+  struct Args { uint64_t unused; };
+  DSR_NO_ACC
+  static __device__ __forceinline__ void runb(const DevHeap& h, uint32_t T, uint32_t b, uint64_t m, const Args&, Acc&) {
+    block_free<false>(h, T, b, m);
+    stat_add(h, ST_FREES, __popcll(m));
+  }
+};
+// MbFreeOdd in block form: the lane reads column 0 of its block's visited
+// quads (independent 128-bit loads, all in flight) and frees the odd ones
+// with one block_free (control-dependent on the loads: no release)
+struct MbFreeOddB {
+  struct Args { uint64_t unused; };
+  DSR_NO_ACC
+  static __device__ __forceinline__ void runb(const DevHeap& h, uint32_t T, uint32_t b, uint64_t m, const Args&, Acc&) {
+    const uint4* col = quad_u32(h, T, 0, b, 0);
+    uint64_t kill = 0;
+#pragma unroll
+    for (uint32_t q = 0; q < 16; ++q) {
+      if ((m >> (4 * q)) & 0xFull) {
+        const uint4 v = __ldg(col + q);
+        kill |= (uint64_t)((v.x & 1u) | ((v.y & 1u) << 1) | ((v.z & 1u) << 2) | ((v.w & 1u) << 3)) << (4 * q);
+      }
+    }
+    kill &= m;
+    if (kill) {
+      block_free<false>(h, T, b, kill);
+      stat_add(h, ST_FREES, __popcll(kill));
+    }
   }
 };
 // handle collection (tests): out[atomic++] = this
@@ -468,11 +514,13 @@ bool mb_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot,
     }
     case DSR_M_MB_FREE_ODD:
       if (c.h.flags & DSR_F_SCALAR_DOALL) launch_doall<MbFreeOdd>(c, T, snapshot, zero);
-      else launch_doall_quad<MbFreeOddQ>(c, T, snapshot, zero);
+      else if (c.h.flags & DSR_F_QUAD_FREE) launch_doall_quad<MbFreeOddQ>(c, T, snapshot, zero);
+      else launch_doall_block<MbFreeOddB>(c, T, snapshot, zero);
       return true;
     case DSR_M_MB_FREE_ALL:
       if (c.h.flags & DSR_F_SCALAR_DOALL) launch_doall<MbFreeAll>(c, T, snapshot, zero);
-      else launch_doall_quad<MbFreeAllQ>(c, T, snapshot, zero);
+      else if (c.h.flags & DSR_F_QUAD_FREE) launch_doall_quad<MbFreeAllQ>(c, T, snapshot, zero);
+      else launch_doall_block<MbFreeAllB>(c, T, snapshot, zero);
       return true;
     case DSR_M_COLLECT: launch_doall<Collect>(c, T, snapshot, args); return true;
     case DSR_M_INH_BUMP: case DSR_M_INH_SUM: case DSR_M_INH_SPAWN:

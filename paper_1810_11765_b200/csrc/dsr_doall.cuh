@@ -275,6 +275,103 @@ __global__ void __launch_bounds__(256) k_doall_quad(DevHeap h, uint32_t T, int s
   Mth::flush(acc, a);
 }
 
+// Selective do-all body, for methods that do real work on a minority of
+// their objects (Mth::select(h, T, b, s, a): a cheap test, e.g. "my action is
+// not NONE"; Mth::run only where it holds).  A warp takes 32 x kDoallChunk
+// elements at a time from a device counter (dynamic distribution), tests them
+// with full warps, appends the selected (block, slot) pairs to its queue in
+// shared memory (ballot + popc), and whenever 32 are queued runs the method
+// on them with all 32 lanes: the allocations and destroys of the body then
+// coalesce over 32 objects instead of the few a warp's slots happen to select
+// (GoL's update passes ran at 6-8 active threads per instruction).
+template <class Mth>
+__global__ void __launch_bounds__(256) k_doall_sel(DevHeap h, uint32_t T, int rk, typename Mth::Args a) {
+  __shared__ unsigned long long s_q[8][64];
+  uint32_t rb = 0, re;
+  if (rk < 0) {
+    re = ld_relaxed_u32((const uint32_t*)&h.ctrl[CTRL_RCOUNT]);
+  } else {
+    rb = ld_relaxed_u32((const uint32_t*)&h.ctrl[CTRL_RBEG + rk]);
+    re = ld_relaxed_u32((const uint32_t*)&h.ctrl[CTRL_RBEG + rk + 1]);
+  }
+  const uint32_t* R = h.R + rb;
+  const uint32_t N = h.types[T].cap;
+  const uint64_t total = (uint64_t)(re - rb) * N;
+  const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
+  unsigned long long* const q = s_q[threadIdx.x >> 5];
+  uint32_t cnt = 0;
+  typename Mth::Acc acc;
+  const uint32_t q32 = 32u / N, r32 = 32u % N;
+  for (;;) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&h.ctrl[CTRL_WORK], 32ull * kDoallChunk);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= total) break;
+    uint64_t e = base + lane;
+    uint64_t bi = e / N;
+    uint32_t s = (uint32_t)(e - bi * N);
+    for (uint32_t k = 0; k < kDoallChunk; ++k, e += 32) {
+      bool sel = false;
+      uint32_t b = 0;
+      if (e < total) {
+        b = R[bi];
+        sel = ((h.iter_bm[b] >> s) & 1ull) && Mth::select(h, T, b, s, a);
+      }
+      const uint32_t bal = __ballot_sync(0xffffffffu, sel);
+      if (sel) q[cnt + __popc(bal & lt)] = ((unsigned long long)b << 6) | s;
+      cnt += __popc(bal);
+      __syncwarp();
+      if (cnt >= 32) {                                     // a full warp of work
+        cnt -= 32;
+        const unsigned long long it = q[cnt + lane];
+        __syncwarp();
+        Mth::run(h, T, (uint32_t)(it >> 6), (uint32_t)(it & 63), a, acc);
+      }
+      bi += q32;
+      s += r32;
+      if (s >= N) { s -= N; ++bi; }
+    }
+  }
+  if (lane < cnt) {
+    const unsigned long long it = q[lane];
+    Mth::run(h, T, (uint32_t)(it >> 6), (uint32_t)(it & 63), a, acc);
+  }
+  Mth::flush(acc, a);
+}
+
+// Block-mapped do-all body: one lane per block of R, for methods whose work
+// on a block's visited objects combines into one action per block (destroying
+// all of them is one atomicAnd of the block's bitmap: the coalescing of
+// P:649 taken to the whole block).  The method gets the block's visited-slot
+// mask w (snapshot: iteration bitmap, else allocation bitmap & valid).  Each
+// warp owns one contiguous range of R (blocked) and each lane one contiguous
+// sub-range of it, so the 32 lanes' block transitions hit bitmap words far
+// apart and every lane keeps its own chain of dependent atomics in flight.
+template <class Mth>
+__global__ void __launch_bounds__(256) k_doall_block(DevHeap h, uint32_t T, int snapshot, int rk, typename Mth::Args a) {
+  uint32_t rb = 0, re;
+  if (rk < 0) {
+    re = ld_relaxed_u32((const uint32_t*)&h.ctrl[CTRL_RCOUNT]);
+  } else {
+    rb = ld_relaxed_u32((const uint32_t*)&h.ctrl[CTRL_RBEG + rk]);
+    re = ld_relaxed_u32((const uint32_t*)&h.ctrl[CTRL_RBEG + rk + 1]);
+  }
+  const uint32_t* R = h.R + rb;
+  const uint64_t valid = h.types[T].valid;
+  const uint64_t nb = re - rb;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5, w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t w0 = w * nb / nw, w1 = (w + 1) * nb / nw;
+  const uint64_t i0 = w0 + (w1 - w0) * lane / 32, i1 = w0 + (w1 - w0) * (lane + 1) / 32;
+  typename Mth::Acc acc;
+  for (uint64_t i = i0; i < i1; ++i) {
+    const uint32_t b = __ldg(R + i);
+    const uint64_t m = snapshot ? __ldg((const unsigned long long*)h.iter_bm + b) : (ld_relaxed(h.alloc_bm + b) & valid);
+    if (m) Mth::runb(h, T, b, m, a, acc);
+  }
+  Mth::flush(acc, a);
+}
+
 // the quad q of a u32 column f: one aligned 16-B segment (4 slots)
 __device__ __forceinline__ uint4* quad_u32(const DevHeap& h, uint32_t T, uint32_t f, uint32_t b, uint32_t q) {
   return reinterpret_cast<uint4*>(h.data + (size_t)b * h.block_bytes + h.types[T].col_off[f] + 16u * q);

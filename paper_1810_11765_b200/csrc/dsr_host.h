@@ -95,4 +95,21 @@ inline void launch_doall_quad(const LaunchCtx& c, uint32_t T, int snapshot, cons
   count_launch();
 }
 
+// selective body (k_doall_sel): the iteration-bitmap snapshot, dynamic distribution
+template <class Mth>
+inline void launch_doall_sel(const LaunchCtx& c, uint32_t T, const void* args) {
+  typename Mth::Args a = *reinterpret_cast<const typename Mth::Args*>(args);
+  cudaMemsetAsync(&c.h.ctrl[CTRL_WORK], 0, 8, c.st);
+  k_doall_sel<Mth><<<persistent_grid(c, k_doall_sel<Mth>), 256, 0, c.st>>>(c.h, T, c.rk, a);
+  count_launch();
+}
+
+// block-mapped body (k_doall_block): one lane per block
+template <class Mth>
+inline void launch_doall_block(const LaunchCtx& c, uint32_t T, int snapshot, const void* args) {
+  typename Mth::Args a = *reinterpret_cast<const typename Mth::Args*>(args);
+  k_doall_block<Mth><<<persistent_grid(c, k_doall_block<Mth>), 256, 0, c.st>>>(c.h, T, snapshot ? 1 : 0, c.rk, a);
+  count_launch();
+}
+
 }  // namespace dsr

@@ -23,6 +23,7 @@ OK, ERR_INVALID, ERR_OOM, ERR_CUDA, ERR_RETRY_BUDGET, ERR_INVARIANT, ERR_UNSUPPO
 F_NO_ROTATE, F_NO_COALESCE, F_STATS, F_SPIN_ON_OOM, F_NO_HINT, F_CTA_NEW, F_HOME_ROT, F_SLOT_ROTATE = (
     0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40, 0x80)
 F_SCALAR_DOALL = 0x100
+F_QUAD_FREE = 0x200
 
 # ids (mirror include/dsr.h)
 K_MB_NEW, M_MB_REDUCE, M_MB_FREE_ODD, M_MB_FREE_ALL = 1, 1, 2, 3
@@ -460,3 +461,41 @@ def probe_atomics(buf, mode=0, iters=64, stream=None) -> int:
                                                        mode, iters, C.byref(n), _stream_ptr(stream)))
     return n.value
 
+
+
+# ---------------------------------------------------------------- stream helpers for the host-side halo copies
+def on_stream(stream):
+    """Context: make `stream` (None = the current stream) torch's current
+    stream, so torch copies / NCCL calls are ordered with the library's
+    launches on it."""
+    import torch
+    return torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream())
+
+
+class StreamJoin:
+    """Context for device copies between several shards' streams (one-GPU
+    loopback exchanges): the copies run on the first stream after it waited for
+    all others, and every other stream waits for the copies afterwards."""
+
+    def __init__(self, streams):
+        import torch
+        cur = torch.cuda.current_stream()
+        self.streams = [s if s is not None else cur for s in streams]
+        self.ctx = None
+
+    def __enter__(self):
+        import torch
+        s0 = self.streams[0]
+        for s in self.streams[1:]:
+            if s != s0:
+                s0.wait_stream(s)
+        self.ctx = torch.cuda.stream(s0)
+        return self.ctx.__enter__()
+
+    def __exit__(self, *exc):
+        r = self.ctx.__exit__(*exc)
+        s0 = self.streams[0]
+        for s in self.streams[1:]:
+            if s != s0:
+                s.wait_stream(s0)
+        return r

@@ -102,7 +102,8 @@ class GameOfLife:
         s = stream if stream is not None else self.stream
         self.first_half(s)
         if self.shard is not None:
-            (self.exchange or self.self_exchange)()
+            with dsr.on_stream(s):                  # the copies / NCCL calls in order with the kernels on s
+                (self.exchange or self.self_exchange)()
         self.second_half(s)
 
     def self_exchange(self):
@@ -228,10 +229,11 @@ class GameOfLifeLoopback:
         for s in self.shards:
             s.first_half(s.stream)
         W = self.shards[0].W
-        for r, s in enumerate(self.shards):
-            up, down = self.shards[(r - 1) % self.P], self.shards[(r + 1) % self.P]
-            s.halo[2 * W:3 * W].copy_(up.halo[W:2 * W])       # the upper shard's last row
-            s.halo[3 * W:4 * W].copy_(down.halo[0:W])         # the lower shard's first row
+        with dsr.StreamJoin([s.stream for s in self.shards]):
+            for r, s in enumerate(self.shards):
+                up, down = self.shards[(r - 1) % self.P], self.shards[(r + 1) % self.P]
+                s.halo[2 * W:3 * W].copy_(up.halo[W:2 * W])       # the upper shard's last row
+                s.halo[3 * W:4 * W].copy_(down.halo[0:W])         # the lower shard's first row
         for s in self.shards:
             s.second_half(s.stream)
 

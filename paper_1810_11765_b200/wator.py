@@ -104,21 +104,23 @@ class WaTor:
                     (seq(k(dsr.K_WT_HALO_OCC_APPLY), *last), None)]
         return out
 
-    def swap(self, seg):
+    def swap(self, seg, stream=None):
         """Exchange one halo segment with the neighbour shards (P = 1 sharded:
-        with myself -- my row 1 borders my row H across the torus seam)."""
-        if self.exchange is not None:
-            return self.exchange(seg)
-        o, i, n = self.halo_layout[seg]
-        self.halo[i:i + n].copy_(self.halo[o + n:o + 2 * n])       # in[0] <- the shard above's out[1]
-        self.halo[i + n:i + 2 * n].copy_(self.halo[o:o + n])       # in[1] <- the shard below's out[0]
+        with myself -- my row 1 borders my row H across the torus seam), on
+        the stream the step's kernels run on."""
+        with dsr.on_stream(stream if stream is not None else self.stream):
+            if self.exchange is not None:
+                return self.exchange(seg)
+            o, i, n = self.halo_layout[seg]
+            self.halo[i:i + n].copy_(self.halo[o + n:o + 2 * n])       # in[0] <- the shard above's out[1]
+            self.halo[i + n:i + 2 * n].copy_(self.halo[o:o + n])       # in[1] <- the shard below's out[0]
 
     def step(self, stream=None):
         s = stream if stream is not None else self.stream
         for stage, seg in self.stages(s):
             stage()
             if seg is not None:
-                self.swap(seg)
+                self.swap(seg, s)
 
     def run(self, steps, stream=None):
         for _ in range(steps):
@@ -222,10 +224,11 @@ class WaTorLoopback:
             if seg is None:
                 continue
             o, i, n = self.shards[0].halo_layout[seg]
-            for r, s in enumerate(self.shards):
-                up, down = self.shards[(r - 1) % self.P], self.shards[(r + 1) % self.P]
-                s.halo[i:i + n].copy_(up.halo[o + n:o + 2 * n])
-                s.halo[i + n:i + 2 * n].copy_(down.halo[o:o + n])
+            with dsr.StreamJoin([s.stream for s in self.shards]):
+                for r, s in enumerate(self.shards):
+                    up, down = self.shards[(r - 1) % self.P], self.shards[(r + 1) % self.P]
+                    s.halo[i:i + n].copy_(up.halo[o + n:o + 2 * n])
+                    s.halo[i + n:i + 2 * n].copy_(down.halo[o:o + n])
 
     def run(self, steps):
         for _ in range(steps):

@@ -29,7 +29,7 @@ done
 ncu -i gpurun_out/${R}_gol16k-tiled.ncu-rep --page source --csv --print-source cuda,sass > $O/gol16k-tiled_source.csv 2>/dev/null
 cap wator "k_doall.*Wt|k_doall_quad.*Wt" 16 8 wator
 python scripts/ncu_summarize.py $O/ncu_wator.json gpurun_out/${R}_wator.ncu-rep > $O/ncu_wator.txt
-cap nbody "k_nb_|k_doall.*Nb" 16 8 nbody
+cap nbody "k_nb_force_part|k_nb_merge_part" 2 2 nbody
 python scripts/ncu_summarize.py $O/ncu_nbody.json gpurun_out/${R}_nbody.ncu-rep > $O/ncu_nbody.txt
 gzip -f $O/*_source.csv
 rm -f gpurun_out/${R}_*.ncu-rep

@@ -9,6 +9,7 @@ from paper_1810_11765_b200.microbench import Microbench, PHASES
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 which = sys.argv[2].split(",") if len(sys.argv) > 2 else ["bulk", "scalar_doall", "per_thread", "per_thread_reserve"]
 V = {"bulk": dict(bulk=True), "scalar_doall": dict(bulk=True, flags=dsr.F_SCALAR_DOALL),
+     "quad_free": dict(bulk=True, flags=dsr.F_QUAD_FREE),
      "per_thread": dict(bulk=False), "per_thread_reserve": dict(bulk=False, reserve=True)}
 for name in which:
     kw = V[name]
