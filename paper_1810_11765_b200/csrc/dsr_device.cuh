@@ -887,6 +887,8 @@ __device__ __forceinline__ uint32_t dsr_new_warp(const DevHeap& h, uint32_t T, u
     const uint32_t nb = min((rem + cap - 1u) / cap, (uint32_t)__popc(freelanes));
     const uint32_t leader = __ffs(freelanes) - 1;
     uint64_t got = 0, wi = 0;
+    // (R-FREEROT's window here too; the full rotation measured the same step:
+    // new1 0.55 vs 0.60 ms, new4 0.54 vs 0.50 ms)
     if (lane == leader) got = bm_clear_many(h.freebm, rot_hash(h, who, 0x100000ull + round) & kFreeRotMask, nb, &wi);
     got = shfl64(0xffffffffu, got, leader);
     wi = shfl64(0xffffffffu, wi, leader);
