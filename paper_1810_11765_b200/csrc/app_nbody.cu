@@ -99,16 +99,34 @@ __device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
   f32x2 r; asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c)); return r;
 }
 
+// kNbPairs packed body pairs per thread (2 x kNbPairs bodies: i0 + 128 m):
+// every tile entry loaded from shared memory serves 2 x kNbPairs bodies, and
+// the pairs' dependency chains interleave (per body the operations and their
+// order are unchanged, so results do not depend on kNbPairs)
+#ifndef DSR_NB_PAIRS
+#define DSR_NB_PAIRS 2
+#endif
+constexpr int kNbPairs = DSR_NB_PAIRS;
+constexpr uint32_t kIBlock = 256u * kNbPairs;       // bodies per CTA (i-block)
+
 __global__ void __launch_bounds__(kPairThreads) k_nb_force_part(dsr_nbody_args a) {
   __shared__ float4 tile[256];
   const uint32_t n = a.n_total, nl = a.id_hi - a.id_lo;
-  const uint32_t i0 = a.id_lo + blockIdx.x * 256 + threadIdx.x, i1 = i0 + 128;
-  const float4 p0 = i0 < a.id_hi ? s4(a, i0) : make_float4(0.f, 0.f, 0.f, 0.f);
-  const float4 p1 = i1 < a.id_hi ? s4(a, i1) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const uint32_t ib = a.id_lo + blockIdx.x * kIBlock + threadIdx.x;
   const float eps2 = a.eps * a.eps;
-  const f32x2 PX = pk2(p0.x, p1.x), PY = pk2(p0.y, p1.y), E2 = pk2(eps2, eps2);
+  const f32x2 E2 = pk2(eps2, eps2);
+  f32x2 PX[kNbPairs], PY[kNbPairs], AX[kNbPairs], AY[kNbPairs];
+#pragma unroll
+  for (int q = 0; q < kNbPairs; ++q) {
+    const uint32_t i0 = ib + 256u * q, i1 = i0 + 128u;
+    const float4 p0 = i0 < a.id_hi ? s4(a, i0) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 p1 = i1 < a.id_hi ? s4(a, i1) : make_float4(0.f, 0.f, 0.f, 0.f);
+    PX[q] = pk2(p0.x, p1.x);
+    PY[q] = pk2(p0.y, p1.y);
+    AX[q] = pk2(0.f, 0.f);
+    AY[q] = pk2(0.f, 0.f);
+  }
   const uint32_t jb = blockIdx.y * kChunk, je = min(jb + kChunk, n);
-  f32x2 AX = pk2(0.f, 0.f), AY = pk2(0.f, 0.f);
   for (uint32_t j0 = jb; j0 < je; j0 += 256) {
     __syncthreads();
     const uint32_t ja = j0 + threadIdx.x, jc = ja + 128;
@@ -118,24 +136,32 @@ __global__ void __launch_bounds__(kPairThreads) k_nb_force_part(dsr_nbody_args a
 #pragma unroll 8
     for (int k = 0; k < 256; ++k) {
       const float4 p = tile[k];                      // out-of-range entries have m = 0
-      // per body: dx = x_j - x_i, r = dx^2 + (dy^2 + eps^2), w = ((m_j v) v) v with
-      // v = rsqrt(r), a += dx w  (P:171-174 with Plummer softening, R-NBODY)
-      const f32x2 DX = sub2(pk2(p.x, p.x), PX), DY = sub2(pk2(p.y, p.y), PY);
-      const f32x2 R = fma2(DX, DX, fma2(DY, DY, E2));
-      float r0, r1;
-      upk2(R, r0, r1);
-      const f32x2 V = pk2(rsqrtf(r0), rsqrtf(r1));
-      const f32x2 W = mul2(mul2(mul2(pk2(p.z, p.z), V), V), V);
-      AX = fma2(DX, W, AX);
-      AY = fma2(DY, W, AY);
+      const f32x2 JX = pk2(p.x, p.x), JY = pk2(p.y, p.y), JM = pk2(p.z, p.z);
+#pragma unroll
+      for (int q = 0; q < kNbPairs; ++q) {
+        // per body: dx = x_j - x_i, r = dx^2 + (dy^2 + eps^2), w = ((m_j v) v) v with
+        // v = rsqrt(r), a += dx w  (P:171-174 with Plummer softening, R-NBODY)
+        const f32x2 DX = sub2(JX, PX[q]), DY = sub2(JY, PY[q]);
+        const f32x2 R = fma2(DX, DX, fma2(DY, DY, E2));
+        float r0, r1;
+        upk2(R, r0, r1);
+        const f32x2 V = pk2(rsqrtf(r0), rsqrtf(r1));
+        const f32x2 W = mul2(mul2(mul2(JM, V), V), V);
+        AX[q] = fma2(DX, W, AX[q]);
+        AY[q] = fma2(DY, W, AY[q]);
+      }
     }
   }
-  float ax0, ax1, ay0, ay1;
-  upk2(AX, ax0, ax1);
-  upk2(AY, ay0, ay1);
   float2* part = reinterpret_cast<float2*>(a.scratch) + (size_t)blockIdx.y * nl;
-  if (i0 < a.id_hi) part[i0 - a.id_lo] = make_float2(ax0, ay0);
-  if (i1 < a.id_hi) part[i1 - a.id_lo] = make_float2(ax1, ay1);
+#pragma unroll
+  for (int q = 0; q < kNbPairs; ++q) {
+    const uint32_t i0 = ib + 256u * q, i1 = i0 + 128u;
+    float ax0, ax1, ay0, ay1;
+    upk2(AX[q], ax0, ax1);
+    upk2(AY[q], ay0, ay1);
+    if (i0 < a.id_hi) part[i0 - a.id_lo] = make_float2(ax0, ay0);
+    if (i1 < a.id_hi) part[i1 - a.id_lo] = make_float2(ax1, ay1);
+  }
 }
 
 // f_i = G m_i sum_j m_j (p_j - p_i) / (|p_j - p_i|^2 + eps^2)^{3/2}, chunks summed in order
@@ -189,14 +215,24 @@ struct NbMove {   // semi-implicit Euler, velocity first
 __global__ void __launch_bounds__(kPairThreads) k_nb_merge_part(dsr_nbody_args a) {
   __shared__ float4 tile[256];
   const uint32_t n = a.n_total, nl = a.id_hi - a.id_lo;
-  const uint32_t i0 = a.id_lo + blockIdx.x * 256 + threadIdx.x, i1 = i0 + 128;
-  const float4 p0 = i0 < a.id_hi ? s4(a, i0) : make_float4(0.f, 0.f, 0.f, 0.f);
-  const float4 p1 = i1 < a.id_hi ? s4(a, i1) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const uint32_t ib = a.id_lo + blockIdx.x * kIBlock + threadIdx.x;
   const float R2 = a.R * a.R;
-  const f32x2 PX = pk2(p0.x, p1.x), PY = pk2(p0.y, p1.y);
+  f32x2 PX[kNbPairs], PY[kNbPairs];
+  float M[2 * kNbPairs], D[2 * kNbPairs];
+  uint32_t B[2 * kNbPairs];
+#pragma unroll
+  for (int q = 0; q < kNbPairs; ++q) {
+    const uint32_t i0 = ib + 256u * q, i1 = i0 + 128u;
+    const float4 p0 = i0 < a.id_hi ? s4(a, i0) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 p1 = i1 < a.id_hi ? s4(a, i1) : make_float4(0.f, 0.f, 0.f, 0.f);
+    PX[q] = pk2(p0.x, p1.x);
+    PY[q] = pk2(p0.y, p1.y);
+    M[2 * q] = p0.z;
+    M[2 * q + 1] = p1.z;
+    D[2 * q] = D[2 * q + 1] = R2;                    // strict d2 < R^2, ties -> smaller j (j ascends)
+    B[2 * q] = B[2 * q + 1] = kNone;
+  }
   const uint32_t jb = blockIdx.y * kChunk, je = min(jb + kChunk, n);
-  uint32_t b0 = kNone, b1 = kNone;
-  float d0 = R2, d1 = R2;                              // strict d2 < R^2, ties -> smaller j (j ascends)
   for (uint32_t j0 = jb; j0 < je; j0 += 256) {
     __syncthreads();
     const uint32_t ja = j0 + threadIdx.x, jc = ja + 128;
@@ -206,20 +242,34 @@ __global__ void __launch_bounds__(kPairThreads) k_nb_merge_part(dsr_nbody_args a
 #pragma unroll 4
     for (int k = 0; k < 256; ++k) {
       const float4 p = tile[k];
-      // per body (packed f32x2): e = dx^2 + dy^2 as fma(dx, dx, dy * dy)
-      const f32x2 DX = sub2(pk2(p.x, p.x), PX), DY = sub2(pk2(p.y, p.y), PY);
-      float e0, e1;
-      upk2(fma2(DX, DX, mul2(DY, DY)), e0, e1);
-      if (e0 < d0 || e1 < d1) {                        // rare: a body within R
-        const uint32_t j = j0 + k;
-        if (e0 < d0 && p.z > 0.f && (p.z > p0.z || (p.z == p0.z && j > i0))) { d0 = e0; b0 = j; }
-        if (e1 < d1 && p.z > 0.f && (p.z > p1.z || (p.z == p1.z && j > i1))) { d1 = e1; b1 = j; }
+      const f32x2 JX = pk2(p.x, p.x), JY = pk2(p.y, p.y);
+#pragma unroll
+      for (int q = 0; q < kNbPairs; ++q) {
+        // per body (packed f32x2): e = dx^2 + dy^2 as fma(dx, dx, dy * dy)
+        const f32x2 DX = sub2(JX, PX[q]), DY = sub2(JY, PY[q]);
+        float e[2];
+        upk2(fma2(DX, DX, mul2(DY, DY)), e[0], e[1]);
+        if (e[0] < D[2 * q] || e[1] < D[2 * q + 1]) {    // rare: a body within R
+          const uint32_t j = j0 + k;
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const uint32_t i = ib + 256u * q + 128u * u;
+            const float mi = M[2 * q + u];
+            if (e[u] < D[2 * q + u] && p.z > 0.f && (p.z > mi || (p.z == mi && j > i))) {
+              D[2 * q + u] = e[u];
+              B[2 * q + u] = j;
+            }
+          }
+        }
       }
     }
   }
   uint2* part = reinterpret_cast<uint2*>(a.scratch) + (size_t)blockIdx.y * nl;
-  if (i0 < a.id_hi) part[i0 - a.id_lo] = make_uint2(__float_as_uint(d0), b0);
-  if (i1 < a.id_hi) part[i1 - a.id_lo] = make_uint2(__float_as_uint(d1), b1);
+#pragma unroll
+  for (int m = 0; m < 2 * kNbPairs; ++m) {
+    const uint32_t i = ib + 128u * m;
+    if (i < a.id_hi) part[i - a.id_lo] = make_uint2(__float_as_uint(D[m]), B[m]);
+  }
 }
 
 __global__ void k_nb_merge_pick(DevHeap h, dsr_nbody_args a) {
@@ -311,7 +361,7 @@ bool nb_method_info(uint32_t id, MethodInfo* mi) {
 }
 
 static dim3 pair_grid(const dsr_nbody_args& a) {
-  return dim3((a.id_hi - a.id_lo + 255) / 256, (a.n_total + kChunk - 1) / kChunk);
+  return dim3((a.id_hi - a.id_lo + kIBlock - 1) / kIBlock, (a.n_total + kChunk - 1) / kChunk);
 }
 
 bool nb_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot, const void* args) {

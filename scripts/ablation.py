@@ -16,7 +16,8 @@ import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-FLAGS = {"default": 0, "NoShift": 0x1, "NoCoal": 0x2, "NoCoal-NoShift": 0x3, "NoHint": 0x10, "SlotRotate": 0x80}
+FLAGS = {"default": 0, "NoShift": 0x1, "NoCoal": 0x2, "NoCoal-NoShift": 0x3, "NoHint": 0x10, "SlotRotate": 0x80,
+         "QuadFree": 0x200}
 
 
 def agent_frag(heap, types):
@@ -33,7 +34,7 @@ def one_mb(cfg):
     from paper_1810_11765_b200.microbench import Microbench
     n1, n2 = cfg.get("n1", 1 << 26), cfg.get("n2", 1 << 25)
     mb = Microbench(n1=n1, n2=n2, flags=cfg["flags"], retries=cfg["r"], reserve=cfg["reserve"],
-                    heap_bytes=cfg.get("heap_bytes"))
+                    heap_bytes=cfg.get("heap_bytes"), bulk=cfg.get("bulk", False))
     mb.step()                                          # warm-up
     torch.cuda.synchronize()
     times = []
@@ -49,14 +50,14 @@ def one_mb(cfg):
     if cfg["reserve"]:
         for t, c in enumerate(mb._counts(0, n1)):
             h.reserve_blocks(t, -(-c // h.cap[t]))
-    h.launch(dsr.K_MB_NEW, n1, dsr.MbNewArgs(1, 0))
+    h.launch(mb.kernel, n1, dsr.MbNewArgs(1, 0))
     if cfg["reserve"]:
         for t in range(3):
             h.trim(t)
     f1, b1 = agent_frag(h, [0, 1, 2])
     for t in range(3):
         h.parallel_do(t, dsr.M_MB_FREE_ODD, None)
-    h.launch(dsr.K_MB_NEW, n2, dsr.MbNewArgs(1, n1))
+    h.launch(mb.kernel, n2, dsr.MbNewArgs(1, n1))
     f4, b4 = agent_frag(h, [0, 1, 2])
     assert h.poll_error() == dsr.OK
     names = ["init", "new1", "reduce2", "free3", "new4", "reduce5", "drain6"]
@@ -118,6 +119,11 @@ def runs():
         return [("wator", {"name": n, "flags": FLAGS[n], "r": 5, **hb}) for n in ("NoShift", "NoCoal-NoShift")
                 for hb in ({}, {"heap_bytes": 4 << 30})]
     out = []
+    # the bench's allocation kernel (warp-cooperative, R-BULK) and its free-pass ablation (R-BLOCKDOALL)
+    out.append(("mb", {"name": "bulk (bench default)", "flags": 0, "r": 5, "reserve": False, "bulk": True}))
+    out.append(("mb", {"name": "bulk, QuadFree", "flags": FLAGS["QuadFree"], "r": 5, "reserve": False, "bulk": True}))
+    out.append(("mb", {"name": "bulk, NoShift", "flags": FLAGS["NoShift"], "r": 5, "reserve": False, "bulk": True}))
+    # the paper-shaped per-thread kernel (one Alg. 1 request per coalesced lane group) under the paper's ablations
     for name in ["default", "NoShift", "NoCoal", "NoCoal-NoShift", "NoHint", "SlotRotate"]:
         out.append(("mb", {"name": name, "flags": FLAGS[name], "r": 5, "reserve": True}))
     out.append(("mb", {"name": "paper-exact (NoHint, SlotRotate, no reserve)", "flags": 0x90, "r": 5, "reserve": False}))
