@@ -98,6 +98,7 @@ typedef struct {
 #define DSR_F_SLOT_ROTATE 0x80u /* paper: also rotate a block's object bitmap before choosing its free slots; off by default */
 #define DSR_F_SCALAR_DOALL 0x100u /* ablation: one thread per object in methods that also have a quad-mapped (vectorised) body */
 #define DSR_F_QUAD_FREE   0x200u /* ablation: microbench free passes as quad-mapped do-alls (lanes of a block combine their masks) instead of block-mapped (one lane per block) */
+#define DSR_F_BULK_DENSE  0x400u /* warp-cooperative new (R-BULK): one failed lookup attempt per round instead of per failed lane -- fills partially free blocks longer (lower fragmentation, slower) */
 
 typedef struct {
   uint32_t active_retries;   /* r: try_find_set attempts before the slow path (Fig. 11); 0 -> 5 */

@@ -24,6 +24,7 @@ F_NO_ROTATE, F_NO_COALESCE, F_STATS, F_SPIN_ON_OOM, F_NO_HINT, F_CTA_NEW, F_HOME
     0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40, 0x80)
 F_SCALAR_DOALL = 0x100
 F_QUAD_FREE = 0x200
+F_BULK_DENSE = 0x400
 
 # ids (mirror include/dsr.h)
 K_MB_NEW, M_MB_REDUCE, M_MB_FREE_ODD, M_MB_FREE_ALL = 1, 1, 2, 3

@@ -17,7 +17,7 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 FLAGS = {"default": 0, "NoShift": 0x1, "NoCoal": 0x2, "NoCoal-NoShift": 0x3, "NoHint": 0x10, "SlotRotate": 0x80,
-         "QuadFree": 0x200}
+         "QuadFree": 0x200, "BulkDense": 0x400}
 
 
 def agent_frag(heap, types):
@@ -123,6 +123,7 @@ def runs():
     out.append(("mb", {"name": "bulk (bench default)", "flags": 0, "r": 5, "reserve": False, "bulk": True}))
     out.append(("mb", {"name": "bulk, QuadFree", "flags": FLAGS["QuadFree"], "r": 5, "reserve": False, "bulk": True}))
     out.append(("mb", {"name": "bulk, NoShift", "flags": FLAGS["NoShift"], "r": 5, "reserve": False, "bulk": True}))
+    out.append(("mb", {"name": "bulk, BulkDense", "flags": FLAGS["BulkDense"], "r": 5, "reserve": False, "bulk": True}))
     # the paper-shaped per-thread kernel (one Alg. 1 request per coalesced lane group) under the paper's ablations
     for name in ["default", "NoShift", "NoCoal", "NoCoal-NoShift", "NoHint", "SlotRotate"]:
         out.append(("mb", {"name": name, "flags": FLAGS[name], "r": 5, "reserve": True}))
