@@ -212,6 +212,12 @@ struct NbMove {   // semi-implicit Euler, velocity first
 };
 
 // prepare_merge partials: per (i, chunk) the best (d2, j) with (m_j, j) >lex (m_i, i), d2 < R^2
+// Merge search: for each body the nearest heavier (m, id) body within R.
+// The common path of a tile entry is the packed distance and a running min;
+// only a group of kMergeGroup entries that has some distance below the
+// thread's largest current bound is re-examined with the exact per-body test
+// (in ascending j, so ties resolve as in a sequential scan).
+constexpr int kMergeGroup = 4;
 __global__ void __launch_bounds__(kPairThreads) k_nb_merge_part(dsr_nbody_args a) {
   __shared__ float4 tile[256];
   const uint32_t n = a.n_total, nl = a.id_hi - a.id_lo;
@@ -232,6 +238,7 @@ __global__ void __launch_bounds__(kPairThreads) k_nb_merge_part(dsr_nbody_args a
     D[2 * q] = D[2 * q + 1] = R2;                    // strict d2 < R^2, ties -> smaller j (j ascends)
     B[2 * q] = B[2 * q + 1] = kNone;
   }
+  float dmax = R2;                                   // max of the D[] (they only decrease)
   const uint32_t jb = blockIdx.y * kChunk, je = min(jb + kChunk, n);
   for (uint32_t j0 = jb; j0 < je; j0 += 256) {
     __syncthreads();
@@ -239,28 +246,47 @@ __global__ void __launch_bounds__(kPairThreads) k_nb_merge_part(dsr_nbody_args a
     tile[threadIdx.x] = ja < je ? s4(a, ja) : make_float4(0.f, 0.f, 0.f, 0.f);
     tile[threadIdx.x + 128] = jc < je ? s4(a, jc) : make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
-#pragma unroll 4
-    for (int k = 0; k < 256; ++k) {
-      const float4 p = tile[k];
-      const f32x2 JX = pk2(p.x, p.x), JY = pk2(p.y, p.y);
+#pragma unroll 2
+    for (int k0 = 0; k0 < 256; k0 += kMergeGroup) {
+      // per body (packed f32x2): e = dx^2 + dy^2 as fma(dx, dx, dy * dy)
+      f32x2 E[kMergeGroup][kNbPairs];
+      float emin = dmax;
 #pragma unroll
-      for (int q = 0; q < kNbPairs; ++q) {
-        // per body (packed f32x2): e = dx^2 + dy^2 as fma(dx, dx, dy * dy)
-        const f32x2 DX = sub2(JX, PX[q]), DY = sub2(JY, PY[q]);
-        float e[2];
-        upk2(fma2(DX, DX, mul2(DY, DY)), e[0], e[1]);
-        if (e[0] < D[2 * q] || e[1] < D[2 * q + 1]) {    // rare: a body within R
-          const uint32_t j = j0 + k;
+      for (int g = 0; g < kMergeGroup; ++g) {
+        const float4 p = tile[k0 + g];
+        const f32x2 JX = pk2(p.x, p.x), JY = pk2(p.y, p.y);
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const uint32_t i = ib + 256u * q + 128u * u;
-            const float mi = M[2 * q + u];
-            if (e[u] < D[2 * q + u] && p.z > 0.f && (p.z > mi || (p.z == mi && j > i))) {
-              D[2 * q + u] = e[u];
-              B[2 * q + u] = j;
+        for (int q = 0; q < kNbPairs; ++q) {
+          const f32x2 DX = sub2(JX, PX[q]), DY = sub2(JY, PY[q]);
+          E[g][q] = fma2(DX, DX, mul2(DY, DY));
+          float e0, e1;
+          upk2(E[g][q], e0, e1);
+          emin = fminf(emin, fminf(e0, e1));
+        }
+      }
+      if (emin < dmax) {                             // rare: some body within its bound
+#pragma unroll
+        for (int g = 0; g < kMergeGroup; ++g) {
+          const float4 p = tile[k0 + g];
+          const uint32_t j = j0 + k0 + g;
+#pragma unroll
+          for (int q = 0; q < kNbPairs; ++q) {
+            float e[2];
+            upk2(E[g][q], e[0], e[1]);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const uint32_t i = ib + 256u * q + 128u * u;
+              const float mi = M[2 * q + u];
+              if (e[u] < D[2 * q + u] && p.z > 0.f && (p.z > mi || (p.z == mi && j > i))) {
+                D[2 * q + u] = e[u];
+                B[2 * q + u] = j;
+              }
             }
           }
         }
+        dmax = D[0];
+#pragma unroll
+        for (int m = 1; m < 2 * kNbPairs; ++m) dmax = fmaxf(dmax, D[m]);
       }
     }
   }
