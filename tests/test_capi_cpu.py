@@ -134,3 +134,22 @@ def test_product_package_never_imports_the_oracle():
     for p in list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")) + list(pkg.rglob("*.h")):
         txt = p.read_text()
         assert not re.search(r"(^|\n)\s*(from|import)\s+oracle|liboracle|oracle\.h|oracle/", txt), p
+
+
+def test_binding_ids_and_flags_mirror_the_header():
+    """Every DSR_F_* flag and DSR_[MKC]_* id of include/dsr.h has the same
+    value under the same name (prefix dropped) in the ctypes binding."""
+    import re
+    from pathlib import Path
+    from paper_1810_11765_b200 import dsr
+    hdr = (Path(__file__).resolve().parents[1] / "include" / "dsr.h").read_text()
+    found = {}
+    for name, val in re.findall(r"#define DSR_(F_[A-Z0-9_]+)\s+(0x[0-9a-fA-F]+)u", hdr):
+        found[name] = int(val, 16)
+    for name, val in re.findall(r"\bDSR_([MKC]_[A-Z0-9_]+)\s*=\s*(\d+)", hdr):
+        found[name] = int(val)
+    assert len(found) > 40
+    missing = [n for n in found if not hasattr(dsr, n)]
+    assert not missing, missing
+    wrong = {n: (v, getattr(dsr, n)) for n, v in found.items() if getattr(dsr, n) != v}
+    assert not wrong, wrong
