@@ -137,8 +137,11 @@ __device__ __forceinline__ void mb_construct(const DevHeap& h, uint32_t T, const
   }
 }
 
+#ifndef DSR_MB_BULK_MINB
+#define DSR_MB_BULK_MINB 1
+#endif
 template <bool IN = false>
-__global__ void __launch_bounds__(256) k_mb_new_bulk(DevHeap h, uint64_t n, dsr_mb_new_args a) {
+__global__ void __launch_bounds__(256, DSR_MB_BULK_MINB) k_mb_new_bulk(DevHeap h, uint64_t n, dsr_mb_new_args a) {
   const uint64_t kp = rng_prefix(a.seed, 0);
   const uint32_t lane = threadIdx.x & 31;
   for (;;) {
