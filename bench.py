@@ -49,6 +49,8 @@ def parse():
                                                                      "gol16k-tiled", "nbody"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-apps", action="store_true", help="skip the per-app block of the default line")
+    ap.add_argument("--launch-list", action="store_true",
+                    help="run only W + K microbench steps (for ncu launch lists) and print no bench line")
     ap.add_argument("--dry-run", action="store_true",
                     help="no GPU work: exercise the launch / rank aggregation / JSON path (gloo; tests)")
     return ap.parse_args()
@@ -280,6 +282,16 @@ def run_ours(args):
         step()
     torch.cuda.synchronize()
     assert mb.heap.poll_error() == dsr.OK, "device error during warm-up"
+    if args.launch_list:
+        # only the step's own kernels (for `ncu --metrics gpu__time_duration.sum`
+        # launch lists): K steps after the warm-up, no probe / variants / e2e / apps
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize()
+        assert mb.heap.poll_error() == dsr.OK
+        if rank == 0:
+            print(json.dumps({"launch_list_steps": args.steps, "warmup": args.warmup}), flush=True)
+        return
 
     # L2 atomic peak (roofline denominator of the allocator's atomics): the
     # library's probe, hashed independent u64 atomicOr-with-return over a

@@ -138,7 +138,7 @@ __device__ __forceinline__ void mb_construct(const DevHeap& h, uint32_t T, const
 }
 
 #ifndef DSR_MB_BULK_MINB
-#define DSR_MB_BULK_MINB 1
+#define DSR_MB_BULK_MINB 6   // 6 CTAs x 256 threads per SM (40 registers, 16 B of spills): sweep 1 / 5 / 6 / 7 / 8 -> 2.14 / 2.04 / 1.99 / 2.35 / 2.36 ms per step
 #endif
 template <bool IN = false>
 __global__ void __launch_bounds__(256, DSR_MB_BULK_MINB) k_mb_new_bulk(DevHeap h, uint64_t n, dsr_mb_new_args a) {

@@ -7,7 +7,7 @@ R=${R:-r02}
 mkdir -p gpurun_out/prof_${R}
 bash scripts/gpu_ncu_apps.sh
 timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_launches.csv \
-  python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-apps > gpurun_out/ncu_launches.log 2>&1
+  python bench.py --steps 1 --warmup 1 --launch-list > gpurun_out/ncu_launches.log 2>&1
 # the bench must find the summaries in profiles/ (same source hash) on this box too
 mkdir -p profiles/${R}
 cp gpurun_out/prof_${R}/ncu_*.json profiles/${R}/

@@ -51,7 +51,7 @@ if lc.exists():
                 a[0] += 1
                 a[1] += float(d["Metric Value"].replace(",", "")) * scale[d["Metric Unit"]]
     tot = sum(a[1] for a in agg.values()) or 1.0
-    lines = [f"# {rnd} launch list: one bench.py step (+ warm-up step), "
+    lines = [f"# {rnd} launch list: one bench.py step (+ warm-up step; `bench.py --launch-list`), "
              "ncu --metrics gpu__time_duration.sum --clock-control none", "",
              "Cold-cache, serialised launches: compare SHARES, not absolute times.", "",
              "| kernel | launches | total us | share |", "|---|---|---|---|"]
