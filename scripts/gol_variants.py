@@ -7,8 +7,12 @@ from paper_1810_11765_b200.gol import GameOfLife, ALIVE, CAND
 
 G = int(sys.argv[1]) if len(sys.argv) > 1 else 6
 a0 = I.gol_soup(16384, 16384, 0.25, 42)
+import os
+ONLY = os.environ.get("GOL_VARIANTS", "handles,tiled_prepare,tiled_all,bits").split(",")
 for name, kw in (("handles", {}), ("tiled_prepare", {"tiled": "prepare"}), ("tiled_all", {"tiled": "all"}),
                  ("bits", {"bit_mirror": True})):
+    if name not in ONLY:
+        continue
     s = torch.cuda.Stream()
     torch.cuda.set_stream(s)
     g = GameOfLife(a0, stream=s, **kw)

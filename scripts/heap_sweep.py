@@ -7,7 +7,8 @@ from paper_1810_11765_b200 import inputs as I
 from paper_1810_11765_b200.wator import WaTor
 
 k, e, n = I.wator_init(2048, 2048, seed=42)
-for gib in (0.5, 2, 8, 16):
+import os
+for gib in [float(x) for x in os.environ.get("HEAP_GIB", "0.5,2,8,16").split(",")]:
     s = torch.cuda.Stream()
     torch.cuda.set_stream(s)
     w = WaTor(k, e, n, heap_bytes=int(gib * (1 << 30)), stream=s)
