@@ -538,6 +538,25 @@ def app_traffic(name, kernels=None):
     return best
 
 
+def full_length(step, n, stream, live_types, heap):
+    """The BASELINE config's whole run (n steps from the initial state, which
+    the caller just built): one pair of CUDA events around all n steps, the
+    live counts of `live_types` recorded on the device after every step (tiny
+    kernels, inside the events).  Returns (ms per step, live counts (n, k))."""
+    import torch
+    cnt = torch.zeros(n, len(live_types), dtype=torch.int64, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for k in range(n):
+        step()
+        for j, t in enumerate(live_types):
+            heap.live_count_async(t, cnt[k, j], stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / n, cnt.cpu().numpy()
+
+
 def hbm_roofline(kernel, nbytes, ms, peak, peak_src, note, bound="hbm"):
     gbs = nbytes / (ms * 1e-3) / 1e9
     return {"bound": bound, "kernel": kernel, "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
@@ -608,6 +627,20 @@ def app_block(stream, peak, peak_src, sm_mhz, want_cpu=True):
                                                                   "the 8 handles, same algorithmic definition" if bits else ""),
                                      bound="latency" if Wd == 64 else "hbm"),
         }
+        if name == "gol_16384":
+            # the whole BASELINE run: 1000 generations from the soup (the density falls
+            # from 0.25 to a few %, so late generations are much cheaper than the first)
+            del sim
+            torch.cuda.empty_cache()
+            sim = GameOfLife(a0, stream=stream, bit_mirror=bits, tiled=tiled)
+            init = sim.heap.live_count(0, stream) + sim.heap.live_count(1, stream)
+            fms, flv = full_length(sim.generation, 1000, stream, (0, 1), sim.heap)
+            visits = 2 * (init + int(flv[:-1].sum()))            # objects at the start of each generation
+            out[name]["full_length"] = {
+                "generations": 1000, "ms_per_step": fms, "value": visits / (1000 * fms * 1e-3),
+                "unit": "object-updates/s", "objects_first_last": [init, int(flv[-1].sum())],
+                "note": "all 1000 generations of configs[3] timed as one region (live counts recorded on the "
+                        "device each generation); object-updates = prepare + update visit of every object"}
         tr = app_traffic({"gol_16384": "gol16k-tiled", "gol_16384_blocklist": "gol16k",
                           "gol_16384_bits": "gol16k-bits"}.get(name))
         if tr:
@@ -680,6 +713,22 @@ def app_block(stream, peak, peak_src, sm_mhz, want_cpu=True):
         out["wator_2048"]["roofline"].update(tr)
     del sim, base
     torch.cuda.empty_cache()
+    sim = WaTor(kind, egg, en, FB=6, SB=12, SS=6, seed=42, stream=stream)
+    sim.capture()                                                # runs step 1 (the warm-up of the capture)
+    ag1 = sim.heap.live_count(0, stream) + sim.heap.live_count(1, stream)
+    fms, flv = full_length(sim.graph.replay, 499, stream, (0, 1), sim.heap)
+    last = [int(flv[-1, 0]), int(flv[-1, 1])]
+    gold = ROOT / "tests" / "golden" / "wator2048_500steps.npz"
+    want = [int(v) for v in np.load(gold)["counters"][-1, :2]] if gold.exists() else None
+    out["wator_2048"]["full_length"] = {
+        "steps": 500, "timed_steps": 499, "ms_per_step": fms,
+        "value": (4 * cells * 499 + 2 * (ag1 + int(flv[:-1].sum()))) / (499 * fms * 1e-3),
+        "unit": "object-updates/s", "fish_sharks_after_500": last, "equals_oracle_golden": last == want,
+        "note": "configs[1]: step 1 runs while the step's CUDA graph is captured, steps 2-500 are graph replays "
+                "timed as one region; the final populations are checked against the oracle's "
+                "(tests/golden/wator2048_500steps.npz)"}
+    del sim
+    torch.cuda.empty_cache()
 
     def wator_cpu():
         from oracle import oracle as O
@@ -739,6 +788,15 @@ def app_block(stream, peak, peak_src, sm_mhz, want_cpu=True):
     tr = app_traffic("nbody", kernels=("k_nb_force_part",))
     if tr:
         out["nbody_65536"]["roofline"].update(tr)
+    del sim
+    torch.cuda.empty_cache()
+    sim = NBody(st, merges=True, stream=stream, **I.NBODY_PARAMS)
+    fms, flv = full_length(lambda: sim.step(stream), 1000, stream, (0,), sim.heap)
+    out["nbody_65536"]["full_length"] = {
+        "steps": 1000, "ms_per_step": fms,
+        "value": 8 * (65536 + float(flv[:-1, 0].sum())) / (1000 * fms * 1e-3), "unit": "object-updates/s",
+        "bodies_last": int(flv[-1, 0]),
+        "note": "all 1000 steps of configs[2] timed as one region (bodies merge: 65,536 -> ~18 k)"}
     del sim
     torch.cuda.empty_cache()
     from paper_1810_11765_b200.nbody import NBodyStatic
