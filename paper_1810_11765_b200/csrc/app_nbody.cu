@@ -235,16 +235,27 @@ __global__ void __launch_bounds__(kPairThreads) k_nb_merge_part(dsr_nbody_args a
     PY[q] = pk2(p0.y, p1.y);
     M[2 * q] = p0.z;
     M[2 * q + 1] = p1.z;
-    D[2 * q] = D[2 * q + 1] = R2;                    // strict d2 < R^2, ties -> smaller j (j ascends)
+    // strict d2 < R^2, ties -> smaller j (j ascends).  An empty id (m = 0: no
+    // body, or one deleted by a merge; its snapshot entry is zero) searches
+    // nothing -- k_nb_merge_pick skips it -- so its bound is -1
+    D[2 * q] = p0.z > 0.f ? R2 : -1.f;
+    D[2 * q + 1] = p1.z > 0.f ? R2 : -1.f;
     B[2 * q] = B[2 * q + 1] = kNone;
   }
-  float dmax = R2;                                   // max of the D[] (they only decrease)
+  float dmax = D[0];                                 // max of the D[] (they only decrease)
+#pragma unroll
+  for (int m = 1; m < 2 * kNbPairs; ++m) dmax = fmaxf(dmax, D[m]);
   const uint32_t jb = blockIdx.y * kChunk, je = min(jb + kChunk, n);
   for (uint32_t j0 = jb; j0 < je; j0 += 256) {
     __syncthreads();
     const uint32_t ja = j0 + threadIdx.x, jc = ja + 128;
-    tile[threadIdx.x] = ja < je ? s4(a, ja) : make_float4(0.f, 0.f, 0.f, 0.f);
-    tile[threadIdx.x + 128] = jc < je ? s4(a, jc) : make_float4(0.f, 0.f, 0.f, 0.f);
+    // empty ids (m = 0, at the origin in the snapshot) can never be a merge
+    // target (the exact test wants m_j > 0): they are staged far away, so they
+    // never make a group take the exact path
+    const float4 fa = ja < je ? s4(a, ja) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 fc = jc < je ? s4(a, jc) : make_float4(0.f, 0.f, 0.f, 0.f);
+    tile[threadIdx.x] = fa.z > 0.f ? fa : make_float4(1e18f, 1e18f, 0.f, 0.f);
+    tile[threadIdx.x + 128] = fc.z > 0.f ? fc : make_float4(1e18f, 1e18f, 0.f, 0.f);
     __syncthreads();
 #pragma unroll 2
     for (int k0 = 0; k0 < 256; k0 += kMergeGroup) {
