@@ -770,7 +770,7 @@ def app_block(stream, peak, peak_src, sm_mhz, want_cpu=True):
     lv = cnt.cpu().numpy()[:, 0]
     ms = sum(t) / K
     force_ms = sum(fev[3 + k][0].elapsed_time(fev[3 + k][1]) for k in range(K)) / K
-    pairs = 65536 * 65536                                       # the force pass evaluates every id pair (S0)
+    pairs = float((lv.astype(np.float64) ** 2).mean())          # the force pass: every pair of existing bodies
     fp32_peak = 148 * 128 * sm_mhz * 1e6                        # FP32 lanes x SM clock
     ops = 9.0 * pairs                                           # 9 FP32 ops per pair + 1 MUFU.RSQ
     out["nbody_65536"] = {
@@ -783,7 +783,8 @@ def app_block(stream, peak, peak_src, sm_mhz, want_cpu=True):
                      "frac": ops / (force_ms * 1e-3) / fp32_peak, "force_ms": force_ms,
                      "peak_source": "148 SMs x 128 FP32 lanes x sampled SM clock (B200_PROFILING.md unit counts)",
                      "note": "9 FP32 ops per pair (2 FADD, 2 FFMA for r^2, 3 FMUL, 2 FFMA accumulate) on packed "
-                             "f32x2 pairs; the snapshot is SMEM/L2-resident"},
+                             "f32x2 pairs, over the pairs of existing bodies (the live list); the snapshot is "
+                             "SMEM/L2-resident"},
     }
     tr = app_traffic("nbody", kernels=("k_nb_force_part",))
     if tr:

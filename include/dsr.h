@@ -466,6 +466,9 @@ typedef struct {
   uint32_t n_total, id_lo, id_hi;
   float* out;                         /* dump: 6 floats per id (x, y, vx, vy, m, alive) */
   float* scratch;                     /* all-pairs partials: >= 2 * ceil(n_total/4096) * (id_hi - id_lo) floats */
+  float* live;                        /* the all-pairs passes' live list (device, caller-owned, scratch):
+                                         >= 4 * n_total + ceil(n_total/4096) floats; each 4096-id chunk of S
+                                         compacted to its bodies with m > 0 (x, y, m, id bits), ascending id */
 } dsr_nbody_args;
 enum {
   DSR_C_NB_BODY = 30,            /* parallel_new<Body>(id_hi - id_lo): body i gets id id_lo + i */
@@ -526,6 +529,7 @@ typedef struct {
   float G, dt, eps, R;
   uint32_t n;
   uint32_t merges;      /* 0: App2 N-Body (force + move only) */
+  float* live;          /* live list scratch, as dsr_nbody_args.live */
 } dsr_nbody_static_args;
 dsr_status dsr_nbody_static_step(const dsr_nbody_static_args* args, uint32_t steps, void* stream);
 

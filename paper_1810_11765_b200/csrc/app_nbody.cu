@@ -99,43 +99,118 @@ __device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
   f32x2 r; asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c)); return r;
 }
 
-// kNbPairs packed body pairs per thread (2 x kNbPairs bodies: i0 + 128 m):
-// every tile entry loaded from shared memory serves 2 x kNbPairs bodies, and
-// the pairs' dependency chains interleave (per body the operations and their
-// order are unchanged, so results do not depend on kNbPairs)
+// kNbPairs packed body pairs per thread (2 x kNbPairs bodies): every tile
+// entry loaded from shared memory serves 2 x kNbPairs bodies, and the pairs'
+// dependency chains interleave (per body the operations and their order are
+// unchanged, so results do not depend on kNbPairs)
 #ifndef DSR_NB_PAIRS
 #define DSR_NB_PAIRS 2
 #endif
 constexpr int kNbPairs = DSR_NB_PAIRS;
 constexpr uint32_t kIBlock = 256u * kNbPairs;       // bodies per CTA (i-block)
+constexpr uint32_t kIBlocksPerChunk = kChunk / kIBlock;
+
+// ---- the live list: both sides of the all-pairs passes run over the bodies
+// that exist (device_do visits the Body objects), not over the whole id
+// space -- the merges take 65,536 bodies down to ~18 k over the 1000 steps.
+// Each 4096-id chunk c of S is compacted to its ids with m > 0, in ascending
+// id order, as (x, y, m, id bits) at live[4 (4096 c + k)], count at cnt[c].
+// A chunk's partial sum over its live bodies adds the same non-zero terms in
+// the same order as the sum over all its ids (an empty id has m = 0 and adds
+// exactly 0), so results do not change.
+__device__ __forceinline__ float4* live_s(const dsr_nbody_args& a) { return reinterpret_cast<float4*>(a.live); }
+__device__ __forceinline__ uint32_t* live_n(const dsr_nbody_args& a) {
+  return reinterpret_cast<uint32_t*>(a.live + 4ull * a.n_total);
+}
+constexpr int kLiveThreads = kChunk / 4;
+__global__ void __launch_bounds__(kLiveThreads) k_nb_live(dsr_nbody_args a) {
+  __shared__ uint32_t s_w[kLiveThreads / 32];
+  const uint32_t base = blockIdx.x * kChunk, end = min(base + kChunk, a.n_total);
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  float4 v[4];
+  uint32_t bits = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {                     // ids base + 4 t .. base + 4 t + 3, in order
+    const uint32_t id = base + 4u * threadIdx.x + k;
+    v[k] = id < end ? s4(a, id) : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (v[k].z > 0.f) bits |= 1u << k;
+  }
+  const uint32_t cnt = __popc(bits);
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += t;
+  }
+  if (lane == 31) s_w[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t x = s_w[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (uint32_t)o) x += t;
+    }
+    s_w[lane] = x;                                   // inclusive warp totals
+  }
+  __syncthreads();
+  uint32_t off = (wid ? s_w[wid - 1] : 0u) + incl - cnt;
+  float4* out = live_s(a) + base;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if ((bits >> k) & 1u) out[off++] = make_float4(v[k].x, v[k].y, v[k].z, __uint_as_float(base + 4u * threadIdx.x + k));
+  if (threadIdx.x == 0) live_n(a)[blockIdx.x] = s_w[kLiveThreads / 32 - 1];
+}
+// the i side of a CTA: live-list chunk ic = id_lo / 4096 + blockIdx.x / kIBlocksPerChunk,
+// positions (blockIdx.x % kIBlocksPerChunk) * kIBlock + threadIdx.x + 128 m
+struct PairI {
+  uint32_t ic, pos0, n;
+  __device__ PairI(const dsr_nbody_args& a)
+      : ic(a.id_lo / kChunk + blockIdx.x / kIBlocksPerChunk),
+        pos0((blockIdx.x % kIBlocksPerChunk) * kIBlock + threadIdx.x),
+        n(live_n(a)[a.id_lo / kChunk + blockIdx.x / kIBlocksPerChunk]) {}
+  // body m (0 .. 2 kNbPairs - 1) of this thread; id = 0xFFFFFFFF if none (or not mine)
+  __device__ __forceinline__ float4 body(const dsr_nbody_args& a, int m, uint32_t& id) const {
+    const uint32_t pos = pos0 + 128u * m;
+    id = 0xFFFFFFFFu;
+    if (pos >= n) return make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 p = __ldg(live_s(a) + (size_t)ic * kChunk + pos);
+    const uint32_t i = __float_as_uint(p.w);
+    if (i < a.id_lo || i >= a.id_hi) return make_float4(0.f, 0.f, 0.f, 0.f);
+    id = i;
+    return p;
+  }
+  __device__ __forceinline__ bool empty() const { return pos0 - threadIdx.x >= n; }   // CTA-uniform
+};
 
 __global__ void __launch_bounds__(kPairThreads) k_nb_force_part(dsr_nbody_args a) {
   __shared__ float4 tile[256];
-  const uint32_t n = a.n_total, nl = a.id_hi - a.id_lo;
-  const uint32_t ib = a.id_lo + blockIdx.x * kIBlock + threadIdx.x;
+  const uint32_t nl = a.id_hi - a.id_lo;
+  const PairI I(a);
+  if (I.empty()) return;                             // no body of this i-block exists
   const float eps2 = a.eps * a.eps;
   const f32x2 E2 = pk2(eps2, eps2);
   f32x2 PX[kNbPairs], PY[kNbPairs], AX[kNbPairs], AY[kNbPairs];
+  uint32_t ID[2 * kNbPairs];
 #pragma unroll
   for (int q = 0; q < kNbPairs; ++q) {
-    const uint32_t i0 = ib + 256u * q, i1 = i0 + 128u;
-    const float4 p0 = i0 < a.id_hi ? s4(a, i0) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 p1 = i1 < a.id_hi ? s4(a, i1) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 p0 = I.body(a, 2 * q, ID[2 * q]), p1 = I.body(a, 2 * q + 1, ID[2 * q + 1]);
     PX[q] = pk2(p0.x, p1.x);
     PY[q] = pk2(p0.y, p1.y);
     AX[q] = pk2(0.f, 0.f);
     AY[q] = pk2(0.f, 0.f);
   }
-  const uint32_t jb = blockIdx.y * kChunk, je = min(jb + kChunk, n);
-  for (uint32_t j0 = jb; j0 < je; j0 += 256) {
+  const uint32_t jc = blockIdx.y, nj = live_n(a)[jc];
+  const float4* J = live_s(a) + (size_t)jc * kChunk;
+  for (uint32_t j0 = 0; j0 < nj; j0 += 256) {
     __syncthreads();
-    const uint32_t ja = j0 + threadIdx.x, jc = ja + 128;
-    tile[threadIdx.x] = ja < je ? s4(a, ja) : make_float4(0.f, 0.f, 0.f, 0.f);
-    tile[threadIdx.x + 128] = jc < je ? s4(a, jc) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const uint32_t ja = j0 + threadIdx.x, jb = ja + 128;
+    tile[threadIdx.x] = ja < nj ? __ldg(J + ja) : make_float4(0.f, 0.f, 0.f, 0.f);   // padding: m = 0
+    tile[threadIdx.x + 128] = jb < nj ? __ldg(J + jb) : make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
 #pragma unroll 8
     for (int k = 0; k < 256; ++k) {
-      const float4 p = tile[k];                      // out-of-range entries have m = 0
+      const float4 p = tile[k];                      // padding entries have m = 0: they add exactly 0
       const f32x2 JX = pk2(p.x, p.x), JY = pk2(p.y, p.y), JM = pk2(p.z, p.z);
 #pragma unroll
       for (int q = 0; q < kNbPairs; ++q) {
@@ -155,12 +230,11 @@ __global__ void __launch_bounds__(kPairThreads) k_nb_force_part(dsr_nbody_args a
   float2* part = reinterpret_cast<float2*>(a.scratch) + (size_t)blockIdx.y * nl;
 #pragma unroll
   for (int q = 0; q < kNbPairs; ++q) {
-    const uint32_t i0 = ib + 256u * q, i1 = i0 + 128u;
     float ax0, ax1, ay0, ay1;
     upk2(AX[q], ax0, ax1);
     upk2(AY[q], ay0, ay1);
-    if (i0 < a.id_hi) part[i0 - a.id_lo] = make_float2(ax0, ay0);
-    if (i1 < a.id_hi) part[i1 - a.id_lo] = make_float2(ax1, ay1);
+    if (ID[2 * q] != 0xFFFFFFFFu) part[ID[2 * q] - a.id_lo] = make_float2(ax0, ay0);
+    if (ID[2 * q + 1] != 0xFFFFFFFFu) part[ID[2 * q + 1] - a.id_lo] = make_float2(ax1, ay1);
   }
 }
 
@@ -212,50 +286,45 @@ struct NbMove {   // semi-implicit Euler, velocity first
 };
 
 // prepare_merge partials: per (i, chunk) the best (d2, j) with (m_j, j) >lex (m_i, i), d2 < R^2
-// Merge search: for each body the nearest heavier (m, id) body within R.
-// The common path of a tile entry is the packed distance and a running min;
-// only a group of kMergeGroup entries that has some distance below the
-// thread's largest current bound is re-examined with the exact per-body test
-// (in ascending j, so ties resolve as in a sequential scan).
+// Merge search: for each body the nearest heavier (m, id) body within R, over
+// the live list (an empty id is never a candidate: the exact test wants
+// m_j > 0).  The common path of a tile entry is the packed distance and a
+// running min; only a group of kMergeGroup entries that has some distance
+// below the thread's largest current bound is re-examined with the exact
+// per-body test (in ascending j, so ties resolve as in a sequential scan).
 constexpr int kMergeGroup = 4;
 __global__ void __launch_bounds__(kPairThreads) k_nb_merge_part(dsr_nbody_args a) {
   __shared__ float4 tile[256];
-  const uint32_t n = a.n_total, nl = a.id_hi - a.id_lo;
-  const uint32_t ib = a.id_lo + blockIdx.x * kIBlock + threadIdx.x;
+  const uint32_t nl = a.id_hi - a.id_lo;
+  const PairI I(a);
+  if (I.empty()) return;
   const float R2 = a.R * a.R;
   f32x2 PX[kNbPairs], PY[kNbPairs];
   float M[2 * kNbPairs], D[2 * kNbPairs];
-  uint32_t B[2 * kNbPairs];
+  uint32_t B[2 * kNbPairs], ID[2 * kNbPairs];
 #pragma unroll
   for (int q = 0; q < kNbPairs; ++q) {
-    const uint32_t i0 = ib + 256u * q, i1 = i0 + 128u;
-    const float4 p0 = i0 < a.id_hi ? s4(a, i0) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 p1 = i1 < a.id_hi ? s4(a, i1) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 p0 = I.body(a, 2 * q, ID[2 * q]), p1 = I.body(a, 2 * q + 1, ID[2 * q + 1]);
     PX[q] = pk2(p0.x, p1.x);
     PY[q] = pk2(p0.y, p1.y);
     M[2 * q] = p0.z;
     M[2 * q + 1] = p1.z;
-    // strict d2 < R^2, ties -> smaller j (j ascends).  An empty id (m = 0: no
-    // body, or one deleted by a merge; its snapshot entry is zero) searches
-    // nothing -- k_nb_merge_pick skips it -- so its bound is -1
-    D[2 * q] = p0.z > 0.f ? R2 : -1.f;
-    D[2 * q + 1] = p1.z > 0.f ? R2 : -1.f;
+    // strict d2 < R^2, ties -> smaller j (j ascends); no body: bound -1 (searches nothing)
+    D[2 * q] = ID[2 * q] != 0xFFFFFFFFu ? R2 : -1.f;
+    D[2 * q + 1] = ID[2 * q + 1] != 0xFFFFFFFFu ? R2 : -1.f;
     B[2 * q] = B[2 * q + 1] = kNone;
   }
   float dmax = D[0];                                 // max of the D[] (they only decrease)
 #pragma unroll
   for (int m = 1; m < 2 * kNbPairs; ++m) dmax = fmaxf(dmax, D[m]);
-  const uint32_t jb = blockIdx.y * kChunk, je = min(jb + kChunk, n);
-  for (uint32_t j0 = jb; j0 < je; j0 += 256) {
+  const uint32_t jc = blockIdx.y, nj = live_n(a)[jc];
+  const float4* J = live_s(a) + (size_t)jc * kChunk;
+  for (uint32_t j0 = 0; j0 < nj; j0 += 256) {
     __syncthreads();
-    const uint32_t ja = j0 + threadIdx.x, jc = ja + 128;
-    // empty ids (m = 0, at the origin in the snapshot) can never be a merge
-    // target (the exact test wants m_j > 0): they are staged far away, so they
-    // never make a group take the exact path
-    const float4 fa = ja < je ? s4(a, ja) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 fc = jc < je ? s4(a, jc) : make_float4(0.f, 0.f, 0.f, 0.f);
-    tile[threadIdx.x] = fa.z > 0.f ? fa : make_float4(1e18f, 1e18f, 0.f, 0.f);
-    tile[threadIdx.x + 128] = fc.z > 0.f ? fc : make_float4(1e18f, 1e18f, 0.f, 0.f);
+    const uint32_t ja = j0 + threadIdx.x, jb = ja + 128;
+    // padding beyond the chunk's live bodies: far away, m = 0 (never a candidate)
+    tile[threadIdx.x] = ja < nj ? __ldg(J + ja) : make_float4(1e18f, 1e18f, 0.f, 0.f);
+    tile[threadIdx.x + 128] = jb < nj ? __ldg(J + jb) : make_float4(1e18f, 1e18f, 0.f, 0.f);
     __syncthreads();
 #pragma unroll 2
     for (int k0 = 0; k0 < 256; k0 += kMergeGroup) {
@@ -279,14 +348,14 @@ __global__ void __launch_bounds__(kPairThreads) k_nb_merge_part(dsr_nbody_args a
 #pragma unroll
         for (int g = 0; g < kMergeGroup; ++g) {
           const float4 p = tile[k0 + g];
-          const uint32_t j = j0 + k0 + g;
+          const uint32_t j = __float_as_uint(p.w);
 #pragma unroll
           for (int q = 0; q < kNbPairs; ++q) {
             float e[2];
             upk2(E[g][q], e[0], e[1]);
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
-              const uint32_t i = ib + 256u * q + 128u * u;
+              const uint32_t i = ID[2 * q + u];
               const float mi = M[2 * q + u];
               if (e[u] < D[2 * q + u] && p.z > 0.f && (p.z > mi || (p.z == mi && j > i))) {
                 D[2 * q + u] = e[u];
@@ -303,10 +372,8 @@ __global__ void __launch_bounds__(kPairThreads) k_nb_merge_part(dsr_nbody_args a
   }
   uint2* part = reinterpret_cast<uint2*>(a.scratch) + (size_t)blockIdx.y * nl;
 #pragma unroll
-  for (int m = 0; m < 2 * kNbPairs; ++m) {
-    const uint32_t i = ib + 128u * m;
-    if (i < a.id_hi) part[i - a.id_lo] = make_uint2(__float_as_uint(D[m]), B[m]);
-  }
+  for (int m = 0; m < 2 * kNbPairs; ++m)
+    if (ID[m] != 0xFFFFFFFFu) part[ID[m] - a.id_lo] = make_uint2(__float_as_uint(D[m]), B[m]);
 }
 
 __global__ void k_nb_merge_pick(DevHeap h, dsr_nbody_args a) {
@@ -397,8 +464,12 @@ bool nb_method_info(uint32_t id, MethodInfo* mi) {
   return false;
 }
 
+// x: the i-blocks of the live-list chunks that hold my ids; y: the j chunks
 static dim3 pair_grid(const dsr_nbody_args& a) {
-  return dim3((a.id_hi - a.id_lo + kIBlock - 1) / kIBlock, (a.n_total + kChunk - 1) / kChunk);
+  return dim3(((a.id_hi - 1) / kChunk - a.id_lo / kChunk + 1) * kIBlocksPerChunk, (a.n_total + kChunk - 1) / kChunk);
+}
+static void launch_live(const dsr_nbody_args& a, cudaStream_t st) {
+  k_nb_live<<<(a.n_total + kChunk - 1) / kChunk, kLiveThreads, 0, st>>>(a);
 }
 
 bool nb_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot, const void* args) {
@@ -406,17 +477,19 @@ bool nb_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot,
   switch (id) {
     case DSR_M_NB_SNAPSHOT: launch_doall<NbSnapshot>(c, T, snapshot, args); return true;
     case DSR_M_NB_FORCE:
-      if (a.id_hi <= a.id_lo) return true;
+      if (a.id_hi <= a.id_lo || !a.live) return a.id_hi <= a.id_lo;
+      launch_live(a, c.st);
       k_nb_force_part<<<pair_grid(a), kPairThreads, 0, c.st>>>(a);
       k_nb_force_sum<<<grid_for(c, a.id_hi - a.id_lo, k_nb_force_sum), 256, 0, c.st>>>(c.h, a);
-      count_launch(2);
+      count_launch(3);
       return true;
     case DSR_M_NB_MOVE: launch_doall<NbMove>(c, T, snapshot, args); return true;
     case DSR_M_NB_PREPARE_MERGE:
-      if (a.id_hi <= a.id_lo) return true;
+      if (a.id_hi <= a.id_lo || !a.live) return a.id_hi <= a.id_lo;
+      launch_live(a, c.st);
       k_nb_merge_part<<<pair_grid(a), kPairThreads, 0, c.st>>>(a);
       k_nb_merge_pick<<<grid_for(c, a.id_hi - a.id_lo, k_nb_merge_pick), 256, 0, c.st>>>(c.h, a);
-      count_launch(2);
+      count_launch(3);
       return true;
     case DSR_M_NB_CLAIM: launch_doall<NbClaim>(c, T, snapshot, args); return true;
     case DSR_M_NB_ABSORB: launch_doall<NbAbsorb>(c, T, snapshot, args); return true;
@@ -522,7 +595,8 @@ __global__ void k_nbs_delete(dsr_nbody_args a) {
 
 extern "C" dsr_status dsr_nbody_static_step(const dsr_nbody_static_args* sa, uint32_t steps, void* stream) {
   using namespace dsr;
-  if (!sa || !sa->S || !sa->V || !sa->target || !sa->incoming || !sa->scratch || sa->n == 0) return DSR_ERR_INVALID;
+  if (!sa || !sa->S || !sa->V || !sa->target || !sa->incoming || !sa->scratch || !sa->live || sa->n == 0)
+    return DSR_ERR_INVALID;
   cudaStream_t st = (cudaStream_t)stream;
   dsr_nbody_args a;
   memset(&a, 0, sizeof(a));
@@ -531,6 +605,7 @@ extern "C" dsr_status dsr_nbody_static_step(const dsr_nbody_static_args* sa, uin
   a.target = sa->target;
   a.incoming = sa->incoming;
   a.scratch = sa->scratch;
+  a.live = sa->live;
   a.G = sa->G; a.dt = sa->dt; a.eps = sa->eps; a.R = sa->R;
   a.n_total = sa->n;
   a.id_lo = 0;
@@ -540,17 +615,19 @@ extern "C" dsr_status dsr_nbody_static_step(const dsr_nbody_static_args* sa, uin
     return DSR_ERR_CUDA;
   const int g = (int)std::min<uint64_t>((sa->n + 255) / 256, (uint64_t)sms * 8);
   for (uint32_t k = 0; k < steps; ++k) {
+    launch_live(a, st);
     k_nb_force_part<<<pair_grid(a), kPairThreads, 0, st>>>(a);           // compute_force over S0
     k_nbs_force_move<<<g, 256, 0, st>>>(a);                             // + move: S becomes S1
     if (sa->merges) {
+      launch_live(a, st);
       k_nb_merge_part<<<pair_grid(a), kPairThreads, 0, st>>>(a);        // prepare_merge over S1
       k_nbs_merge_pick<<<g, 256, 0, st>>>(a);
       k_nb_claim_all<<<g, 256, 0, st>>>(a.n_total, a);
       k_nbs_absorb<<<g, 256, 0, st>>>(a);
       k_nbs_delete<<<g, 256, 0, st>>>(a);
-      count_launch(5);
+      count_launch(6);
     }
-    count_launch(2);
+    count_launch(3);
   }
   return cudaGetLastError() == cudaSuccess ? DSR_OK : DSR_ERR_CUDA;
 }

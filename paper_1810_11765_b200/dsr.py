@@ -143,7 +143,7 @@ class WatorArgs(C.Structure):
 class NbodyStaticArgs(C.Structure):
     _fields_ = [("S", C.c_void_p), ("V", C.c_void_p), ("target", C.c_void_p), ("incoming", C.c_void_p),
                 ("scratch", C.c_void_p), ("G", C.c_float), ("dt", C.c_float), ("eps", C.c_float), ("R", C.c_float),
-                ("n", C.c_uint32), ("merges", C.c_uint32)]
+                ("n", C.c_uint32), ("merges", C.c_uint32), ("live", C.c_void_p)]
 
 
 class GolStaticArgs(C.Structure):
@@ -162,7 +162,7 @@ class NbodyArgs(C.Structure):
                 ("x0", C.c_void_p), ("y0", C.c_void_p), ("vx0", C.c_void_p), ("vy0", C.c_void_p),
                 ("m0", C.c_void_p), ("G", C.c_float), ("dt", C.c_float), ("eps", C.c_float), ("R", C.c_float),
                 ("n_total", C.c_uint32), ("id_lo", C.c_uint32), ("id_hi", C.c_uint32), ("out", C.c_void_p),
-                ("scratch", C.c_void_p)]
+                ("scratch", C.c_void_p), ("live", C.c_void_p)]
 
 
 class DsrError(RuntimeError):

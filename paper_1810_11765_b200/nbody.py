@@ -72,12 +72,13 @@ class NBody:
         self.out = torch.zeros(N, 6, dtype=torch.float32, device=dev)
         chunks = (N + 4095) // 4096
         self.scratch = torch.zeros(2 * chunks * n, dtype=torch.float32, device=dev)
+        self.live = torch.zeros(4 * N + chunks, dtype=torch.float32, device=dev)   # all-pairs live list (dsr.h)
         i = self.init
         self.args = dsr.NbodyArgs(self.S.data_ptr(), self.V.data_ptr(), self.target.data_ptr(),
                                   self.incoming.data_ptr(), self.shandle.data_ptr(),
                                   i["x"].data_ptr(), i["y"].data_ptr(), i["vx"].data_ptr(), i["vy"].data_ptr(),
                                   i["m"].data_ptr(), G, dt, eps, R, N, self.lo, self.hi, self.out.data_ptr(),
-                                  self.scratch.data_ptr())
+                                  self.scratch.data_ptr(), self.live.data_ptr())
         self.heap.parallel_new(0, n, dsr.C_NB_BODY, self.args, stream)
 
     # ---- one step as a sequence of local phases ("p") and exchange points ("x")
@@ -162,9 +163,10 @@ class NBodyStatic:
         self.target = torch.full((n,), -1, dtype=torch.int32, device=dev)
         self.incoming = torch.full((n,), -1, dtype=torch.int32, device=dev)
         self.scratch = torch.zeros(2 * ((n + 4095) // 4096) * n, dtype=torch.float32, device=dev)
+        self.live = torch.zeros(4 * n + (n + 4095) // 4096, dtype=torch.float32, device=dev)
         self.args = dsr.NbodyStaticArgs(self.S.data_ptr(), self.V.data_ptr(), self.target.data_ptr(),
                                         self.incoming.data_ptr(), self.scratch.data_ptr(), G, dt, eps, R, n,
-                                        1 if merges else 0)
+                                        1 if merges else 0, self.live.data_ptr())
 
     def run(self, steps, stream=None):
         s = stream if stream is not None else self.stream
