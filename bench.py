@@ -934,8 +934,10 @@ def run_app(args):
         visits = 8 * int(lv[:, 0].sum())
         visits, = reduce_over_ranks([float(visits)], "sum")
         ms, = reduce_over_ranks([ms], "max")
-        cfg = {"workload": "nbody with merging (BASELINE configs[2]) 65536 bodies", "pairs_per_step": 2 * 65536 ** 2,
-               "pair_interactions_per_s": 2 * 65536 ** 2 / (ms * 1e-3),
+        tot_live = reduce_over_ranks([float(v) for v in lv[:, 0]], "sum")     # bodies in existence per step
+        pairs = 2 * float(np.mean(np.square(tot_live)))                       # force + merge pass pairs
+        cfg = {"workload": "nbody with merging (BASELINE configs[2]) 65536 bodies", "pairs_per_step": pairs,
+               "pair_interactions_per_s": pairs / (ms * 1e-3),
                "parallelism": f"{world} id-range shards, NCCL all-gather of snapshot chunks" if world > 1 else "1 GPU"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
