@@ -127,13 +127,10 @@ __device__ __forceinline__ void mb_construct(const DevHeap& h, uint32_t T, const
     // below it (no per-object n-th-bit search)
     const uint32_t lo = ctz64(cm);
     const uint64_t run = cm >> lo;
-    if ((run & (run + 1ull)) == 0) {
-      for (uint32_t j = lane; j < cn; j += 32) construct(lo + j, c0 + j);
-    } else {
-#pragma unroll
-      for (uint32_t p = lane; p < 64; p += 32)
-        if ((cm >> p) & 1ull) construct(p, c0 + (uint32_t)__popcll(cm & ((1ull << p) - 1ull)));
-    }
+    const bool single = (run & (run + 1ull)) == 0;       // warp-uniform
+    // one copy of the constructor in the code (the kernel's instruction
+    // footprint showed as no-instruction stalls)
+    for (uint32_t j = lane; j < cn; j += 32) construct(single ? lo + j : nth_bit(cm, j), c0 + j);
   }
 }
 
