@@ -21,9 +21,10 @@ for bulk in (True, False):
     ok.append(("microbench bulk" if bulk else "microbench per-thread",
                np.array_equal(mb.results(), O.microbench(3, 20_000, 10_000)[0]) and mb.heap.check_invariants() == 0))
 a0 = I.gol_soup(64, 64, 0.3, 1)
-g = GameOfLife(a0, heap_bytes=16 << 20)
-g.run(10)
-ok.append(("gol 64", np.array_equal(g.alive(), O.life_dense(a0, 10))))
+for tiled in (False, "prepare", "all"):  # GoL
+    g = GameOfLife(a0, heap_bytes=16 << 20, tiled=tiled)
+    g.run(10)
+    ok.append((f"gol 64 tiled={tiled}", np.array_equal(g.alive(), O.life_dense(a0, 10))))
 k, e, n = I.wator_init(64, 64, seed=21)
 w = WaTor(k, e, n, FB=6, SB=12, SS=6, seed=42, heap_bytes=16 << 20)
 w.run(10)
@@ -36,6 +37,10 @@ nb.run(3)
 got = nb.state()
 want = O.nbody_run(st, merges=True, steps=3, **prm)
 ok.append(("nbody 1000", np.array_equal(got["alive"], want["alive"])))
+from paper_1810_11765_b200.nbody import NBodyStatic
+nbs = NBodyStatic(st, merges=True, **prm)
+nbs.run(3)
+ok.append(("nbody 1000 static", np.array_equal(nbs.state()["alive"], want["alive"])))
 for name, v in ok:
     print(f"{name}: {'ok' if v else 'MISMATCH'}")
 print("ALL OK" if all(v for _, v in ok) else "FAILED")
