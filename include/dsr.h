@@ -445,10 +445,7 @@ enum {
   DSR_K_WT_HALO_OCC_APPLY = 27,  /* occ in -> ghost cells' agent kinds */
   DSR_M_WT_CELL_PREPARE = 20, DSR_M_WT_FISH_PREPARE = 21, DSR_M_WT_CELL_DECIDE_FISH = 22,
   DSR_M_WT_FISH_UPDATE = 23, DSR_M_WT_SHARK_PREPARE = 24, DSR_M_WT_CELL_DECIDE_SHARK = 25,
-  DSR_M_WT_SHARK_UPDATE = 26, DSR_M_WT_DUMP = 27,
-  /* Fish.prepare / Shark.prepare as cell-tiled do-alls (reading R-TILED): the agents enumerated
-   * through the cell grid, neighbours' Cells and agents staged in shared memory; same results */
-  DSR_M_WT_FISH_PREPARE_TILED = 28, DSR_M_WT_SHARK_PREPARE_TILED = 29
+  DSR_M_WT_SHARK_UPDATE = 26, DSR_M_WT_DUMP = 27
 };
 
 /* ---- N-body with collisions (BASELINE configs[2], reading R-NBODY) ----

@@ -210,51 +210,23 @@ struct WtCellDecideQ {
   }
 };
 
-// Fish.prepare / Shark.prepare of the agent in slot s of block b at cell c.
-// nbagent(d): the agent handle in neighbour d (N, E, S, W); req(d): set the
-// request byte of the cell the agent asks to move into (d < 4: neighbour d,
-// whose byte d ^ 2 records where the request comes from; d = 4: own cell,
-// "stays").  Shared by the block-list do-alls and the cell-tiled ones.
-template <class NbAgent, class Req>
-__device__ __forceinline__ void wt_fish_prepare(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s,
-                                                const dsr_wator_args& a, uint32_t c, NbAgent nbagent, Req req) {
-  *field_ptr<uint32_t>(h, T, 2, b, s) += 1;
-  *field_ptr<uint32_t>(h, T, 1, b, s) = c;
-  uint32_t fr[4], nf = 0;
-#pragma unroll
-  for (uint32_t d = 0; d < 4; ++d)
-    if (nbagent(d) == 0) fr[nf++] = d;
-  if (nf) req(wt_pick(fr, nf, rng_key(a.seed, wt_step(a), PH_FISH_REQ, wt_gid(a, c))));
-  else req(4);
-}
-template <class NbAgent, class Req>
-__device__ __forceinline__ void wt_shark_prepare(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s,
-                                                 const dsr_wator_args& a, uint32_t c, NbAgent nbagent, Req req) {
-  *field_ptr<uint32_t>(h, T, 2, b, s) += 1;
-  uint32_t* en = field_ptr<uint32_t>(h, T, 3, b, s);
-  *en -= 1;
-  *field_ptr<uint32_t>(h, T, 1, b, s) = c;
-  if (*en == 0) return;                                           // starves in Shark.update
-  uint32_t fd[4], nfd = 0, fr[4], nfr = 0;
-#pragma unroll
-  for (uint32_t d = 0; d < 4; ++d) {
-    const uint64_t ag = nbagent(d);
-    if (ag == 0) fr[nfr++] = d;
-    else if (h_is(ag, WT_FISH)) fd[nfd++] = d;
-  }
-  const uint64_t key = rng_key(a.seed, wt_step(a), PH_SHARK_REQ, wt_gid(a, c));
-  if (nfd) req(wt_pick(fd, nfd, key));
-  else if (nfr) req(wt_pick(fr, nfr, key));
-  else req(4);
-}
-
 struct WtFishPrepare {
   typedef dsr_wator_args Args;
   DSR_NO_ACC
   static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args& a, Acc&) {
     const uint32_t c = *field_ptr<uint32_t>(h, T, 0, b, s);
-    wt_fish_prepare(h, T, b, s, a, c, [&](uint32_t d) { return *wt_agent(h, a, wt_nbr(a, c, d)); },
-                    [&](uint32_t d) { *(d == 4 ? wt_req(h, a, c, 4) : wt_req(h, a, wt_nbr(a, c, d), d ^ 2)) = 1; });
+    *field_ptr<uint32_t>(h, T, 2, b, s) += 1;
+    *field_ptr<uint32_t>(h, T, 1, b, s) = c;
+    uint32_t fr[4], nf = 0;
+#pragma unroll
+    for (uint32_t d = 0; d < 4; ++d)
+      if (*wt_agent(h, a, wt_nbr(a, c, d)) == 0) fr[nf++] = d;
+    if (nf) {
+      const uint32_t d = wt_pick(fr, nf, rng_key(a.seed, wt_step(a), PH_FISH_REQ, wt_gid(a, c)));
+      *wt_req(h, a, wt_nbr(a, c, d), d ^ 2) = 1;
+    } else {
+      *wt_req(h, a, c, 4) = 1;
+    }
   }
 };
 
@@ -288,69 +260,30 @@ struct WtSharkPrepare {
   DSR_NO_ACC
   static __device__ __forceinline__ void run(const DevHeap& h, uint32_t T, uint32_t b, uint32_t s, const Args& a, Acc&) {
     const uint32_t c = *field_ptr<uint32_t>(h, T, 0, b, s);
-    wt_shark_prepare(h, T, b, s, a, c, [&](uint32_t d) { return *wt_agent(h, a, wt_nbr(a, c, d)); },
-                     [&](uint32_t d) { *(d == 4 ? wt_req(h, a, c, 4) : wt_req(h, a, wt_nbr(a, c, d), d ^ 2)) = 1; });
+    *field_ptr<uint32_t>(h, T, 2, b, s) += 1;
+    uint32_t* en = field_ptr<uint32_t>(h, T, 3, b, s);
+    *en -= 1;
+    *field_ptr<uint32_t>(h, T, 1, b, s) = c;
+    if (*en == 0) return;                                           // starves in Shark.update
+    uint32_t fd[4], nfd = 0, fr[4], nfr = 0;
+#pragma unroll
+    for (uint32_t d = 0; d < 4; ++d) {
+      const uint64_t ag = *wt_agent(h, a, wt_nbr(a, c, d));
+      if (ag == 0) fr[nfr++] = d;
+      else if (h_is(ag, WT_FISH)) fd[nfd++] = d;
+    }
+    const uint64_t key = rng_key(a.seed, wt_step(a), PH_SHARK_REQ, wt_gid(a, c));
+    if (nfd) {
+      const uint32_t d = wt_pick(fd, nfd, key);
+      *wt_req(h, a, wt_nbr(a, c, d), d ^ 2) = 1;
+    } else if (nfr) {
+      const uint32_t d = wt_pick(fr, nfr, key);
+      *wt_req(h, a, wt_nbr(a, c, d), d ^ 2) = 1;
+    } else {
+      *wt_req(h, a, c, 4) = 1;
+    }
   }
 };
-
-// Cell-tiled Fish.prepare / Shark.prepare (reading R-TILED, as GoL's): every
-// agent sits in exactly one cell, so visiting the cells whose agent has the
-// pass's type visits every agent of that type exactly once.  A CTA stages an
-// (8 + 2) x (128 + 2) tile of the Cell handles and of their agents in shared
-// memory (coalesced: cells[] row segments, and the Cells were created in id
-// order), then runs the same prepare logic with the neighbours' agents and
-// Cells from the tile: the four neighbour lookups of an agent (two dependent
-// scattered loads each in the block-list do-all) become shared-memory reads.
-constexpr int kWtTileH = 8, kWtTileW = 128;
-template <int TT>
-__global__ void __launch_bounds__(256) k_wt_tile_prepare(DevHeap h, dsr_wator_args a) {
-  __shared__ unsigned long long s_cell[kWtTileH + 2][kWtTileW + 2];
-  __shared__ unsigned long long s_ag[kWtTileH + 2][kWtTileW + 2];
-  const uint32_t W = a.W, H = a.H;
-  const uint32_t rows_total = a.ghost ? H + 2 : H;
-  const uint32_t tx = (W + kWtTileW - 1) / kWtTileW, ty = (H + kWtTileH - 1) / kWtTileH;
-  const uint32_t nt = tx * ty, t0 = (uint32_t)((uint64_t)blockIdx.x * nt / gridDim.x),
-                 t1 = (uint32_t)((uint64_t)(blockIdx.x + 1) * nt / gridDim.x);
-  for (uint32_t tile = t0; tile < t1; ++tile) {                             // blocked: neighbouring tiles per CTA
-    const uint32_t y0 = (tile / tx) * kWtTileH, x0 = (tile % tx) * kWtTileW;   // local cell coordinates
-    __syncthreads();                                                        // the previous tile is consumed
-    for (uint32_t i = threadIdx.x; i < (kWtTileH + 2) * (kWtTileW + 2); i += blockDim.x) {
-      const int r = (int)(i / (kWtTileW + 2)), cc = (int)(i % (kWtTileW + 2));
-      const int yy = (int)y0 + r - 1, xx = (int)x0 + cc - 1;               // local row -1 .. H + 8
-      const int gy = a.ghost ? yy + 1 : ((yy % (int)H) + (int)H) % (int)H; // grid row (ghost rows 0, H + 1)
-      const uint32_t gx = (uint32_t)(((xx % (int)W) + (int)W) % (int)W);
-      unsigned long long hc = 0, ag = 0;
-      if (gy >= 0 && gy < (int)rows_total) {
-        hc = __ldg((const unsigned long long*)a.cells + (size_t)gy * W + gx);
-        ag = ld_relaxed(field_ptr<uint64_t>(h, hc, 1));
-      }
-      s_cell[r][cc] = hc;
-      s_ag[r][cc] = ag;
-    }
-    __syncthreads();
-    for (uint32_t idx = threadIdx.x; idx < kWtTileH * kWtTileW; idx += blockDim.x) {
-      const uint32_t r = idx / kWtTileW, cc = idx % kWtTileW, y = y0 + r, x = x0 + cc;
-      if (y >= H || x >= W) continue;
-      const uint64_t hd = s_ag[r + 1][cc + 1];
-      if (!h_is(hd, TT)) continue;
-      const uint32_t c = (y + (a.ghost ? 1u : 0u)) * W + x;                // cell id (grid row)
-      // neighbour d in {N, E, S, W} = tile offsets (-1, 0), (0, +1), (+1, 0), (0, -1)
-      auto nb = [&](uint32_t d) -> uint32_t {
-        return d == 0 ? (r + 0) * (kWtTileW + 2) + cc + 1 : d == 1 ? (r + 1) * (kWtTileW + 2) + cc + 2
-             : d == 2 ? (r + 2) * (kWtTileW + 2) + cc + 1 : (r + 1) * (kWtTileW + 2) + cc;
-      };
-      const unsigned long long* sag = &s_ag[0][0];
-      const unsigned long long* scl = &s_cell[0][0];
-      auto nbagent = [&](uint32_t d) { return (uint64_t)sag[nb(d)]; };
-      auto req = [&](uint32_t d) {
-        const uint64_t cell = d == 4 ? scl[(r + 1) * (kWtTileW + 2) + cc + 1] : scl[nb(d)];
-        *field_ptr<uint8_t>(h, cell, 2 + (d == 4 ? 4u : (d ^ 2u))) = 1;
-      };
-      if (TT == WT_FISH) wt_fish_prepare(h, TT, h_bid(hd), h_slot(hd), a, c, nbagent, req);
-      else wt_shark_prepare(h, TT, h_bid(hd), h_slot(hd), a, c, nbagent, req);
-    }
-  }
-}
 
 struct WtSharkUpdate {  // allocates Shark (snapshot pass); destroys Fish and itself
   typedef dsr_wator_args Args;
@@ -481,8 +414,6 @@ bool wt_method_info(uint32_t id, MethodInfo* mi) {
     case DSR_M_WT_CELL_PREPARE: case DSR_M_WT_FISH_PREPARE: case DSR_M_WT_CELL_DECIDE_FISH:
     case DSR_M_WT_SHARK_PREPARE: case DSR_M_WT_CELL_DECIDE_SHARK: case DSR_M_WT_DUMP:
       *mi = {0, sizeof(dsr_wator_args)}; return true;
-    case DSR_M_WT_FISH_PREPARE_TILED: case DSR_M_WT_SHARK_PREPARE_TILED:
-      *mi = {4, sizeof(dsr_wator_args)}; return true;      // enumerated through the cell grid: no block list
     case DSR_M_WT_FISH_UPDATE: case DSR_M_WT_SHARK_UPDATE:
       *mi = {1, sizeof(dsr_wator_args)}; return true;
   }
@@ -496,15 +427,6 @@ bool wt_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot,
       else launch_doall_quad<WtCellPrepareQ>(c, T, snapshot, args);
       return true;
     case DSR_M_WT_FISH_PREPARE: launch_doall<WtFishPrepare>(c, T, snapshot, args); return true;
-    case DSR_M_WT_FISH_PREPARE_TILED: case DSR_M_WT_SHARK_PREPARE_TILED: {
-      const dsr_wator_args a = *(const dsr_wator_args*)args;
-      const bool fish = id == DSR_M_WT_FISH_PREPARE_TILED;
-      if (T != (fish ? (uint32_t)WT_FISH : (uint32_t)WT_SHARK) || c.rk >= 0 || a.W < 1 || a.H < 1) return false;
-      if (fish) k_wt_tile_prepare<WT_FISH><<<persistent_grid(c, k_wt_tile_prepare<WT_FISH>), 256, 0, c.st>>>(c.h, a);
-      else k_wt_tile_prepare<WT_SHARK><<<persistent_grid(c, k_wt_tile_prepare<WT_SHARK>), 256, 0, c.st>>>(c.h, a);
-      count_launch();
-      return true;
-    }
     case DSR_M_WT_CELL_DECIDE_FISH:
       if (c.h.flags & DSR_F_SCALAR_DOALL) launch_doall<WtCellDecide<PH_FISH_DEC>>(c, T, snapshot, args);
       else launch_doall_quad<WtCellDecideQ<PH_FISH_DEC>>(c, T, snapshot, args);

@@ -47,7 +47,6 @@ def wt_halo_layout(W: int) -> dict:
             "mig": (mig_out, mig_out + 24 * W, 12 * W), "bytes": mig_out + 48 * W}
 (M_WT_CELL_PREPARE, M_WT_FISH_PREPARE, M_WT_CELL_DECIDE_FISH, M_WT_FISH_UPDATE, M_WT_SHARK_PREPARE,
  M_WT_CELL_DECIDE_SHARK, M_WT_SHARK_UPDATE, M_WT_DUMP) = range(20, 28)
-M_WT_FISH_PREPARE_TILED, M_WT_SHARK_PREPARE_TILED = 28, 29
 C_NB_BODY, K_NB_CLEAR_SNAPSHOT, K_NB_CLAIM = 30, 30, 31
 (M_NB_SNAPSHOT, M_NB_FORCE, M_NB_MOVE, M_NB_PREPARE_MERGE, M_NB_CLAIM, M_NB_ABSORB, M_NB_DELETE_MERGED,
  M_NB_DUMP) = range(30, 38)

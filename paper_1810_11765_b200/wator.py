@@ -25,12 +25,11 @@ class WaTor:
     result bit for bit."""
 
     def __init__(self, kind, egg, energy, FB=6, SB=12, SS=6, seed=42, heap_bytes=None, device=None,
-                 stream=None, retries=5, flags=0, step0=0, shard=None, exchange=None, tiled=False):
+                 stream=None, retries=5, flags=0, step0=0, shard=None, exchange=None):
         import numpy as np
         import torch
         Hg, W = kind.shape
         self.shard, self.exchange, self.Hg = shard, exchange, Hg
-        self.tiled = tiled          # Fish/Shark.prepare as cell-tiled do-alls (DSR_M_WT_*_PREPARE_TILED)
         if shard is not None:
             r, P = shard
             y0, y1 = row_range(Hg, P, r)
@@ -91,10 +90,7 @@ class WaTor:
         out = []
         for T, dec, upd in ((FISH, dsr.M_WT_CELL_DECIDE_FISH, dsr.M_WT_FISH_UPDATE),
                             (SHARK, dsr.M_WT_CELL_DECIDE_SHARK, dsr.M_WT_SHARK_UPDATE)):
-            if self.tiled:
-                prep = dsr.M_WT_FISH_PREPARE_TILED if T == FISH else dsr.M_WT_SHARK_PREPARE_TILED
-            else:
-                prep = dsr.M_WT_FISH_PREPARE if T == FISH else dsr.M_WT_SHARK_PREPARE
+            prep = dsr.M_WT_FISH_PREPARE if T == FISH else dsr.M_WT_SHARK_PREPARE
             first = [begin] if T == FISH else []
             last = [end] if T == SHARK else []
             if not sh:

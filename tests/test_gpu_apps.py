@@ -21,14 +21,11 @@ def P():
 WT = dict(FB=6, SB=12, SS=6, seed=42)
 
 
-@pytest.mark.parametrize("tiled", [False, True])
-@pytest.mark.parametrize("W,H,seed", [(64, 64, 5), (48, 32, 9), (200, 120, 3), (130, 17, 4)])
-def test_wator_every_step_bit_exact(P, O, W, H, seed, tiled):
-    """tiled: Fish/Shark.prepare as cell-tiled do-alls (R-TILED; ragged tiles
-    at 200 x 120 and 130 x 17)."""
+@pytest.mark.parametrize("W,H,seed", [(64, 64, 5), (48, 32, 9), (200, 120, 3)])
+def test_wator_every_step_bit_exact(P, O, W, H, seed):
     from paper_1810_11765_b200 import inputs as I, wator
     kind, egg, en = I.wator_init(W, H, seed=seed)
-    sim = wator.WaTor(kind, egg, en, tiled=tiled, **WT)
+    sim = wator.WaTor(kind, egg, en, **WT)
     k, e, n = kind, egg, en
     prev = [0, 0, 0, 0]
     for s in range(60):
@@ -60,12 +57,11 @@ def test_wator_cuda_graph_replay(P, O):
     assert sim.heap.check_invariants() == 0
 
 
-@pytest.mark.parametrize("tiled", [False, True])
-def test_wator_2048_prefix_against_oracle(P, O, tiled):
+def test_wator_2048_prefix_against_oracle(P, O):
     """BASELINE configs[1] grid (2048^2, seed 42) for 10 steps."""
     from paper_1810_11765_b200 import inputs as I, wator
     kind, egg, en = I.wator_init(2048, 2048, seed=42)
-    sim = wator.WaTor(kind, egg, en, tiled=tiled, **WT)
+    sim = wator.WaTor(kind, egg, en, **WT)
     sim.run(10)
     gk, ge, gn = sim.state()
     k, e, n, c = O.wator_run(kind, egg, en, steps=10, **WT)
@@ -73,18 +69,16 @@ def test_wator_2048_prefix_against_oracle(P, O, tiled):
     assert sim.heap.check_invariants() == 0
 
 
-@pytest.mark.parametrize("Pn,W,H,seed,steps,tiled", [(1, 64, 64, 5, 40, False), (2, 64, 64, 5, 40, False),
-                                                      (4, 48, 32, 9, 40, False), (8, 64, 64, 11, 30, False),
-                                                      (2, 200, 120, 3, 25, False), (4, 200, 120, 3, 25, True),
-                                                      (8, 64, 64, 11, 30, True)])
-def test_wator_row_shards_loopback_bit_exact(P, O, Pn, W, H, seed, steps, tiled):
+@pytest.mark.parametrize("Pn,W,H,seed,steps", [(1, 64, 64, 5, 40), (2, 64, 64, 5, 40), (4, 48, 32, 9, 40),
+                                                (8, 64, 64, 11, 30), (2, 200, 120, 3, 25)])
+def test_wator_row_shards_loopback_bit_exact(P, O, Pn, W, H, seed, steps):
     """Row-band sharding (ghost rows, 4 boundary exchanges per half step,
     agents migrating between heaps) equals the single-heap oracle every step,
     including the event counters summed over shards.  Pn = 8 at H = 64 gives
     8-row bands, so agents cross several bands over the run."""
     from paper_1810_11765_b200 import inputs as I, wator
     kind, egg, en = I.wator_init(W, H, seed=seed)
-    lb = wator.WaTorLoopback(kind, egg, en, Pn, tiled=tiled, **WT)
+    lb = wator.WaTorLoopback(kind, egg, en, Pn, **WT)
     k, e, n = kind, egg, en
     tot = np.zeros(4, dtype=np.int64)
     for s in range(steps):

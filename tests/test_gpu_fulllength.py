@@ -68,15 +68,14 @@ def digest(x, dtype):
     return hashlib.sha256(np.ascontiguousarray(x, dtype=np.dtype(dtype).newbyteorder("<")).tobytes()).hexdigest()
 
 
-@pytest.mark.parametrize("tiled", [False, True])
-def test_wator_2048_500_steps_golden(P, tiled):
+def test_wator_2048_500_steps_golden(P):
     from paper_1810_11765_b200 import inputs as I, wator
     g0 = np.load(GOLDEN / "wator2048_500steps.npz")
     assert list(g0["meta"]) == [2048, 2048, 42, 500, 6, 12, 6]
     c = g0["counters"]
     WT = dict(FB=6, SB=12, SS=6, seed=42)
     kind, egg, en = I.wator_init(2048, 2048, seed=42)
-    sim = wator.WaTor(kind, egg, en, tiled=tiled, **WT)
+    sim = wator.WaTor(kind, egg, en, **WT)
     prev = [0, 0, 0, 0]
     for s in range(500):
         sim.step()
