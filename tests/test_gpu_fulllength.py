@@ -15,8 +15,9 @@ scripts/make_nbody_golden.py, which call only oracle/):
   at step 10 (BASELINE's tolerance point), then mass conservation (<= 1e-5
   relative, BASELINE) and momentum conservation at step 1000.
 
-With DSR_FULL=1 the GoL variants (bit mirror, cell-tiled passes) run the same
-windows, and the Wa-Tor run is also checked against the oracle recomputed live
+The GoL run is checked for the block-list passes and for the bench's variant
+(tiled prepare passes); with DSR_FULL=1 the other GoL variants (bit mirror,
+all passes tiled) run the same windows, and the Wa-Tor run is also checked against the oracle recomputed live
 (minutes of CPU) and against the static baseline.
 """
 import hashlib
@@ -42,7 +43,7 @@ def P():
     return pkg
 
 
-@pytest.mark.parametrize("variant", ["handles", pytest.param("bits", marks=FULL), pytest.param("tiled", marks=FULL),
+@pytest.mark.parametrize("variant", ["handles", "tiled", pytest.param("bits", marks=FULL),
                                      pytest.param("tiled_all", marks=FULL)])
 def test_gol_16384_1000_generations_windows(P, variant):
     from paper_1810_11765_b200 import inputs as I
