@@ -261,6 +261,18 @@ dsr_status dsr_device_view(const dsr_heap* h, void* out, size_t out_bytes);
  *   mode 1  every thread on word 0 (same-address serialisation)
  * *ops_out (host) receives the number of atomics issued; time the call with
  * events on `stream`.  DSR_ERR_INVALID if bytes < 8 or iters == 0. */
+/* CUDA IPC for the peer-memory exchanges: export the device
+ * allocation that contains dev_ptr as a 64-byte handle (handle_out, host) and
+ * dev_ptr's byte offset in it (*offset_out, host; caching allocators such as
+ * torch's hand out pieces of larger blocks), open another process's handle
+ * into this one (*dev_ptr_out: the block's base, usable by kernels on the
+ * current device -- over NVLink when the memory lives on a peer GPU; add the
+ * offset), and close it.  DSR_ERR_CUDA when the driver refuses (e.g. no P2P
+ * path between the GPUs). */
+dsr_status dsr_ipc_handle(void* dev_ptr, void* handle_out, uint64_t* offset_out);
+dsr_status dsr_ipc_open(const void* handle, void** dev_ptr_out);
+dsr_status dsr_ipc_close(void* dev_ptr);
+
 dsr_status dsr_probe_atomics(void* dev_buf, uint64_t bytes, uint32_t mode, uint32_t iters, uint64_t* ops_out,
                              void* stream);
 
@@ -368,13 +380,32 @@ typedef struct {
    * the prepare passes then count neighbours from it instead of loading 8
    * handles (SURVEY D4 "state-grid mirror" design knob). */
   uint32_t* bits;
+  /* Peer-memory halo exchange ("fused pack + send"; peer_up =
+   * NULL: off).  peer_up / peer_down: the halo buffers of the shards above and
+   * below, mapped into this process (dsr_ipc_open over NVLink / NVSwitch when
+   * they live on other GPUs; plain device pointers when they are other shards
+   * on this GPU; my own buffer when P = 1).  halo is then
+   * DSR_GOL_PEER_HALO_BYTES(W) bytes: received masks double-buffered by the
+   * parity of `gen` -- segment 2 + 2 (gen & 1) from the shard above, 3 + 2 (gen & 1)
+   * from the shard below -- and at DSR_GOL_PEER_FLAGS(W) two u32 flags (from
+   * above, from below) that the neighbours set to gen + 1 (system-scope
+   * release) after writing generation gen's masks.  gen: the generation. */
+  uint8_t* peer_up;
+  uint8_t* peer_down;
+  uint32_t gen;
 } dsr_gol_args;
+#define DSR_GOL_PEER_FLAGS(W) ((6u * (W) + 15u) & ~15u)
+#define DSR_GOL_PEER_HALO_BYTES(W) (DSR_GOL_PEER_FLAGS(W) + 16u)
 enum {
   DSR_K_GOL_INIT_ALIVE = 10,     /* n = W*H (W*(H+2) sharded); Alive(c) for alive0[c] (+ ghost cells) */
   DSR_K_GOL_INIT_CAND = 11,      /* n as above; Candidate(c) for dead c with >= 1 alive neighbour */
   DSR_K_GOL_HALO_PACK = 12,      /* n = W: after pass 3, masks of the boundary rows into halo[0], halo[1] */
   DSR_K_GOL_HALO_APPLY = 13,     /* n = W: before pass 4, ghost rows from halo[2], halo[3]; Candidates on
-                                    empty boundary cells next to a remote new Alive (owner computes) */
+                                    empty boundary cells next to a remote new Alive (owner computes).
+                                    Peer mode: waits until both flags reach gen + 1, reads the gen-parity slots */
+  DSR_K_GOL_HALO_PUSH = 14,      /* n = W, peer mode only: after pass 3, the masks of my row 1 / row H written
+                                    straight into the halo buffers of the shards above / below (one kernel,
+                                    no staging, no collective), then their flags := gen + 1 */
   DSR_M_GOL_CAND_PREPARE = 10,   /* type 1 */
   DSR_M_GOL_ALIVE_PREPARE = 11,  /* type 0 */
   DSR_M_GOL_CAND_UPDATE = 12,    /* type 1 (allocates Alive) */

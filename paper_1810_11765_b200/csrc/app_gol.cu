@@ -8,6 +8,7 @@
 // In pass 4 a new Alive creates a Candidate on every empty neighbour exactly
 // once: the creator claims the empty cell with atomicCAS(0 -> RESERVED), so
 // the created set is the same for every visit order.
+#include <cuda.h>   // cuStreamWaitValue32 (types only: resolved at run time, no libcuda link dependency)
 #include "dsr_host.h"
 
 namespace dsr {
@@ -225,19 +226,67 @@ __global__ void k_gol_halo_pack(DevHeap h, uint64_t n, dsr_gol_args a) {
     a.halo[a.W + x] = gol_mask(h, a.cell[(uint64_t)a.H * a.W + x]);
   }
 }
+// Peer-memory exchange (fused pack + send): after pass 3, one CTA computes
+// the masks of my row 1 and row H and stores them straight into the halo
+// buffers of the shards above / below (their segment "from below" / "from
+// above" of this generation's parity), then -- all stores issued, fenced at
+// system scope -- sets their flags to gen + 1 with a system-scope release.
+// Over NVLink the stores are the transfer; there is no staging copy and no
+// collective call.
+__device__ __forceinline__ void st_release_sys_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__global__ void __launch_bounds__(1024) k_gol_halo_push(DevHeap h, dsr_gol_args a) {
+  const uint32_t W = a.W, par = a.gen & 1u;
+  uint8_t* const to_up = a.peer_up + (size_t)(3u + 2u * par) * W;       // the upper shard's "from below"
+  uint8_t* const to_down = a.peer_down + (size_t)(2u + 2u * par) * W;   // the lower shard's "from above"
+  for (uint32_t x = threadIdx.x; x < W; x += blockDim.x) {
+    to_up[x] = gol_mask(h, a.cell[(uint64_t)1 * W + x]);
+    to_down[x] = gol_mask(h, a.cell[(uint64_t)a.H * W + x]);
+  }
+  __threadfence_system();                                              // every thread's stores, system scope,
+  __syncthreads();                                                     // before the flags
+  if (threadIdx.x == 0) {
+    st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer_up + DSR_GOL_PEER_FLAGS(W)) + 1, a.gen + 1u);
+    st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer_down + DSR_GOL_PEER_FLAGS(W)), a.gen + 1u);
+  }
+}
+
 // before pass 4: ghost rows := the neighbours' next-alive cells (read by the
 // next generation's prepare passes), and a Candidate on every empty boundary
 // cell next to a remote new Alive (the owner computes it; the CAS claim makes
 // it exactly once together with pass 4's local claims)
 __global__ void __launch_bounds__(256) k_gol_halo_apply(DevHeap h, uint64_t n, dsr_gol_args a) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t in0 = 2, in1 = 3;                                           // received segments (pack + collective)
+  if (a.peer_up) {
+    // peer mode: the launching stream waited (cuStreamWaitValue32) until both
+    // neighbours' flags reached gen + 1; the acquire loads order this kernel's
+    // reads of their masks after those flags (they pass at once)
+    if (threadIdx.x == 0) {
+      const uint32_t* f = reinterpret_cast<const uint32_t*>(a.halo + DSR_GOL_PEER_FLAGS(a.W));
+      uint32_t ns = 64;
+      while (ld_acquire_sys_u32(f) < a.gen + 1u || ld_acquire_sys_u32(f + 1) < a.gen + 1u) {
+        __nanosleep(ns);
+        ns = ns < 1024 ? ns * 2 : 1024;
+      }
+    }
+    __syncthreads();
+    in0 = 2u + 2u * (a.gen & 1u);
+    in1 = 3u + 2u * (a.gen & 1u);
+  }
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < 2 * n; base += stride) {   // uniform trip count
     const uint64_t i = base + threadIdx.x;
     bool want = false;
     uint32_t e = 0;
     if (i < 2 * n) {
       const uint32_t side = (uint32_t)(i / n), x = (uint32_t)(i % n);
-      const uint8_t* m = a.halo + (2 + side) * a.W;                    // received masks
+      const uint8_t* m = a.halo + (size_t)(side ? in1 : in0) * a.W;   // received masks
       const uint32_t grow = side ? a.H + 1 : 0, brow = side ? a.H : 1;   // ghost row, my boundary row
       a.cell[(uint64_t)grow * a.W + x] = (m[x] & 1) ? ghost_alive(h) : 0ull;
       if (a.bits) gol_bit_set(a, grow * a.W + x, m[x] & 1);
@@ -433,12 +482,41 @@ bool gol_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot
 bool gol_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* args, size_t bytes, int* ok) {
   *ok = 1;
   if (id != DSR_K_GOL_INIT_ALIVE && id != DSR_K_GOL_INIT_CAND && id != DSR_K_GOL_HALO_PACK &&
-      id != DSR_K_GOL_HALO_APPLY)
+      id != DSR_K_GOL_HALO_APPLY && id != DSR_K_GOL_HALO_PUSH)
     return false;
   if (bytes != sizeof(dsr_gol_args) || c.h.ntypes < 2) { *ok = 0; return true; }
   const dsr_gol_args a = *(const dsr_gol_args*)args;
+  if (id == DSR_K_GOL_HALO_PUSH) {
+    if (!a.ghost || !a.halo || !a.peer_up || !a.peer_down || n != a.W) { *ok = 0; return true; }
+    k_gol_halo_push<<<1, 1024, 0, c.st>>>(c.h, a);
+    count_launch();
+    return true;
+  }
   if (id == DSR_K_GOL_HALO_PACK || id == DSR_K_GOL_HALO_APPLY) {
     if (!a.ghost || !a.halo || n != a.W) { *ok = 0; return true; }
+    if (id == DSR_K_GOL_HALO_APPLY && a.peer_up) {
+      // the wait for the neighbours' pushes is a stream-level wait on the flags
+      // (front end, no SM held): their kernels -- on other GPUs, or other
+      // processes time-sharing this one -- run meanwhile
+      typedef CUresult (*WaitFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+      static WaitFn wait = nullptr;
+      if (!wait) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn) {
+          *ok = 0;
+          return true;
+        }
+        wait = (WaitFn)fn;
+      }
+      const CUdeviceptr f = (CUdeviceptr)(a.halo + DSR_GOL_PEER_FLAGS(a.W));
+      if (wait((CUstream)c.st, f, a.gen + 1u, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS ||
+          wait((CUstream)c.st, f + 4, a.gen + 1u, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
+        *ok = 0;
+        return true;
+      }
+    }
     if (id == DSR_K_GOL_HALO_PACK) k_gol_halo_pack<<<grid_for(c, n, k_gol_halo_pack), 256, 0, c.st>>>(c.h, n, a);
     else k_gol_halo_apply<<<grid_for(c, 2 * n, k_gol_halo_apply), 256, 0, c.st>>>(c.h, n, a);
     count_launch();

@@ -2,6 +2,7 @@
 // lifecycle, do-all orchestration, audit / statistics kernels.
 #include <cstdio>
 #include <cstring>
+#include <cuda.h>   // driver types for entry points resolved at run time (no libcuda link dependency)
 #include <new>
 #include "dsr_host.h"
 #include "dsr_doall.cuh"
@@ -847,6 +848,42 @@ static __global__ void __launch_bounds__(256) k_probe_atom(unsigned long long* b
     acc += atomicOr(buf + w, 1ull << (t & 63));                 // RMW with return (ATOMG)
   }
   if (acc == 0x5EED5EED5EED5EEDull) *sink = acc;                 // keeps the results live
+}
+
+extern "C" dsr_status dsr_ipc_handle(void* dev_ptr, void* handle_out, uint64_t* offset_out) {
+  if (!dev_ptr || !handle_out || !offset_out) return DSR_ERR_INVALID;
+  // the handle names the whole cudaMalloc block (a caching allocator such as
+  // torch's hands out pieces of larger blocks): report dev_ptr's offset in it
+  typedef CUresult (*RangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static RangeFn range = nullptr;
+  if (!range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return DSR_ERR_CUDA;
+    range = (RangeFn)fn;
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (CUdeviceptr)dev_ptr) != CUDA_SUCCESS) return DSR_ERR_CUDA;
+  cudaIpcMemHandle_t hd;
+  if (cudaIpcGetMemHandle(&hd, (void*)base) != cudaSuccess) return DSR_ERR_CUDA;
+  static_assert(sizeof(hd) == 64, "CUDA IPC handles are 64 bytes");
+  memcpy(handle_out, &hd, sizeof(hd));
+  *offset_out = (uint64_t)((CUdeviceptr)dev_ptr - base);
+  return DSR_OK;
+}
+extern "C" dsr_status dsr_ipc_open(const void* handle, void** dev_ptr_out) {
+  if (!handle || !dev_ptr_out) return DSR_ERR_INVALID;
+  cudaIpcMemHandle_t hd;
+  memcpy(&hd, handle, sizeof(hd));
+  if (cudaIpcOpenMemHandle(dev_ptr_out, hd, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return DSR_ERR_CUDA;
+  return DSR_OK;
+}
+extern "C" dsr_status dsr_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return DSR_ERR_INVALID;
+  return cudaIpcCloseMemHandle(dev_ptr) == cudaSuccess ? DSR_OK : DSR_ERR_CUDA;
 }
 
 extern "C" dsr_status dsr_probe_atomics(void* dev_buf, uint64_t bytes, uint32_t mode, uint32_t iters,

@@ -32,7 +32,16 @@ K_MB_NEW_BULK = 8
 K_LS_ALLOC, K_LS_FREE = 2, 3
 K_REPLAY, K_TORTURE, M_COLLECT = 4, 5, 4
 K_INH_NEW, K_INH_READ, M_INH_BUMP, M_INH_SUM, M_INH_SPAWN = 6, 7, 5, 6, 7
-K_GOL_INIT_ALIVE, K_GOL_INIT_CAND, K_GOL_HALO_PACK, K_GOL_HALO_APPLY = 10, 11, 12, 13
+K_GOL_INIT_ALIVE, K_GOL_INIT_CAND, K_GOL_HALO_PACK, K_GOL_HALO_APPLY, K_GOL_HALO_PUSH = 10, 11, 12, 13, 14
+
+
+def gol_peer_flags(W: int) -> int:
+    """Byte offset of the two u32 flags in a peer-mode GoL halo (dsr.h DSR_GOL_PEER_FLAGS)."""
+    return (6 * W + 15) & ~15
+
+
+def gol_peer_halo_bytes(W: int) -> int:
+    return gol_peer_flags(W) + 16
 M_GOL_CAND_PREPARE, M_GOL_ALIVE_PREPARE, M_GOL_CAND_UPDATE, M_GOL_ALIVE_UPDATE, M_GOL_DUMP = 10, 11, 12, 13, 14
 M_GOL_CAND_PREPARE_TILED, M_GOL_ALIVE_PREPARE_TILED, M_GOL_CAND_UPDATE_TILED, M_GOL_ALIVE_UPDATE_TILED = 15, 16, 17, 18
 C_WT_CELL, K_WT_INIT_AGENTS = 20, 21
@@ -128,7 +137,8 @@ class CollectArgs(C.Structure):
 
 class GolArgs(C.Structure):
     _fields_ = [("cell", C.c_void_p), ("W", C.c_uint32), ("H", C.c_uint32), ("alive0", C.c_void_p),
-                ("dump", C.c_void_p), ("ghost", C.c_uint32), ("halo", C.c_void_p), ("bits", C.c_void_p)]
+                ("dump", C.c_void_p), ("ghost", C.c_uint32), ("halo", C.c_void_p), ("bits", C.c_void_p),
+                ("peer_up", C.c_void_p), ("peer_down", C.c_void_p), ("gen", C.c_uint32)]
 
 
 class WatorArgs(C.Structure):
@@ -200,6 +210,12 @@ def lib():
         if hasattr(L, "dsr_probe_atomics"):       # (absent in older builds loaded via DSR_LIBPATH for A/B runs)
             L.dsr_probe_atomics.restype = st
             L.dsr_probe_atomics.argtypes = [vp, C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64), vp]
+        L.dsr_ipc_handle.restype = st
+        L.dsr_ipc_handle.argtypes = [vp, vp, C.POINTER(C.c_uint64)]
+        L.dsr_ipc_open.restype = st
+        L.dsr_ipc_open.argtypes = [vp, C.POINTER(vp)]
+        L.dsr_ipc_close.restype = st
+        L.dsr_ipc_close.argtypes = [vp]
         L.dsr_wator_static_step.restype = st
         L.dsr_wator_static_step.argtypes = [C.POINTER(WatorStaticArgs), C.c_uint32, vp]
         L.dsr_nbody_static_step.restype = st
@@ -462,6 +478,26 @@ def probe_atomics(buf, mode=0, iters=64, stream=None) -> int:
                                                        mode, iters, C.byref(n), _stream_ptr(stream)))
     return n.value
 
+
+
+def ipc_handle(tensor):
+    """(64-byte CUDA IPC handle of the allocation holding a torch CUDA tensor,
+    the tensor's byte offset in it) -- dsr_ipc_handle."""
+    buf = C.create_string_buffer(64)
+    off = C.c_uint64(0)
+    check("dsr_ipc_handle", lib().dsr_ipc_handle(C.c_void_p(tensor.data_ptr()), buf, C.byref(off)))
+    return buf.raw, off.value
+
+
+def ipc_open(handle: bytes) -> int:
+    """Device pointer of (the base of) another process's allocation (dsr_ipc_open)."""
+    p = C.c_void_p()
+    check("dsr_ipc_open", lib().dsr_ipc_open(C.create_string_buffer(bytes(handle), 64), C.byref(p)))
+    return p.value
+
+
+def ipc_close(ptr: int) -> None:
+    check("dsr_ipc_close", lib().dsr_ipc_close(C.c_void_p(ptr)))
 
 
 # ---------------------------------------------------------------- stream helpers for the host-side halo copies

@@ -26,7 +26,7 @@ class GameOfLife:
     single-heap result bit for bit."""
 
     def __init__(self, alive0, heap_bytes=None, device=None, stream=None, retries=5, flags=0, shard=None,
-                 exchange=None, bit_mirror=False, tiled=False):
+                 exchange=None, bit_mirror=False, tiled=False, peer=False):
         """tiled: True / "prepare" -- the two prepare passes (the neighbour
         gathers) as cell-tiled do-alls (DSR_M_GOL_*_PREPARE_TILED: objects
         enumerated through the cell grid, neighbour handles staged in shared
@@ -68,6 +68,13 @@ class GameOfLife:
         self.args = dsr.GolArgs(self.cell.data_ptr(), W, H, self.alive0.data_ptr(), self.dumpbuf.data_ptr(),
                                 1 if shard is not None else 0, self.halo.data_ptr() if shard is not None else None,
                                 self.bits.data_ptr() if bit_mirror else None)
+        # peer: the halo is exchanged through peer memory (DSR_K_GOL_HALO_PUSH writes my boundary masks
+        # straight into the neighbours' halo buffers, dsr.h "Peer-memory halo exchange"); connect() sets
+        # the neighbours' buffers before the first generation
+        self.peer = bool(peer) and shard is not None
+        if self.peer:
+            self.halo = torch.zeros(dsr.gol_peer_halo_bytes(W), dtype=torch.uint8, device=dev)
+            self.args.halo = self.halo.data_ptr()
         if tiled and bit_mirror:
             raise ValueError("tiled passes read the handle grid; the bit mirror is the other variant")
         if tiled == "all":
@@ -82,13 +89,21 @@ class GameOfLife:
         self.heap.launch(dsr.K_GOL_INIT_CAND, self.N, self.args, stream)
         self.gen = 0
 
+    def connect(self, peer_up: int, peer_down: int):
+        """Peer mode: device pointers of the halo buffers of the shards above
+        and below (another shard's `halo` on this GPU, or an IPC-mapped one)."""
+        self.args.peer_up, self.args.peer_down = peer_up, peer_down
+
     # the generation split at the exchange point (sharded mode)
     def first_half(self, s):
         h, a = self.heap, self.args
         h.parallel_do(CAND, self.m[0], a, s)
         h.parallel_do(ALIVE, self.m[1], a, s)
         h.parallel_do(CAND, self.m[2], a, s)
-        if self.shard is not None:
+        if self.peer:
+            a.gen = self.gen
+            h.launch(dsr.K_GOL_HALO_PUSH, self.W, a, s)
+        elif self.shard is not None:
             h.launch(dsr.K_GOL_HALO_PACK, self.W, a, s)
 
     def second_half(self, s):
@@ -101,7 +116,7 @@ class GameOfLife:
     def generation(self, stream=None):
         s = stream if stream is not None else self.stream
         self.first_half(s)
-        if self.shard is not None:
+        if self.shard is not None and not self.peer:
             with dsr.on_stream(s):                  # the copies / NCCL calls in order with the kernels on s
                 (self.exchange or self.self_exchange)()
         self.second_half(s)
@@ -122,6 +137,9 @@ class GameOfLife:
         replay it with run_graph().  Small grids are launch-bound, so this
         removes ~14 launches of host overhead per generation."""
         import torch
+        if self.peer:
+            raise ValueError("peer-mode generations carry their generation number in the launch arguments "
+                             "(the flags' target); they are not graph-replayable")
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         self.graph = torch.cuda.CUDAGraph()
@@ -217,6 +235,41 @@ class NcclHaloExchange:
             r.wait()
 
 
+class PeerHalo:
+    """Multi-process peer mode: every rank exports its halo buffer as a CUDA IPC
+    handle, the handles are all-gathered over torch.distributed (any backend),
+    and each rank maps its two neighbours' buffers (over NVLink / NVSwitch when
+    they are on other GPUs) into its kernel arguments.  After that no host
+    exchange happens: DSR_K_GOL_HALO_PUSH writes into the neighbours' memory and
+    DSR_K_GOL_HALO_APPLY waits on the flags they set."""
+
+    def __init__(self, sim, group=None):
+        import torch.distributed as dist
+        assert sim.peer, "GameOfLife(..., peer=True)"
+        self.sim = sim
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        handles = [None] * world
+        dist.all_gather_object(handles, dsr.ipc_handle(sim.halo), group=group)
+        up, down = (rank - 1) % world, (rank + 1) % world
+        self.opened = []
+
+        def ptr(r):
+            if r == rank:
+                return sim.halo.data_ptr()
+            hd, off = handles[r]
+            p = dsr.ipc_open(hd)
+            self.opened.append(p)
+            return p + off
+        mapped = {r: ptr(r) for r in {up, down}}
+        sim.connect(mapped[up], mapped[down])
+        dist.barrier(group)                         # every rank mapped its neighbours before the first push
+
+    def close(self):
+        for p in self.opened:
+            dsr.ipc_close(p)
+        self.opened = []
+
+
 class GameOfLifeLoopback:
     """P row-band shards on ONE GPU (P heaps): the same kernels and exchange
     points as the multi-GPU run, the messages replaced by device copies."""
@@ -224,10 +277,22 @@ class GameOfLifeLoopback:
     def __init__(self, alive0, P, **kw):
         self.P = P
         self.shards = [GameOfLife(alive0, shard=(r, P), **kw) for r in range(P)]
+        if self.shards[0].peer:                     # peer mode: each shard pushes into its neighbours' halos
+            for r, s in enumerate(self.shards):
+                s.connect(self.shards[(r - 1) % P].halo.data_ptr(), self.shards[(r + 1) % P].halo.data_ptr())
 
     def generation(self):
         for s in self.shards:
             s.first_half(s.stream)
+        if self.shards[0].peer:
+            # the pushes of every shard precede every apply in stream order (one
+            # stream per shard would need the events below; the apply kernels wait
+            # on the flags anyway)
+            with dsr.StreamJoin([s.stream for s in self.shards]):
+                pass
+            for s in self.shards:
+                s.second_half(s.stream)
+            return
         W = self.shards[0].W
         with dsr.StreamJoin([s.stream for s in self.shards]):
             for r, s in enumerate(self.shards):

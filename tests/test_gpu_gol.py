@@ -114,6 +114,47 @@ def test_gol_row_shards_loopback_equal_dense(G, O, P, W, H, gens):
         assert s.heap.check_invariants() == 0
 
 
+@pytest.mark.parametrize("P,W,H,gens,tiled", [(1, 64, 64, 60, False), (2, 64, 64, 60, False),
+                                              (3, 96, 48, 70, False), (4, 200, 64, 40, "prepare")])
+def test_gol_peer_memory_exchange_equal_dense(G, O, P, W, H, gens, tiled):
+    """The peer-memory halo exchange (DSR_K_GOL_HALO_PUSH stores each shard's
+    boundary masks straight into its neighbours' halo buffers and sets their
+    flags; DSR_K_GOL_HALO_APPLY waits on its own flags and reads the
+    generation-parity slot): P heaps on one GPU exchanging through each
+    other's device memory, no host copies, give dense Life every generation
+    (P = 1: a shard is its own neighbour across the torus seam)."""
+    from paper_1810_11765_b200 import inputs as I
+    from paper_1810_11765_b200.gol import GameOfLifeLoopback
+    a0 = I.gol_soup(W, H, 0.3, P + 40)
+    lb = GameOfLifeLoopback(a0, P, peer=True, tiled=tiled)
+    a = a0
+    for g in range(gens):
+        lb.generation()
+        a = O.life_dense(a, 1)
+        if g % 10 == 9 or g == gens - 1:
+            assert np.array_equal(lb.alive(), a), g
+    for s in lb.shards:
+        assert s.heap.check_invariants() == 0
+
+
+def test_gol_peer_memory_exchange_two_processes(G, O):
+    """Two processes (one shard each) map each other's halo buffers through
+    CUDA IPC (handles all-gathered over gloo) and exchange only through that
+    memory -- the multi-GPU path, here with both processes on one GPU."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(29000 + os.getpid() % 1000),
+           str(root / "tests" / "peer_worker.py")]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=str(root))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "PEER OK" in r.stdout, r.stdout[-3000:]
+
+
 def test_gol_glider_crosses_shard_boundaries(G, O):
     from paper_1810_11765_b200 import inputs as I
     from paper_1810_11765_b200.gol import GameOfLifeLoopback
