@@ -49,6 +49,9 @@ def parse():
                                                                      "gol16k-tiled", "nbody"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-apps", action="store_true", help="skip the per-app block of the default line")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
+                    help="GoL row bands under torchrun: NCCL P2P of the boundary masks, or the peer-memory push "
+                         "(DSR_K_GOL_HALO_PUSH into the neighbours' IPC-mapped halo buffers)")
     ap.add_argument("--launch-list", action="store_true",
                     help="run only W + K microbench steps (for ncu launch lists) and print no bench line")
     ap.add_argument("--dry-run", action="store_true",
@@ -893,14 +896,19 @@ def run_app(args):
         from paper_1810_11765_b200.gol import GameOfLife, NcclHaloExchange
         Wd = 64 if args.workload == "gol" else 16384
         a0 = I.gol_soup(Wd, Wd, 0.3 if Wd == 64 else 0.25, 1 if Wd == 64 else 42)
-        if world > 1:                      # row bands + NCCL exchange of boundary masks
+        if world > 1:                      # row bands + an exchange of boundary masks
+            peer = args.exchange == "peer"
             sim = GameOfLife(a0, stream=stream, shard=(rank, world), bit_mirror=args.workload.endswith("bits"),
-                             tiled=args.workload.endswith("tiled"))
-            sim.exchange = NcclHaloExchange(sim)
+                             tiled=args.workload.endswith("tiled") and "prepare", peer=peer)
+            if peer:                       # the neighbours' halo buffers mapped over NVLink (CUDA IPC)
+                from paper_1810_11765_b200.gol import PeerHalo
+                sim.peer_halo = PeerHalo(sim)
+            else:
+                sim.exchange = NcclHaloExchange(sim)
             dist.barrier()
         else:
             sim = GameOfLife(a0, stream=stream, bit_mirror=args.workload.endswith("bits"),
-                             tiled=args.workload.endswith("tiled"))
+                             tiled=args.workload.endswith("tiled") and "prepare")
         step_fn = sim.generation
         if Wd == 64:                       # launch-bound: replay one generation as a CUDA graph
             sim.capture()
@@ -917,7 +925,9 @@ def run_app(args):
         cfg = {"workload": f"gol {Wd}^2 torus (BASELINE configs[{0 if Wd == 64 else 3}])"
                            + (", alive-bit mirror variant" if args.workload.endswith("bits") else "")
                            + (", cell-tiled prepare passes" if args.workload.endswith("tiled") else ""),
-               "parallelism": f"{world} row bands, NCCL P2P halo masks" if world > 1 else "1 GPU"}
+               "parallelism": (f"{world} row bands, " + ("peer-memory push of the halo masks over NVLink"
+                                                          if args.exchange == "peer" else "NCCL P2P halo masks"))
+               if world > 1 else "1 GPU"}
     else:
         from paper_1810_11765_b200.nbody import NBody
         st = I.nbody_init(65536, seed=7)
