@@ -8,3 +8,4 @@ grep '^{' gpurun_out/bench_ref.log | tail -1 > $P/bench_reference.json
 cp gpurun_out/pytest_gpu.log $P/pytest_gpu.log
 cp gpurun_out/smoke.log $P/smoke.log
 cp gpurun_out/build_info.txt $P/ncu_build_info.txt
+cp gpurun_out/fulllength.log $P/fulllength.log 2>/dev/null || true

@@ -17,3 +17,6 @@ python scripts/refresh_profiles.py ${R} gpurun_out/prof_${R} > gpurun_out/refres
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout -s KILL 1800 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=15 > gpurun_out/pytest_gpu.log 2>&1
 echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
+# the extra full-length variants (bit mirror, all-tiled GoL; Wa-Tor against the live oracle and the static baseline)
+DSR_FULL=1 timeout -s KILL 1500 python -m pytest tests/test_gpu_fulllength.py -q -p no:cacheprovider --durations=10 -s > gpurun_out/fulllength.log 2>&1
+echo "pytest exit $?" >> gpurun_out/fulllength.log
