@@ -500,6 +500,29 @@ typedef struct {
   float* live;                        /* the all-pairs passes' live list (device, caller-owned, scratch):
                                          >= 4 * n_total + ceil(n_total/4096) floats; each 4096-id chunk of S
                                          compacted to its bodies with m > 0 (x, y, m, id bits), ascending id */
+  /* Peer-memory all-gathers (npeers = 0: off, the caller
+   * all-gathers S, V and target itself).  The snapshot pass writes each of
+   * this rank's bodies into S / V here AND into every peer's S / V (the
+   * peers' buffers of the same epoch parity, mapped into this process:
+   * dsr_ipc_open over NVLink, or other shards' buffers on this GPU), and
+   * DSR_K_NB_CLEAR_SNAPSHOT clears this rank's rows in all of them; after
+   * the snapshot DSR_K_NB_SIGNAL sets flag slot `rank` of every peer's
+   * `flags` to epoch + 1 (system-scope release); DSR_M_NB_FORCE and
+   * DSR_M_NB_PREPARE_MERGE first make the stream wait (cuStreamWaitValue32)
+   * until every other slot of this rank's flags[0 .. world) reached
+   * epoch + 1.  target: after prepare_merge, DSR_K_NB_PUSH_TARGET writes this
+   * rank's rows of target into every peer's target and sets their slot
+   * world + rank to step + 1; DSR_K_NB_CLAIM waits for slots world .. 2 world.
+   * The caller alternates S / V by epoch parity and target by step parity
+   * (two buffers each), which makes the exchanges safe without a barrier. */
+  uint32_t npeers;                    /* number of other ranks (<= 7) */
+  uint32_t rank, world;               /* this rank; ranks in the group (peer i = rank (rank + 1 + i) % world) */
+  uint32_t epoch;                     /* snapshot epoch (2 per step); for the target exchange: step */
+  uint32_t* flags;                    /* this rank's flags: 2 * world u32 (device) */
+  float* peer_S[7];
+  float* peer_V[7];
+  uint32_t* peer_target[7];
+  uint32_t* peer_flags[7];
 } dsr_nbody_args;
 enum {
   DSR_C_NB_BODY = 30,            /* parallel_new<Body>(id_hi - id_lo): body i gets id id_lo + i */
@@ -511,8 +534,12 @@ enum {
   DSR_M_NB_ABSORB = 35,
   DSR_M_NB_DELETE_MERGED = 36,   /* destroy(this) iff incoming[target] == id and target[target] == NONE */
   DSR_M_NB_DUMP = 37,
-  DSR_K_NB_CLEAR_SNAPSHOT = 30,  /* n = n_total: S.m = 0, shandle = 0, target = incoming = NONE */
-  DSR_K_NB_CLAIM = 31            /* n = n_total: the claim pass over the (gathered) target array */
+  DSR_K_NB_CLEAR_SNAPSHOT = 30,  /* n = n_total: S.m = 0, shandle = 0, target = incoming = NONE
+                                    (peer mode: this rank's rows of S in every peer too) */
+  DSR_K_NB_CLAIM = 31,           /* n = n_total: the claim pass over the (gathered) target array
+                                    (peer mode: waits for the peers' target rows first) */
+  DSR_K_NB_SIGNAL = 32,          /* n = n_total, peer mode: the snapshot's rows are in every peer: set their flags */
+  DSR_K_NB_PUSH_TARGET = 33      /* n = n_total, peer mode: this rank's target rows into every peer + their flags */
 };
 
 /* ---- Static-allocation baseline of Wa-Tor ----

@@ -13,6 +13,7 @@
 // V and target are all-gathered between passes).
 #include <algorithm>
 #include <cstring>
+#include <cuda.h>   // cuStreamWaitValue32 (types only: resolved at run time)
 #include "dsr_host.h"
 
 namespace dsr {
@@ -52,10 +53,36 @@ __global__ void __launch_bounds__(256) k_nb_new(DevHeap h, uint64_t n, dsr_nbody
 
 __global__ void k_nb_clear(uint64_t n, dsr_nbody_args a) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    reinterpret_cast<float4*>(a.S)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     a.shandle[i] = 0;
-    a.target[i] = kNone;
     a.incoming[i] = kNone;
+    if (!a.npeers) {
+      reinterpret_cast<float4*>(a.S)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      a.target[i] = kNone;
+    } else if (i >= a.id_lo && i < a.id_hi) {
+      // peer mode: only my rows -- the others' rows of S and target are theirs
+      // to write (their pushes may already have arrived); mine are cleared in
+      // every peer's S as well
+      reinterpret_cast<float4*>(a.S)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      a.target[i] = kNone;
+      for (uint32_t p = 0; p < a.npeers; ++p) reinterpret_cast<float4*>(a.peer_S[p])[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+}
+// peer mode: this rank's rows of the epoch are in every peer (kernel boundary:
+// the previous kernels' stores are performed) -> their flag slot `slot0 + rank`
+__global__ void k_nb_signal(dsr_nbody_args a, uint32_t slot0) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    __threadfence_system();
+    for (uint32_t p = 0; p < a.npeers; ++p)
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.peer_flags[p] + slot0 + a.rank), "r"(a.epoch + 1u)
+                   : "memory");
+  }
+}
+// peer mode: this rank's rows of target into every peer's target
+__global__ void k_nb_push_target(dsr_nbody_args a) {
+  for (uint32_t i = a.id_lo + blockIdx.x * blockDim.x + threadIdx.x; i < a.id_hi; i += gridDim.x * blockDim.x) {
+    const uint32_t t = a.target[i];
+    for (uint32_t p = 0; p < a.npeers; ++p) a.peer_target[p][i] = t;
   }
 }
 
@@ -64,10 +91,18 @@ struct NbSnapshot {
   DSR_NO_ACC
   static __device__ __forceinline__ void run(const DevHeap& h, uint32_t, uint32_t b, uint32_t s, const Args& a, Acc&) {
     const uint32_t id = bf<uint32_t>(h, b, s, NB_ID);
-    reinterpret_cast<float4*>(a.S)[id] = make_float4(bf<float>(h, b, s, NB_X), bf<float>(h, b, s, NB_Y),
-                                                     bf<float>(h, b, s, NB_M), 0.f);
-    reinterpret_cast<float2*>(a.V)[id] = make_float2(bf<float>(h, b, s, NB_VX), bf<float>(h, b, s, NB_VY));
+    const float4 p = make_float4(bf<float>(h, b, s, NB_X), bf<float>(h, b, s, NB_Y), bf<float>(h, b, s, NB_M), 0.f);
+    const float2 v = make_float2(bf<float>(h, b, s, NB_VX), bf<float>(h, b, s, NB_VY));
+    reinterpret_cast<float4*>(a.S)[id] = p;
+    reinterpret_cast<float2*>(a.V)[id] = v;
     a.shandle[id] = make_handle(0, h.types[0].cap, b, s);
+    // peer mode: the all-gather is this pass's stores into every peer's
+    // snapshot (over NVLink when they are other GPUs) -- one kernel computes
+    // the snapshot and distributes it
+    for (uint32_t q = 0; q < a.npeers; ++q) {
+      reinterpret_cast<float4*>(a.peer_S[q])[id] = p;
+      reinterpret_cast<float2*>(a.peer_V[q])[id] = v;
+    }
   }
 };
 
@@ -464,6 +499,27 @@ bool nb_method_info(uint32_t id, MethodInfo* mi) {
   return false;
 }
 
+// peer mode: the launching stream waits (front end, no SM held) until every
+// other rank's flag slot slot0 + r reached epoch + 1
+static bool peer_wait(const dsr_nbody_args& a, uint32_t slot0, cudaStream_t st) {
+  if (!a.npeers) return true;
+  typedef CUresult (*WaitFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+  static WaitFn wait = nullptr;
+  if (!wait) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    wait = (WaitFn)fn;
+  }
+  for (uint32_t r = 0; r < a.world; ++r)
+    if (r != a.rank && wait((CUstream)st, (CUdeviceptr)(a.flags + slot0 + r), a.epoch + 1u, CU_STREAM_WAIT_VALUE_GEQ) !=
+                           CUDA_SUCCESS)
+      return false;
+  return true;
+}
+
 // x: the i-blocks of the live-list chunks that hold my ids; y: the j chunks
 static dim3 pair_grid(const dsr_nbody_args& a) {
   return dim3(((a.id_hi - 1) / kChunk - a.id_lo / kChunk + 1) * kIBlocksPerChunk, (a.n_total + kChunk - 1) / kChunk);
@@ -478,6 +534,7 @@ bool nb_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot,
     case DSR_M_NB_SNAPSHOT: launch_doall<NbSnapshot>(c, T, snapshot, args); return true;
     case DSR_M_NB_FORCE:
       if (a.id_hi <= a.id_lo || !a.live) return a.id_hi <= a.id_lo;
+      if (!peer_wait(a, 0, c.st)) return false;
       launch_live(a, c.st);
       k_nb_force_part<<<pair_grid(a), kPairThreads, 0, c.st>>>(a);
       k_nb_force_sum<<<grid_for(c, a.id_hi - a.id_lo, k_nb_force_sum), 256, 0, c.st>>>(c.h, a);
@@ -486,6 +543,7 @@ bool nb_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot,
     case DSR_M_NB_MOVE: launch_doall<NbMove>(c, T, snapshot, args); return true;
     case DSR_M_NB_PREPARE_MERGE:
       if (a.id_hi <= a.id_lo || !a.live) return a.id_hi <= a.id_lo;
+      if (!peer_wait(a, 0, c.st)) return false;
       launch_live(a, c.st);
       k_nb_merge_part<<<pair_grid(a), kPairThreads, 0, c.st>>>(a);
       k_nb_merge_pick<<<grid_for(c, a.id_hi - a.id_lo, k_nb_merge_pick), 256, 0, c.st>>>(c.h, a);
@@ -501,12 +559,27 @@ bool nb_method_launch(uint32_t id, const LaunchCtx& c, uint32_t T, int snapshot,
 
 bool nb_kernel_launch(uint32_t id, const LaunchCtx& c, uint64_t n, const void* args, size_t bytes, int* ok) {
   *ok = 1;
-  if (id != DSR_K_NB_CLEAR_SNAPSHOT && id != DSR_K_NB_CLAIM) return false;
+  if (id != DSR_K_NB_CLEAR_SNAPSHOT && id != DSR_K_NB_CLAIM && id != DSR_K_NB_SIGNAL && id != DSR_K_NB_PUSH_TARGET)
+    return false;
   if (bytes != sizeof(dsr_nbody_args)) { *ok = 0; return true; }
   const dsr_nbody_args a = *(const dsr_nbody_args*)args;
-  if (n != a.n_total) { *ok = 0; return true; }
-  if (id == DSR_K_NB_CLEAR_SNAPSHOT) k_nb_clear<<<grid_for(c, n, k_nb_clear), 256, 0, c.st>>>(n, a);
-  else k_nb_claim_all<<<grid_for(c, n, k_nb_claim_all), 256, 0, c.st>>>(n, a);
+  if (n != a.n_total || a.npeers > 7 || (a.npeers && (!a.flags || a.world != a.npeers + 1 || a.rank >= a.world))) {
+    *ok = 0;
+    return true;
+  }
+  if ((id == DSR_K_NB_SIGNAL || id == DSR_K_NB_PUSH_TARGET) && !a.npeers) { *ok = 0; return true; }
+  if (id == DSR_K_NB_CLEAR_SNAPSHOT) {
+    k_nb_clear<<<grid_for(c, n, k_nb_clear), 256, 0, c.st>>>(n, a);
+  } else if (id == DSR_K_NB_CLAIM) {
+    if (!peer_wait(a, a.world, c.st)) { *ok = 0; return true; }
+    k_nb_claim_all<<<grid_for(c, n, k_nb_claim_all), 256, 0, c.st>>>(n, a);
+  } else if (id == DSR_K_NB_SIGNAL) {
+    k_nb_signal<<<1, 32, 0, c.st>>>(a, 0);
+  } else {
+    k_nb_push_target<<<grid_for(c, a.id_hi - a.id_lo, k_nb_push_target), 256, 0, c.st>>>(a);
+    k_nb_signal<<<1, 32, 0, c.st>>>(a, a.world);
+    count_launch();
+  }
   count_launch();
   return true;
 }

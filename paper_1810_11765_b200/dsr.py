@@ -56,7 +56,7 @@ def wt_halo_layout(W: int) -> dict:
             "mig": (mig_out, mig_out + 24 * W, 12 * W), "bytes": mig_out + 48 * W}
 (M_WT_CELL_PREPARE, M_WT_FISH_PREPARE, M_WT_CELL_DECIDE_FISH, M_WT_FISH_UPDATE, M_WT_SHARK_PREPARE,
  M_WT_CELL_DECIDE_SHARK, M_WT_SHARK_UPDATE, M_WT_DUMP) = range(20, 28)
-C_NB_BODY, K_NB_CLEAR_SNAPSHOT, K_NB_CLAIM = 30, 30, 31
+C_NB_BODY, K_NB_CLEAR_SNAPSHOT, K_NB_CLAIM, K_NB_SIGNAL, K_NB_PUSH_TARGET = 30, 30, 31, 32, 33
 (M_NB_SNAPSHOT, M_NB_FORCE, M_NB_MOVE, M_NB_PREPARE_MERGE, M_NB_CLAIM, M_NB_ABSORB, M_NB_DELETE_MERGED,
  M_NB_DUMP) = range(30, 38)
 
@@ -172,7 +172,10 @@ class NbodyArgs(C.Structure):
                 ("x0", C.c_void_p), ("y0", C.c_void_p), ("vx0", C.c_void_p), ("vy0", C.c_void_p),
                 ("m0", C.c_void_p), ("G", C.c_float), ("dt", C.c_float), ("eps", C.c_float), ("R", C.c_float),
                 ("n_total", C.c_uint32), ("id_lo", C.c_uint32), ("id_hi", C.c_uint32), ("out", C.c_void_p),
-                ("scratch", C.c_void_p), ("live", C.c_void_p)]
+                ("scratch", C.c_void_p), ("live", C.c_void_p),
+                ("npeers", C.c_uint32), ("rank", C.c_uint32), ("world", C.c_uint32), ("epoch", C.c_uint32),
+                ("flags", C.c_void_p), ("peer_S", C.c_void_p * 7), ("peer_V", C.c_void_p * 7),
+                ("peer_target", C.c_void_p * 7), ("peer_flags", C.c_void_p * 7)]
 
 
 class DsrError(RuntimeError):

@@ -45,9 +45,12 @@ class Exchange:
 
 class NBody:
     def __init__(self, state, G, dt, eps, R, merges=True, heap_bytes=None, device=None, stream=None, group=None,
-                 n_total=None, shard=None):
+                 n_total=None, shard=None, peer=False):
         """state: dict of x, y, vx, vy, m for ALL ids (each rank keeps its chunk).
-        shard = (rank, world) emulates a rank without a process group (loopback)."""
+        shard = (rank, world) emulates a rank without a process group (loopback).
+        peer: the all-gathers are the snapshot pass's own stores into every
+        peer's (epoch-parity) buffers plus flags (dsr.h "Peer-memory
+        all-gathers"); connect() sets the peers' buffers first."""
         import numpy as np
         import torch
         self.xch = Exchange(group)
@@ -80,6 +83,39 @@ class NBody:
                                   i["m"].data_ptr(), G, dt, eps, R, N, self.lo, self.hi, self.out.data_ptr(),
                                   self.scratch.data_ptr(), self.live.data_ptr())
         self.heap.parallel_new(0, n, dsr.C_NB_BODY, self.args, stream)
+        self.peer = bool(peer) and self.world > 1
+        self.epoch = 0                              # snapshots taken (2 per step)
+        self.step_no = 0
+        if self.peer:
+            # double buffers by epoch (S, V) and step (target) parity; flags: 2 x world u32
+            self.S2 = [self.S, torch.zeros_like(self.S)]
+            self.V2 = [self.V, torch.zeros_like(self.V)]
+            self.T2 = [self.target, torch.full_like(self.target, -1)]
+            self.flags = torch.zeros(2 * self.world, dtype=torch.int32, device=dev)
+            a = self.args
+            a.npeers, a.rank, a.world, a.flags = self.world - 1, self.rank, self.world, self.flags.data_ptr()
+            self.peers = None
+
+    def peer_buffers(self):
+        """This rank's exchanged buffers (for the peers to map): S[2], V[2], target[2], flags."""
+        return {"S": self.S2, "V": self.V2, "target": self.T2, "flags": self.flags}
+
+    def connect(self, peers):
+        """peers[i]: device pointers {"S": [p0, p1], "V": [...], "target": [...], "flags": p} of rank
+        (rank + 1 + i) % world (other shards' buffers on this GPU, or IPC-mapped ones)."""
+        assert self.peer and len(peers) == self.world - 1
+        self.peers = peers
+
+    def _peer_args(self, e=None, k=None):
+        a = self.args
+        if e is not None:
+            a.S, a.V, a.epoch = self.S2[e & 1].data_ptr(), self.V2[e & 1].data_ptr(), e
+            for i, p in enumerate(self.peers):
+                a.peer_S[i], a.peer_V[i], a.peer_flags[i] = p["S"][e & 1], p["V"][e & 1], p["flags"]
+        if k is not None:
+            a.target = self.T2[k & 1].data_ptr()
+            for i, p in enumerate(self.peers):
+                a.peer_target[i] = p["target"][k & 1]
 
     # ---- one step as a sequence of local phases ("p") and exchange points ("x")
     def sequence(self):
@@ -90,8 +126,15 @@ class NBody:
 
     def p_snapshot(self, s):
         h, a = self.heap, self.args
+        if self.peer:
+            if self.epoch % 2 == 0:                 # a step begins: its target buffer
+                self._peer_args(k=self.step_no)
+            self._peer_args(e=self.epoch)
         h.launch(dsr.K_NB_CLEAR_SNAPSHOT, self.n_total, a, s)
         h.parallel_do(0, dsr.M_NB_SNAPSHOT, a, s)
+        if self.peer:
+            h.launch(dsr.K_NB_SIGNAL, self.n_total, a, s)
+            self.epoch += 1
 
     def p_force_move(self, s):
         self.heap.parallel_do(0, dsr.M_NB_FORCE, self.args, s)
@@ -102,27 +145,41 @@ class NBody:
 
     def p_claim_absorb_delete(self, s):
         h, a = self.heap, self.args
+        if self.peer:
+            a.epoch = self.step_no                   # the claim waits for the peers' target rows of this step
         if self.world > 1:
             h.launch(dsr.K_NB_CLAIM, self.n_total, a, s)       # over the gathered targets of all ids
         else:
             h.parallel_do(0, dsr.M_NB_CLAIM, a, s)
         h.parallel_do(0, dsr.M_NB_ABSORB, a, s)
         h.parallel_do(0, dsr.M_NB_DELETE_MERGED, a, s)
+        if self.peer:
+            self.args.epoch = self.epoch - 1         # (only the target exchange used the step number)
+        self.step_no += 1
 
-    def x_SV(self):
-        self.xch.all_gather_rows(self.S, self.lo, self.hi)
-        self.xch.all_gather_rows(self.V, self.lo, self.hi)
+    def _push_target(self, s):
+        a = self.args
+        a.epoch = self.step_no
+        self.heap.launch(dsr.K_NB_PUSH_TARGET, self.n_total, a, s)
 
-    def x_target(self):
-        self.xch.all_gather_rows(self.target, self.lo, self.hi)
+    def x_SV(self, s=None):
+        if self.peer:
+            return                                   # the snapshot pass wrote every peer's rows
+        with dsr.on_stream(s if s is not None else self.stream):   # in order with the kernels on s
+            self.xch.all_gather_rows(self.S, self.lo, self.hi)
+            self.xch.all_gather_rows(self.V, self.lo, self.hi)
+
+    def x_target(self, s=None):
+        if self.peer:
+            self._push_target(s if s is not None else self.stream)   # my rows into every peer's target + flags
+            return
+        with dsr.on_stream(s if s is not None else self.stream):
+            self.xch.all_gather_rows(self.target, self.lo, self.hi)
 
     def step(self, stream=None):
         s = stream if stream is not None else self.stream
         for name in self.sequence():
-            if name.startswith("p_"):
-                getattr(self, name)(s)
-            else:
-                getattr(self, name)()
+            getattr(self, name)(s)
 
     def run(self, steps, stream=None):
         for _ in range(steps):
@@ -183,6 +240,43 @@ class NBodyStatic:
         return {"x": z(S[:, 0]), "y": z(S[:, 1]), "vx": z(V[:, 0]), "vy": z(V[:, 1]), "m": z(S[:, 2]), "alive": alive}
 
 
+class NBodyPeer:
+    """Multi-process peer mode: every rank exports its exchanged buffers (S and
+    V of both epoch parities, target of both step parities, flags) as CUDA IPC
+    handles, all-gathers them over torch.distributed and maps every other
+    rank's (over NVLink / NVSwitch when they are other GPUs)."""
+
+    def __init__(self, sim, group=None):
+        import torch.distributed as dist
+        assert sim.peer, "NBody(..., peer=True) under a process group of > 1 ranks"
+        bufs = sim.peer_buffers()
+        mine = {k: ([dsr.ipc_handle(t) for t in v] if isinstance(v, list) else dsr.ipc_handle(v))
+                for k, v in bufs.items()}
+        allh = [None] * sim.world
+        dist.all_gather_object(allh, mine, group=group)
+        self.opened = []
+        bases = {}                                  # one mapping per exported block (a caching allocator
+                                                    # may put several buffers in one block)
+
+        def open_(hd):
+            h, off = hd
+            if h not in bases:
+                bases[h] = dsr.ipc_open(h)
+                self.opened.append(bases[h])
+            return bases[h] + off
+        peers = []
+        for i in range(sim.world - 1):
+            r = (sim.rank + 1 + i) % sim.world
+            peers.append({k: ([open_(x) for x in v] if isinstance(v, list) else open_(v)) for k, v in allh[r].items()})
+        sim.connect(peers)
+        dist.barrier(group)
+
+    def close(self):
+        for p in self.opened:
+            dsr.ipc_close(p)
+        self.opened = []
+
+
 class NBodyLoopback:
     """P id-range shards of the N-body step on ONE GPU: P heaps, the same
     kernels and phase order as the multi-GPU run, the all-gathers replaced by
@@ -191,6 +285,12 @@ class NBodyLoopback:
 
     def __init__(self, state, P, **kw):
         self.shards = [NBody(state, shard=(r, P), **kw) for r in range(P)]
+        if self.shards[0].peer:                      # peer mode: each shard writes into the others' buffers
+            bufs = [sh.peer_buffers() for sh in self.shards]
+            ptrs = [{"S": [t.data_ptr() for t in b["S"]], "V": [t.data_ptr() for t in b["V"]],
+                     "target": [t.data_ptr() for t in b["target"]], "flags": b["flags"].data_ptr()} for b in bufs]
+            for r, sh in enumerate(self.shards):
+                sh.connect([ptrs[(r + 1 + i) % P] for i in range(P - 1)])
 
     def _gather(self, attr):
         src = self.shards
@@ -204,6 +304,10 @@ class NBodyLoopback:
             if name.startswith("p_"):
                 for sh in self.shards:
                     getattr(sh, name)(sh.stream)
+            elif self.shards[0].peer:
+                if name == "x_target":              # push every shard's rows before any claim waits for them
+                    for sh in self.shards:
+                        sh.x_target(sh.stream)
             elif name == "x_SV":
                 self._gather("S")
                 self._gather("V")

@@ -158,6 +158,23 @@ def test_nbody_against_oracle(P, O, n, steps, merges):
     assert sim.heap.check_invariants() == 0
 
 
+def test_nbody_peer_two_processes(P, O):
+    """Two processes (one id range each) map each other's snapshot / target
+    buffers through CUDA IPC and exchange only through them -- the multi-GPU
+    path, here with both processes on one GPU; equal to the one-heap run."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(30000 + os.getpid() % 1000),
+           str(root / "tests" / "peer_worker_nbody.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=str(root))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "NBODY PEER OK" in r.stdout, r.stdout[-3000:]
+
+
 @pytest.mark.slow
 def test_nbody_65536_one_step(P, O):
     from paper_1810_11765_b200 import inputs as I, nbody
@@ -174,11 +191,14 @@ def test_nbody_65536_one_step(P, O):
     assert rel_pos_err(got["y"][al], want["y"][al]) <= 1e-4
 
 
-@pytest.mark.parametrize("P", [2, 4])
-def test_nbody_sharded_loopback_equals_one_gpu(P, O):
+@pytest.mark.parametrize("P,peer", [(2, False), (4, False), (2, True), (4, True), (8, True)])
+def test_nbody_sharded_loopback_equals_one_gpu(P, O, peer):
     """The id-range-sharded N-body (P heaps, chunk exchanges) reproduces the
     single-heap run bit for bit: the all-pairs partials use fixed global
-    j-chunks, so nothing depends on P."""
+    j-chunks, so nothing depends on P.  peer: the exchanges
+    are the snapshot pass's own stores into every other shard's epoch-parity
+    buffers plus flags, and the target rows pushed the same way (no copies,
+    no collective)."""
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     from paper_1810_11765_b200 import inputs as I, nbody
@@ -187,7 +207,7 @@ def test_nbody_sharded_loopback_equals_one_gpu(P, O):
     one = nbody.NBody(st, merges=True, **prm)
     one.run(6)
     a = one.state()
-    lb = nbody.NBodyLoopback(st, P, merges=True, **prm)
+    lb = nbody.NBodyLoopback(st, P, merges=True, peer=peer, **prm)
     lb.run(6)
     b = lb.state()
     assert (a["alive"] == 0).sum() > 10
