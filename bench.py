@@ -50,8 +50,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-apps", action="store_true", help="skip the per-app block of the default line")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
-                    help="GoL row bands under torchrun: NCCL P2P of the boundary masks, or the peer-memory push "
-                         "(DSR_K_GOL_HALO_PUSH into the neighbours' IPC-mapped halo buffers)")
+                    help="sharded apps under torchrun: NCCL collectives, or peer memory (GoL: DSR_K_GOL_HALO_PUSH "
+                         "into the neighbours' IPC-mapped halo buffers; N-body: the snapshot pass stores into "
+                         "every rank's buffers)")
     ap.add_argument("--launch-list", action="store_true",
                     help="run only W + K microbench steps (for ncu launch lists) and print no bench line")
     ap.add_argument("--dry-run", action="store_true",
@@ -931,9 +932,13 @@ def run_app(args):
     else:
         from paper_1810_11765_b200.nbody import NBody
         st = I.nbody_init(65536, seed=7)
-        # N > 1: id-range shards, S/V/target all-gathered over NCCL
+        # N > 1: id-range shards, S/V/target all-gathered over NCCL, or (--exchange peer) stored by the
+        # snapshot pass straight into every rank's IPC-mapped buffers
         sim = NBody(st, merges=True, stream=stream, group=dist.group.WORLD if world > 1 else None,
-                    **I.NBODY_PARAMS)
+                    peer=args.exchange == "peer", **I.NBODY_PARAMS)
+        if sim.peer:
+            from paper_1810_11765_b200.nbody import NBodyPeer
+            sim.peer_map = NBodyPeer(sim)
 
         def per(k):
             sim.heap.live_count_async(0, live[k, 0], stream)
@@ -948,7 +953,11 @@ def run_app(args):
         pairs = 2 * float(np.mean(np.square(tot_live)))                       # force + merge pass pairs
         cfg = {"workload": "nbody with merging (BASELINE configs[2]) 65536 bodies", "pairs_per_step": pairs,
                "pair_interactions_per_s": pairs / (ms * 1e-3),
-               "parallelism": f"{world} id-range shards, NCCL all-gather of snapshot chunks" if world > 1 else "1 GPU"}
+               "parallelism": (f"{world} id-range shards, " + ("snapshot / target rows stored into every "
+                                                               "rank's memory over NVLink (peer mode)"
+                                                               if args.exchange == "peer"
+                                                               else "NCCL all-gather of snapshot chunks"))
+               if world > 1 else "1 GPU"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
