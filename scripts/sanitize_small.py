@@ -37,6 +37,18 @@ nb.run(3)
 got = nb.state()
 want = O.nbody_run(st, merges=True, steps=3, **prm)
 ok.append(("nbody 1000", np.array_equal(got["alive"], want["alive"])))
+from paper_1810_11765_b200.gol import GameOfLifeLoopback
+lbg = GameOfLifeLoopback(a0, 2, peer=True, heap_bytes=16 << 20)
+lbg.run(10)
+ok.append(("gol 64 two shards, peer-memory halo", np.array_equal(lbg.alive(), O.life_dense(a0, 10))))
+from paper_1810_11765_b200.nbody import NBodyLoopback
+st2 = I.nbody_init(1024, seed=7)
+lbn = NBodyLoopback(st2, 2, merges=True, peer=True, **prm)
+lbn.run(3)
+one = NBody(st2, merges=True, **prm)
+one.run(3)
+ok.append(("nbody 1024 two shards, peer-memory all-gathers",
+           all(np.array_equal(lbn.state()[k], one.state()[k]) for k in ("x", "y", "m", "alive"))))
 from paper_1810_11765_b200.nbody import NBodyStatic
 nbs = NBodyStatic(st, merges=True, **prm)
 nbs.run(3)
