@@ -78,18 +78,85 @@ __global__ void __launch_bounds__(256, MINB) k_mb_new(DevHeap h, uint64_t n, dsr
 #endif
 constexpr uint32_t kMbUnit = DSR_MB_UNIT;
 
-// Constructor of the reserved slots of one dsr_new_warp call for type T with
-// NF u32 fields (compile-time, so the field loop is unrolled and the column
-// offsets live in registers): chunk by chunk in lane order, lane j -> the
-// chunk's j-th reserved slot = the (done + cum + j)-th object of T in the unit.
-template <int NF, bool IN>
+// Constructor of the reserved slots of one dsr_new_warp call for type T.
+// The objects are ranked in lane order of the chunks, then by slot: the chunk
+// of lane c holds objects done + cum_c ...
+//  * quads: a chunk that is one run of slots starting at a multiple of 4
+//    (every fresh block, the free tail of a block) is cut into quads of 4
+//    slots; the warp's quads of all such chunks are dealt out to the lanes (a
+//    per-warp table in shared memory, walked with a cursor), and a lane
+//    computes the 4 objects' keys and writes each column with one 128-bit
+//    store; the last cnt % 4 objects of such a chunk are written by the lane
+//    that holds the chunk;
+//  * other chunks (holes of partly freed blocks): chunk by chunk, lane j ->
+//    the chunk's j-th reserved slot, looked up in a per-warp slot list the
+//    lanes build with one popc each (no per-object n-th-bit search).
+// One copy of each loop for all types, with the field loop not unrolled and
+// the column offsets read from the kernel parameter space: the constructor's
+// instruction footprint, not its instruction count, decided its speed (ncu:
+// "no instruction" was the top stall with an unrolled copy per type).
+// sw: this warp's shared scratch, kMbScratch words.
+constexpr uint32_t kMbScratch = 4 * 32 + 16;
+#ifndef DSR_MB_KEYMAD
+#define DSR_MB_KEYMAD 1
+#endif
+#ifndef DSR_MB_KEYHI
+#define DSR_MB_KEYHI 1
+#endif
+// 1, but not a constant to the compiler: multiplies by it (and by its powers
+// of two) stay IMADs on the FMA pipe instead of being folded into adds and
+// shifts on the ALU pipe (pipe balancing of the key's mix, see sm64_mix_lo)
+__constant__ uint32_t kMbOne = 1;
+// low 32 bits of sm64 after its first step (z = x + G).  The key is 11 ALU-pipe
+// instructions (shifts, xors) to 9 FMA-pipe ones (the 64-bit multiplies); each
+// pipe takes a warp instruction every 2 cycles per scheduler, so with KEYHI the
+// high word's first shift (hi >> 30) is a multiply-high by 4 (= one << 2).
+__device__ __forceinline__ uint32_t sm64_mix_lo(uint64_t z, uint32_t one) {
+#if DSR_MB_KEYHI
+  const uint32_t hi = (uint32_t)(z >> 32), lo = (uint32_t)z;
+  z = ((uint64_t)(hi ^ __umulhi(hi, one << 2)) << 32 | (lo ^ (uint32_t)(z >> 30))) * 0xBF58476D1CE4E5B9ull;
+#else
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+#endif
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return (uint32_t)(z ^ (z >> 31));
+}
+// t of the i-th object of type T in the unit (residues off0 [, off1] of t & 3)
+__device__ __forceinline__ uint64_t mb_t(uint64_t ts, uint32_t nres, uint32_t off0, uint32_t off1, uint32_t i) {
+  return nres == 2 ? ts + 4ull * (i >> 1) + ((i & 1) ? off1 : off0) : ts + 4ull * i + off0;
+}
+// the same for 4 independent keys, step by step (the 4 dependent chains
+// interleaved in program order, so a warp has 4 independent instructions to
+// issue back to back instead of waiting out each one's latency)
+#ifndef DSR_MB_KEY4
+#define DSR_MB_KEY4 1
+#endif
+__device__ __forceinline__ void sm64_mix_lo4(uint64_t z[4], uint32_t one, uint32_t v[4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+#if DSR_MB_KEYHI
+    const uint32_t hi = (uint32_t)(z[j] >> 32), lo = (uint32_t)z[j];
+    z[j] = (uint64_t)(hi ^ __umulhi(hi, one << 2)) << 32 | (lo ^ (uint32_t)(z[j] >> 30));
+#else
+    z[j] ^= z[j] >> 30;
+#endif
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) z[j] *= 0xBF58476D1CE4E5B9ull;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) z[j] ^= z[j] >> 27;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) z[j] *= 0x94D049BB133111EBull;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) v[j] = (uint32_t)(z[j] ^ (z[j] >> 31));
+}
+template <bool IN>
 __device__ __forceinline__ void mb_construct(const DevHeap& h, uint32_t T, const dsr_mb_new_args& a, uint64_t kp,
                                              uint64_t ts, uint32_t nres, uint32_t off0, uint32_t off1, uint32_t done,
-                                             uint32_t bid, uint64_t mask) {
+                                             uint32_t bid, uint64_t mask, uint32_t* sw) {
   const uint32_t lane = threadIdx.x & 31;
-  uint32_t col[NF];
-#pragma unroll
-  for (int k = 0; k < NF; ++k) col[k] = h.types[T].col_off[k];
+  const uint32_t lt = (1u << lane) - 1u;
+  const uint32_t nf = h.types[T].nfields;
   const uint32_t cnt = (uint32_t)__popcll(mask);
   uint32_t cum = cnt;                                      // exclusive prefix in lane order
 #pragma unroll
@@ -98,7 +165,113 @@ __device__ __forceinline__ void mb_construct(const DevHeap& h, uint32_t T, const
     if (lane >= (uint32_t)o) cum += v;
   }
   cum -= cnt;
-  uint32_t chunks = __ballot_sync(0xffffffffu, mask != 0);
+  // one object: slot s of block b, the i-th of T in the unit (fields unrolled
+  // up to the microbench's largest type, column offsets in registers)
+  constexpr uint32_t kMaxF = 6;
+  uint32_t col[kMaxF];
+#pragma unroll
+  for (uint32_t k = 0; k < kMaxF; ++k) col[k] = k < nf ? h.types[T].col_off[k] : 0u;
+  auto construct = [&](uint32_t b, uint32_t s, uint32_t i) {
+    const uint64_t t = mb_t(ts, nres, off0, off1, i);
+    uint8_t* const obj = h.data + (size_t)b * h.block_bytes + 4u * s;
+    const uint32_t* src = nullptr;
+    if (IN) {
+      const uint64_t ti = t - a.t0;
+      src = a.in + 16 * (ti >> 2) + ((0xA630u >> (4 * (ti & 3))) & 0xFu);
+    }
+#pragma unroll
+    for (uint32_t k = 0; k < kMaxF; ++k)
+      if (k < nf) *reinterpret_cast<uint32_t*>(obj + col[k]) = IN ? __ldg(src + k) : (uint32_t)rng_key_p(kp, 5, t * 16 + k);
+  };
+  const uint32_t lo = mask ? ctz64(mask) : 0u;
+  const uint64_t run = mask >> lo;
+  const bool quad = !IN && mask != 0 && (lo & 3u) == 0 && (run & (run + 1ull)) == 0;
+  const uint32_t nq = quad ? cnt >> 2 : 0u;                // full quads
+  const uint32_t qball = __ballot_sync(0xffffffffu, nq != 0);
+  if (qball) {
+    uint32_t qin = nq;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, qin, o);
+      if (lane >= (uint32_t)o) qin += v;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, qin, 31);
+    const uint32_t nqc = (uint32_t)__popc(qball);
+    if (nq) {                                              // table entry: quad start, block, first slot, first object
+      const uint32_t e = (uint32_t)__popc(qball & lt);
+      sw[e] = qin - nq;
+      sw[32 + e] = bid;
+      sw[64 + e] = lo;
+      sw[96 + e] = cum + done;
+    }
+    __syncwarp();
+    const uint64_t kx = kp ^ (5ull << 40);                 // key of field k of t = sm64(kx ^ (16 t + k)), 16 t + k < 2^40
+#if DSR_MB_KEYMAD
+    // sm64 starts with x + G.  x = kx ^ 16t ^ k = (kx ^ 16t ^ c) + (c ^ k), c = kx & 15:
+    // per object Y = (kx ^ 16t ^ c) + G, per field z = Y + (c ^ k) as one
+    // IMAD.WIDE.U32 (c ^ k) * one + Y on the FMA pipe (the key's xor-shifts
+    // keep the ALU pipe the busier one; `one` is 1 but not a constant to ptxas,
+    // which would turn the multiply-add back into an IADD3 pair)
+    const uint32_t cx = (uint32_t)kx & 15u;
+    const uint32_t one = kMbOne;
+#endif
+    // the quad's chunk: when all quad chunks have the same length (whole fresh
+    // blocks: the common case), g / nq by a float reciprocal (exact after one
+    // upward correction for g < 2^20); otherwise a cursor over the table
+    const uint32_t nqmax = __reduce_max_sync(0xffffffffu, nq);
+    const bool even = __reduce_min_sync(0xffffffffu, nq ? nq : 0xFFFFFFFFu) == nqmax;
+    const float rq = __frcp_rn((float)nqmax);
+    // t of the 4 objects of a quad from the first one's: t0 + {0, u, w, u + w}
+    // (nres = 1: u = 4, w = 8; nres = 2: w = 4, u = off1 - off0 if the first
+    // object has residue off0, else 4 - (off1 - off0))
+    const uint32_t w = nres == 2 ? 4u : 8u;
+    uint32_t cur = 0;
+    for (uint32_t g = lane; g < total; g += 32) {
+      uint32_t q;
+      if (even) {
+        cur = (uint32_t)((float)g * rq);
+        q = g - cur * nqmax;
+        if (q >= nqmax) { q -= nqmax; ++cur; }
+      } else {
+        while (cur + 1 < nqc && sw[cur + 1] <= g) ++cur;
+        q = g - sw[cur];
+      }
+      const uint32_t i = sw[96 + cur] + 4u * q;
+      uint8_t* const p = h.data + (size_t)sw[32 + cur] * h.block_bytes + 4u * (sw[64 + cur] + 4u * q);
+      const uint64_t t0 = mb_t(ts, nres, off0, off1, i);
+      const uint32_t u = nres == 2 ? ((i & 1) ? 4u - (off1 - off0) : off1 - off0) : 4u;
+      const uint64_t x0 = kx ^ (t0 << 4), x1 = kx ^ ((t0 + u) << 4);
+      const uint64_t x2 = kx ^ ((t0 + w) << 4), x3 = kx ^ ((t0 + u + w) << 4);
+#if DSR_MB_KEYMAD
+      const uint64_t y0 = (x0 ^ cx) + 0x9E3779B97F4A7C15ull, y1 = (x1 ^ cx) + 0x9E3779B97F4A7C15ull;
+      const uint64_t y2 = (x2 ^ cx) + 0x9E3779B97F4A7C15ull, y3 = (x3 ^ cx) + 0x9E3779B97F4A7C15ull;
+#endif
+#pragma unroll 1
+      for (uint32_t k = 0; k < nf; ++k) {
+#if DSR_MB_KEYMAD && DSR_MB_KEY4
+        const uint32_t ck = cx ^ k;
+        uint64_t z[4] = {y0 + (uint64_t)ck * one, y1 + (uint64_t)ck * one, y2 + (uint64_t)ck * one, y3 + (uint64_t)ck * one};
+        uint32_t v[4];
+        sm64_mix_lo4(z, one, v);
+        const uint32_t v0 = v[0], v1 = v[1], v2 = v[2], v3 = v[3];
+#elif DSR_MB_KEYMAD
+        const uint32_t ck = cx ^ k;
+        const uint32_t v0 = sm64_mix_lo(y0 + (uint64_t)ck * one, one), v1 = sm64_mix_lo(y1 + (uint64_t)ck * one, one);
+        const uint32_t v2 = sm64_mix_lo(y2 + (uint64_t)ck * one, one), v3 = sm64_mix_lo(y3 + (uint64_t)ck * one, one);
+#else
+        const uint32_t v0 = (uint32_t)sm64(x0 ^ (uint64_t)k), v1 = (uint32_t)sm64(x1 ^ (uint64_t)k);
+        const uint32_t v2 = (uint32_t)sm64(x2 ^ (uint64_t)k), v3 = (uint32_t)sm64(x3 ^ (uint64_t)k);
+#endif
+        *reinterpret_cast<uint4*>(p + h.types[T].col_off[k]) = make_uint4(v0, v1, v2, v3);
+      }
+    }
+    __syncwarp();
+  }
+  // the last cnt % 4 objects of a quad chunk: by the lane that holds it
+  if (quad)
+    for (uint32_t j = 4u * nq; j < cnt; ++j) construct(bid, lo + j, cum + done + j);
+  uint32_t chunks = __ballot_sync(0xffffffffu, mask != 0 && !quad);
+  uint8_t* const slots = reinterpret_cast<uint8_t*>(sw + 128);
   while (chunks) {
     const uint32_t c = __ffs(chunks) - 1;
     chunks &= chunks - 1;
@@ -106,41 +279,25 @@ __device__ __forceinline__ void mb_construct(const DevHeap& h, uint32_t T, const
     const uint64_t cm = shfl64(0xffffffffu, mask, c);
     const uint32_t c0 = __shfl_sync(0xffffffffu, cum, c) + done;
     const uint32_t cn = (uint32_t)__popcll(cm);
-    uint8_t* const blk = h.data + (size_t)cb * h.block_bytes;
-    // object i (the i-th of T in the unit) goes to slot s of the chunk's block
-    auto construct = [&](uint32_t s, uint32_t i) {
-      const uint64_t t = nres == 2 ? ts + 4ull * (i >> 1) + ((i & 1) ? off1 : off0) : ts + 4ull * i + off0;
-      uint8_t* const obj = blk + 4u * s;
-      if (IN) {
-        const uint64_t ti = t - a.t0;
-        const uint32_t* src = a.in + 16 * (ti >> 2) + ((0xA630u >> (4 * (ti & 3))) & 0xFu);
-#pragma unroll
-        for (int k = 0; k < NF; ++k) *reinterpret_cast<uint32_t*>(obj + col[k]) = __ldg(src + k);
-      } else {
-#pragma unroll
-        for (int k = 0; k < NF; ++k) *reinterpret_cast<uint32_t*>(obj + col[k]) = (uint32_t)rng_key_p(kp, 5, t * 16 + k);
-      }
-    };
-    // the chunk's mask is warp-uniform: one run of slots (a fresh block, the
-    // free tail of a block) -> lane j takes slot lo + j; otherwise lane p takes
-    // slot p (and p + 32) if it is in the mask, ranked by a popc of the bits
-    // below it (no per-object n-th-bit search)
-    const uint32_t lo = ctz64(cm);
-    const uint64_t run = cm >> lo;
-    const bool single = (run & (run + 1ull)) == 0;       // warp-uniform
-    // one copy of the constructor in the code (the kernel's instruction
-    // footprint showed as no-instruction stalls)
-    for (uint32_t j = lane; j < cn; j += 32) construct(single ? lo + j : nth_bit(cm, j), c0 + j);
+    // slot list: lane p places slots p and p + 32 at their ranks
+    const uint32_t mlo = (uint32_t)cm, mhi = (uint32_t)(cm >> 32);
+    if ((mlo >> lane) & 1u) slots[__popc(mlo & lt)] = (uint8_t)lane;
+    if ((mhi >> lane) & 1u) slots[__popc(mlo) + __popc(mhi & lt)] = (uint8_t)(lane + 32);
+    __syncwarp();
+    for (uint32_t j = lane; j < cn; j += 32) construct(cb, slots[j], c0 + j);
+    __syncwarp();
   }
 }
 
 #ifndef DSR_MB_BULK_MINB
-#define DSR_MB_BULK_MINB 6   // 6 CTAs x 256 threads per SM (40 registers, 16 B of spills): sweep 1 / 5 / 6 / 7 / 8 -> 2.14 / 2.04 / 1.99 / 2.35 / 2.36 ms per step
+#define DSR_MB_BULK_MINB 4   // CTAs x 256 threads per SM (64 registers, no spills); see DESIGN §6 for the sweep
 #endif
 template <bool IN = false>
 __global__ void __launch_bounds__(256, DSR_MB_BULK_MINB) k_mb_new_bulk(DevHeap h, uint64_t n, dsr_mb_new_args a) {
   const uint64_t kp = rng_prefix(a.seed, 0);
   const uint32_t lane = threadIdx.x & 31;
+  __shared__ uint32_t s_scr[8][kMbScratch];
+  uint32_t* const sw = s_scr[threadIdx.x >> 5];
   for (;;) {
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(&h.ctrl[CTRL_WORK], (unsigned long long)kMbUnit);
@@ -169,9 +326,7 @@ __global__ void __launch_bounds__(256, DSR_MB_BULK_MINB) k_mb_new_bulk(DevHeap h
         uint64_t mask;
         const uint32_t got = dsr_new_warp(h, T, need - done, &bid, &mask);
         if (!got) break;                                   // OOM (sticky error set)
-        if (T == 0) mb_construct<3, IN>(h, T, a, kp, ts, nres, off0, off1, done, bid, mask);
-        else if (T == 1) mb_construct<4, IN>(h, T, a, kp, ts, nres, off0, off1, done, bid, mask);
-        else mb_construct<6, IN>(h, T, a, kp, ts, nres, off0, off1, done, bid, mask);
+        mb_construct<IN>(h, T, a, kp, ts, nres, off0, off1, done, bid, mask, sw);
         done += got;
       }
     }
