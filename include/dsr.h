@@ -205,7 +205,9 @@ dsr_status dsr_live_count(dsr_heap* h, uint32_t type, uint64_t* dev_out, void* s
 dsr_status dsr_live_count_sync(dsr_heap* h, uint32_t type, uint64_t* host_out, void* stream);
 
 /* Synchronise `stream`; return and clear the sticky device error
- * (DSR_ERR_OOM / DSR_ERR_RETRY_BUDGET) or DSR_OK. */
+ * (DSR_ERR_OOM / DSR_ERR_RETRY_BUDGET; in a -DDSR_DEBUG build also
+ * DSR_ERR_INVARIANT for an object access that failed its bounds check) or
+ * DSR_OK. */
 dsr_status dsr_poll_error(dsr_heap* h, void* stream);
 
 /* Quiescent audit (synchronising): hierarchy consistency of every bitmap

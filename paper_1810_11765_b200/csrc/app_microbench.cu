@@ -172,6 +172,12 @@ __device__ __forceinline__ void mb_construct(const DevHeap& h, uint32_t T, const
 #pragma unroll
   for (uint32_t k = 0; k < kMaxF; ++k) col[k] = k < nf ? h.types[T].col_off[k] : 0u;
   auto construct = [&](uint32_t b, uint32_t s, uint32_t i) {
+#ifdef DSR_DEBUG
+    if (b >= h.M || s >= h.types[T].cap) {
+      atomicOr(&h.ctrl[CTRL_ERR], (unsigned long long)ERRB_BOUNDS);
+      return;
+    }
+#endif
     const uint64_t t = mb_t(ts, nres, off0, off1, i);
     uint8_t* const obj = h.data + (size_t)b * h.block_bytes + 4u * s;
     const uint32_t* src = nullptr;
@@ -237,6 +243,14 @@ __device__ __forceinline__ void mb_construct(const DevHeap& h, uint32_t T, const
         q = g - sw[cur];
       }
       const uint32_t i = sw[96 + cur] + 4u * q;
+#ifdef DSR_DEBUG
+      // the quad lies in its chunk's run of reserved slots, inside the block
+      if (cur >= nqc || sw[32 + cur] >= h.M || sw[64 + cur] + 4u * q + 4u > h.types[T].cap ||
+          q >= (cur + 1 < nqc ? sw[cur + 1] : total) - sw[cur]) {
+        atomicOr(&h.ctrl[CTRL_ERR], (unsigned long long)ERRB_BOUNDS);
+        continue;
+      }
+#endif
       uint8_t* const p = h.data + (size_t)sw[32 + cur] * h.block_bytes + 4u * (sw[64 + cur] + 4u * q);
       const uint64_t t0 = mb_t(ts, nres, off0, off1, i);
       const uint32_t u = nres == 2 ? ((i & 1) ? 4u - (off1 - off0) : off1 - off0) : 4u;
@@ -284,6 +298,10 @@ __device__ __forceinline__ void mb_construct(const DevHeap& h, uint32_t T, const
     if ((mlo >> lane) & 1u) slots[__popc(mlo & lt)] = (uint8_t)lane;
     if ((mhi >> lane) & 1u) slots[__popc(mlo) + __popc(mhi & lt)] = (uint8_t)(lane + 32);
     __syncwarp();
+#ifdef DSR_DEBUG
+    for (uint32_t j = lane; j < cn; j += 32)
+      if (!((cm >> slots[j]) & 1ull)) atomicOr(&h.ctrl[CTRL_ERR], (unsigned long long)ERRB_BOUNDS);   // not reserved
+#endif
     for (uint32_t j = lane; j < cn; j += 32) construct(cb, slots[j], c0 + j);
     __syncwarp();
   }

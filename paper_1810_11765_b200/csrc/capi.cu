@@ -604,6 +604,7 @@ extern "C" dsr_status dsr_poll_error(dsr_heap* h, void* stream) {
   CUDA_TRY(cudaStreamSynchronize(st));
   if (e & ERRB_OOM) return DSR_ERR_OOM;
   if (e & ERRB_BUDGET) return DSR_ERR_RETRY_BUDGET;
+  if (e & ERRB_BOUNDS) return DSR_ERR_INVARIANT;
   return DSR_OK;
 }
 

@@ -45,7 +45,11 @@ struct DevType {
 // CTRL_RBEG + k: begin of the k-th type's range of R in a subtree do-all (k <= DSR_MAX_TYPES)
 // CTRL_WORK: dynamic work counter of persistent user kernels
 enum { CTRL_ERR = 0, CTRL_RCOUNT = 1, CTRL_SCRATCH = 2, CTRL_WORK = 3, CTRL_RBEG = 4, CTRL_STATS = 16, CTRL_AUDIT = 40 };
-enum { ERRB_OOM = 1, ERRB_BUDGET = 2 };
+// ERRB_BOUNDS: a debug build's bounds check failed (an object access outside
+// the heap's blocks / a type's slots or fields, dsr_poll_error -> DSR_ERR_INVARIANT)
+enum { ERRB_OOM = 1, ERRB_BUDGET = 2, ERRB_BOUNDS = 4 };
+// control-page words 480..511: where a debug build redirects an out-of-bounds access
+enum { CTRL_SINK = 480 };
 enum { ST_ALLOCS = 0, ST_FREES, ST_INITS, ST_BFREES, ST_ROLLBACKS, ST_INVFAIL, ST_RESRETRY, ST_OOM,
        ST_REQ, ST_FIND, ST_FINDFAIL, ST_RESZERO, ST_CYC_FIND, ST_CYC_SLOW, ST_CYC_RES, ST_CYC_REQ, ST_HINTZERO,
        ST_N };
@@ -215,8 +219,24 @@ __device__ __forceinline__ uint32_t h_bid(uint64_t h) { return (uint32_t)((h & 0
 __device__ __forceinline__ uint32_t h_type(uint64_t h) { return (uint32_t)(h >> 56) - 1u; }  // 0-based
 __device__ __forceinline__ bool h_is(uint64_t h, uint32_t T) { return (h >> 56) == (uint64_t)(T + 1); }
 
+// Debug builds (-DDSR_DEBUG): every object access through field_ptr is
+// bounds-checked -- type, field, block index and slot -- and an access that
+// fails is reported (ERRB_BOUNDS) and redirected to a sink in the control
+// page instead of touching memory outside the heap's blocks (the own-checks
+// replacement for compute-sanitizer memcheck, which this pool does not run).
+#ifdef DSR_DEBUG
+__device__ __forceinline__ bool dbg_obj_ok(const DevHeap& h, uint32_t T, uint32_t f, uint32_t bid, uint32_t slot) {
+  return T < h.ntypes && f < h.types[T].nfields && bid < h.M && slot < h.types[T].cap;
+}
+#endif
 template <class V>
 __device__ __forceinline__ V* field_ptr(const DevHeap& h, uint32_t T, uint32_t f, uint32_t bid, uint32_t slot) {
+#ifdef DSR_DEBUG
+  if (!dbg_obj_ok(h, T, f, bid, slot)) {
+    atomicOr(&h.ctrl[CTRL_ERR], (unsigned long long)ERRB_BOUNDS);
+    return reinterpret_cast<V*>(&h.ctrl[CTRL_SINK]);
+  }
+#endif
   // Listing 2: block + field_offset * capacity + slot * sizeof
   return reinterpret_cast<V*>(h.data + (size_t)bid * h.block_bytes + h.types[T].col_off[f]) + slot;
 }
@@ -943,6 +963,12 @@ __device__ __forceinline__ uint32_t dsr_new_warp(const DevHeap& h, uint32_t T, u
 template <bool RELEASE = true>
 __device__ __forceinline__ void dsr_destroy_mask(const DevHeap& h, uint32_t T, uint32_t bid, uint64_t bits) {
   if (bits == 0) return;
+#ifdef DSR_DEBUG
+  if (T >= h.ntypes || bid >= h.M || (bits & ~h.types[T].valid)) {    // a forged / corrupted handle
+    atomicOr(&h.ctrl[CTRL_ERR], (unsigned long long)ERRB_BOUNDS);
+    return;
+  }
+#endif
   const uint32_t lane = lane_id();
   const uint32_t act = __activemask();
   const uint64_t key = ((uint64_t)T << 32) | bid;

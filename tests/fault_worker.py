@@ -96,6 +96,64 @@ def double_destroy():
     return out
 
 
+def bounds():
+    """Small configurations of every workload on the debug build, whose
+    field_ptr and microbench constructor bounds-check every object access
+    (ERRB_BOUNDS -> DSR_ERR_INVARIANT): each heap's sticky error must stay
+    clear and each result must equal the oracle (the own-checks replacement for
+    compute-sanitizer memcheck, which this GPU pool does not run)."""
+    from oracle import oracle as O
+    from paper_1810_11765_b200 import inputs as I
+    from paper_1810_11765_b200.microbench import Microbench
+    from paper_1810_11765_b200.gol import GameOfLife
+    from paper_1810_11765_b200.wator import WaTor
+    from paper_1810_11765_b200.nbody import NBody
+    res = {}
+    # microbench: runs of whole blocks, tails, odd chunk starts, hole chunks; both allocation kernels
+    for bulk in (True, False):
+        for n1, n2 in ((20_000, 10_000), (3 * 3072 + 77, 4001), (1 << 18, 1 << 17)):
+            mb = Microbench(n1=n1, n2=n2, seed=3, bulk=bulk)
+            mb.step()
+            torch.cuda.synchronize()
+            ok = np.array_equal(mb.results(), O.microbench(3, n1, n2)[0]) and mb.heap.check_invariants() == 0
+            res[f"mb_{int(bulk)}_{n1}"] = [bool(ok), mb.heap.poll_error()]
+    a0 = I.gol_soup(64, 64, 0.3, 1)
+    for tiled in (False, "prepare", "all"):
+        g = GameOfLife(a0, tiled=tiled)
+        g.run(20)
+        res[f"gol_{tiled}"] = [bool(np.array_equal(g.alive(), O.life_dense(a0, 20))), g.heap.poll_error()]
+    k, e, n = I.wator_init(64, 64, seed=21)
+    w = WaTor(k, e, n, FB=6, SB=12, SS=6, seed=42)
+    w.run(20)
+    res["wator"] = [bool(np.array_equal(w.state()[0], O.wator_run(k, e, n, FB=6, SB=12, SS=6, seed=42, steps=20)[0])),
+                    w.heap.poll_error()]
+    st = I.nbody_init(1000, seed=7)
+    prm = dict(G=2e-9, dt=0.5, eps=0.01, R=0.02)
+    nb = NBody(st, merges=True, **prm)
+    nb.run(3)
+    want = O.nbody_run(st, merges=True, steps=3, **prm)
+    res["nbody"] = [bool(np.array_equal(nb.state()["alive"], want["alive"])), nb.heap.poll_error()]
+    return res
+
+
+def bounds_violation():
+    """The check itself fires: destroying a forged handle whose slot is beyond
+    its type's N_T (a padding slot) is reported and not executed."""
+    heap = dsr.Heap([[4], [4, 4, 4]], 1 << 22)             # type 1: N_T = 64 * 4 / 12 = 21
+    hs = torch.zeros(8, dtype=torch.int64, device="cuda")
+    heap.launch(dsr.K_LS_ALLOC, 8, dsr.LsArgs(hs.data_ptr(), 1, 1))
+    torch.cuda.synchronize()
+    out = {"good": heap.poll_error(), "cap": heap.cap[1]}
+    h0 = int(hs[0].item())
+    forged = torch.tensor([(h0 & ~0x3F) | 63], dtype=torch.int64, device="cuda")   # slot 63 >= N_T
+    heap.launch(dsr.K_LS_FREE, 1, dsr.LsArgs(forged.data_ptr(), 1, 1))
+    torch.cuda.synchronize()
+    out["forged"] = heap.poll_error()
+    out["live"] = heap.live_count(1)
+    out["audit"] = heap.check_invariants()
+    return out
+
+
 if __name__ == "__main__":
     what = sys.argv[1]
     res = {"build": dsr.lib().dsr_build_info().decode()}
@@ -103,4 +161,8 @@ if __name__ == "__main__":
         res.update(torture(int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5]), sys.argv[6] == "1"))
     elif what == "double_destroy":
         res.update(double_destroy())
+    elif what == "bounds":
+        res.update(bounds())
+    elif what == "bounds_violation":
+        res.update(bounds_violation())
     print(json.dumps(res), flush=True)

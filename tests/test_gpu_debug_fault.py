@@ -81,3 +81,26 @@ def test_debug_build_reports_double_destroy(libs):
     assert r["a_second"] == dsr.ERR_RETRY_BUDGET, r          # precondition of Alg. 7
     assert r["a_live"] == 63 and r["a_audit"] == 0, r          # the illegal destroy changed nothing
     assert r["b_second"] == dsr.ERR_RETRY_BUDGET, r          # bounded spin
+
+
+def test_bounds_checked_build_runs_every_workload_clean(libs):
+    """The debug build bounds-checks every object access (field_ptr, the
+    microbench constructor's quads and slot lists, destroy): small
+    configurations of every workload raise no report and equal the oracle."""
+    r = run_worker(libs["debug"], "bounds", timeout=900)
+    assert "sm_100a" in r.pop("build")
+    for name, (ok, poll) in r.items():
+        assert ok, name
+        assert poll == 0, (name, poll)
+
+
+def test_bounds_check_reports_a_forged_handle(libs):
+    """...and the check fires: destroying a forged handle (slot >= N_T) is
+    reported as DSR_ERR_INVARIANT and not executed (live count and the
+    quiescent audit unchanged)."""
+    from paper_1810_11765_b200 import dsr
+    r = run_worker(libs["debug"], "bounds_violation")
+    assert r["good"] == dsr.OK and r["cap"] == 21
+    assert r["forged"] == dsr.ERR_INVARIANT
+    assert r["live"] == 8
+    assert r["audit"] == 0
